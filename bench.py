@@ -1,0 +1,341 @@
+"""bench.py — SpMV GFLOP/s and HBM GB/s (% of roofline) of the searched operator graph.
+
+Default workload (N=1): BASELINE configs[1] = C2 `lap2d-2048`, the 5-point Laplacian on a
+2048x2048 grid (4,194,304 rows, 20,963,328 nnz, fp64), alpha=1, beta=0.  One step = one
+as_spmv call (the whole hot loop a5+a6; the plan a1-a4 and the search a7 run before the
+timed region, as in the paper, which times the generated SpMV program) with the
+inputs resident in HBM.  L2 is flushed (memset of 2 x L2 bytes) before every timed step,
+outside the timed events.
+
+Multi-GPU (torchrun, one rank per GPU): ROW_DIV bands with nnz-balanced cuts (reading A35),
+each rank plans/searches its own band; y all-gather over NCCL only with --allgather.
+`--impl reference` times the oracle (long-double CPU SpMV) on the host instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "SpMV GFLOP/s and achieved HBM GB/s (% of roofline) per matrix at 1/2/4/8 B200"
+C2_SEEDS = [
+    "DIA_DECOM(theta=0.5,max=8) { DIA; SET_RESOURCE(256) }",
+    "DIA_DECOM(theta=0.5,max=8) { DIA; SET_RESOURCE(512) }",
+    "COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED",
+    "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED",
+    "COMPRESS; BMTB_ROW_BLOCK(128); SHMEM_OFFSET_RED; GMEM_ATOM_RED",
+]
+
+
+def peaks():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, idx):
+        self.idx, self.samples, self.stop = idx, [], threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def load_config(name, int_mode=False):
+    if name == "c2":
+        return synth.c2_lap2d(2048), "lap2d-2048", C2_SEEDS
+    if name == "c1":
+        return synth.c1_uniform(int_mode=int_mode), "uniform-1k", [
+            "COMPRESS; BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; SET_RESOURCE(128); GMEM_ATOM_RED"]
+    if name == "c4":
+        coo, _ = synth.c4_blockdense()
+        return coo, "blockdense-8m", [
+            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }"]
+    if name == "c3":
+        return synth.c3_rmat(), "rmat-24", [
+            "BIN(t=[32,2048]) { COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED | COMPRESS; BMTB_NNZ_BLOCK(2048); SHMEM_OFFSET_RED; GMEM_ATOM_RED | COMPRESS; BMTB_NNZ_BLOCK(2048); SHMEM_TOTAL_RED; GMEM_ATOM_RED }"]
+    raise SystemExit(f"unknown config {name}")
+
+
+def csr_of(coo):
+    rp = np.zeros(coo.m + 1, np.int64)
+    np.add.at(rp, coo.row + 1, 1)
+    return np.cumsum(rp)
+
+
+def reference_arm(args, coo, wl):
+    """The oracle (long-double CSR SpMV, oracle/spmv_ref.c) on the host cores."""
+    from oracle import spmv as S
+    rp = csr_of(coo)
+    x, _ = synth.vectors(coo.n, coo.m, 2, coo.val.dtype)
+    cores = os.cpu_count() or 1
+    # bounded sample: the first rows covering ~1/8 of the nonzeros (C2: ~2.6M nnz) per step
+    frac_rows = max(1, coo.m // 8)
+    srp = rp[:frac_rows + 1]
+    nnz_s = int(srp[-1])
+    col, val = coo.col[:nnz_s], coo.val[:nnz_s].astype(np.float64)
+    for _ in range(max(1, args.warmup)):
+        S.spmv_csr(srp, col, val, x, nthreads=cores)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        S.spmv_csr(srp, col, val, x, nthreads=cores)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.mean(ts)
+    v = 2.0 * nnz_s / t / 1e9
+    sample = f"first {frac_rows} rows ({nnz_s} nnz) of {wl} per step, long double, {cores} threads"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64x", "data": "synthetic",
+            "config": {"workload": wl, "nnz": coo.nnz, "rows": coo.m},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def cpu_baseline(coo, wl, budget_s=10.0):
+    from oracle import spmv as S
+    rp = csr_of(coo)
+    x, _ = synth.vectors(coo.n, coo.m, 2, coo.val.dtype)
+    cores = os.cpu_count() or 1
+    col, val = coo.col, coo.val.astype(np.float64)
+    S.spmv_csr(rp, col, val, x, nthreads=cores)
+    n, t_tot = 0, 0.0
+    while t_tot < budget_s and n < 50:
+        t0 = time.perf_counter()
+        S.spmv_csr(rp, col, val, x, nthreads=cores)
+        t_tot += time.perf_counter() - t0
+        n += 1
+    return {"value": 2.0 * coo.nnz * n / t_tot / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} full passes over {wl} ({coo.nnz} nnz), long double, {cores} threads, {t_tot:.1f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--graph", default=None, help="skip the search and time this graph")
+    ap.add_argument("--search-budget", type=float, default=20.0)
+    ap.add_argument("--search-candidates", type=int, default=24)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--allgather", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no search/baseline/e2e)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if not args.profile else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    coo, wl, seeds = load_config(args.config)
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args, coo, wl)
+        return
+
+    import torch
+    import paper_2212_10432_b200 as asp
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    A_full = asp.Matrix.from_coo(coo.m, coo.n, coo.row, coo.col, coo.val)
+    cuts = A_full.row_cuts(world)
+    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    A = A_full if world == 1 else A_full.row_slice(r0, r1)
+    nnz_local = A.nnz
+    stream = torch.cuda.current_stream()
+
+    t_plan = time.perf_counter()
+    if args.graph:
+        P = asp.Plan(A, args.graph, device=local)
+        graph = str(asp.Graph(args.graph))
+        searched = False
+    elif args.profile:
+        P = asp.Plan(A, seeds[0], device=local)
+        graph = str(asp.Graph(seeds[0]))
+        searched = False
+    else:
+        P, graph = asp.search(A, device=local, seed=1, max_candidates=args.search_candidates,
+                              budget_seconds=args.search_budget, warmup=3, reps=10, seed_graphs=seeds,
+                              log_path=os.path.join(ROOT, "gpurun_out", f"search_{wl}_r{rank}.jsonl")
+                              if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else None)
+        searched = True
+    plan_s = time.perf_counter() - t_plan
+    info = P.info()
+    dt = coo.val.dtype
+    x, _ = synth.vectors(coo.n, coo.m, 2, dt)
+    dx = torch.from_numpy(x).cuda()
+    m_local = r1 - r0
+    dy = torch.zeros(m_local, dtype=torch.float64 if dt == np.float64 else torch.float32, device="cuda")
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = torch.empty(2 * l2, dtype=torch.uint8, device="cuda")
+
+    def step():
+        P.spmv(1.0, dx, 0.0, dy, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        for e0, e1 in evs:
+            if not args.no_flush:
+                flush.zero_()
+            e0.record(stream)
+            step()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        if args.allgather and dist:
+            # y all-gather (uneven bands): NCCL broadcasts of each rank's slice
+            y_full = torch.zeros(coo.m, dtype=dy.dtype, device="cuda")
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            y_full[r0:r1] = dy
+            for r in range(world):
+                dist.broadcast(y_full[int(cuts[r]):int(cuts[r + 1])], src=r)
+            g1.record(stream)
+            torch.cuda.synchronize()
+            gather_ms = g0.elapsed_time(g1)
+        else:
+            gather_ms = None
+    ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    t_ms = statistics.mean(ms)
+    if dist:
+        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        tot = torch.tensor([float(nnz_local)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tot)
+        nnz_total = int(tot.item())
+    else:
+        nnz_total = nnz_local
+    gflops = 2.0 * nnz_total / (t_ms * 1e-3) / 1e9
+    hbm, hbm_kind = peaks()
+    achieved_gbs = info["bytes_model"] / (t_ms * 1e-3) / 1e9
+    launches = int(info["n_launches"])
+
+    # e2e through the C-ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.profile:
+        xh = torch.from_numpy(x).pin_memory()
+        yh = torch.zeros(m_local, dtype=dy.dtype).pin_memory()
+        xn, yn = xh.numpy(), yh.numpy()
+        for _ in range(2):
+            P.spmv_host(1.0, xn, 0.0, yn, stream)
+        e2e_ms = []
+        for _ in range(max(3, args.steps // 3)):
+            if not args.no_flush:
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            P.spmv_host(1.0, xn, 0.0, yn, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms.append(e0.elapsed_time(e1))
+        tm = statistics.mean(e2e_ms)
+        if dist:
+            tt = torch.tensor([tm], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tm = float(tt.item())
+        sv = dx.element_size()
+        e2e = {"value": 2.0 * nnz_total / (tm * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": tm,
+               "h2d_bytes_per_step": int(coo.n * sv), "d2h_bytes_per_step": int(m_local * sv)}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
+    if os.path.exists(prof):
+        try:
+            tj = json.load(open(prof))
+            if tj.get("graph") == graph:
+                traffic = tj["dram_bytes_per_launch"]
+        except Exception:
+            pass
+    line = {
+        "metric": METRIC, "value": gflops, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64" if dt == np.float64 else "f32", "data": "synthetic",
+        "config": {"workload": wl, "rows": coo.m, "nnz": coo.nnz, "graph": graph, "searched": searched,
+                   "alpha": 1.0, "beta": 0.0, "l2": "flushed before every step" if not args.no_flush else "not flushed",
+                   "parallelism": f"row_div{world}", "plan_and_search_s": round(plan_s, 2),
+                   "kernels": info["kernels"], "bytes_model": info["bytes_model"], "bytes_floor": info["bytes_floor"]},
+        "hbm_gbs_model": achieved_gbs,
+        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved_gbs / hbm, "traffic": traffic, "peak_kind": hbm_kind,
+                     "frac_of_8tbs": achieved_gbs / 8000.0,
+                     "note": "achieved = plan bytes model per as_spmv / mean event time of the step"
+                             + (" (single launch)" if launches == 1 else f" ({launches} launches)")},
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if gather_ms is not None:
+        line["allgather_ms"] = gather_ms
+    if not args.no_cpu_baseline and not args.profile and world == 1:
+        line["cpu_baseline"] = cpu_baseline(coo, wl)
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/* as.h — C ABI of libalphasparse: the data-parallel hot path of AlphaSparse
+ * (arXiv 2212.10432) re-designed for NVIDIA B200 (sm_100a).
+ *
+ * The paper's statement of the problem: a sparse matrix comes in as Matrix Market / COO
+ * ("takes a sparse matrix stored in the Matrix Market file format as input", PAPER.md
+ * P:2; "AlphaSparse chooses the COO format as the universal source format"); an
+ * Operator Graph ("connecting operators in order", §IV-B) is executed on the
+ * Matrix Metadata Set (§V-A) into a format plus the SpMV kernel that reads it
+ * (§V-B, §V-C); the Search Engine runs candidate graphs on the device and
+ * keeps the fastest (§VI-A).  The operation is y = alpha*A*x + beta*y ("y=Ax";
+ * alpha/beta per BASELINE.json north_star, reading A1 in DESIGN.md).
+ *
+ * Conventions for every entry point
+ *   - returns as_status_t, never throws across the ABI; as_last_error() gives a message
+ *     (thread-local) for the last non-OK status;
+ *   - on a precondition failure nothing is launched and no output is written;
+ *   - device pointers are CUDA device memory of the plan's device; "stream" is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - index arrays in the API are int64, values are the plan dtype (AS_R32F = float,
+ *     AS_R64F = double); the device format uses int32 indices (all counts < 2^31,
+ *     checked: AS_ERR_PLAN_INFEASIBLE otherwise).
+ */
+#ifndef ALPHASPARSE_AS_H
+#define ALPHASPARSE_AS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  AS_OK = 0,
+  AS_ERR_INVALID_ARG = 1,      /* NULL / size / alignment / aliasing / dtype precondition */
+  AS_ERR_MALFORMED = 2,        /* Matrix Market header or entry line malformed */
+  AS_ERR_INDEX_OUT_OF_RANGE = 3,
+  AS_ERR_DUPLICATE = 4,        /* duplicate (row, col) triplet: reading A4, not summed */
+  AS_ERR_GRAPH_PARSE = 5,      /* graph text does not follow the DSL grammar */
+  AS_ERR_GRAPH_ILLEGAL = 6,    /* operator dependency rule R1..R11 violated (reading A16) */
+  AS_ERR_PLAN_INFEASIBLE = 7,  /* matrix-dependent check failed (P1..P4, cut ranges, no kernel) */
+  AS_ERR_OOM = 8,
+  AS_ERR_CUDA = 9,
+  AS_ERR_NO_FEASIBLE = 10,     /* as_search: no candidate could be planned */
+  AS_ERR_DTYPE = 11,
+  AS_ERR_NOT_FOUND = 12        /* as_plan_export: key not present in this plan */
+} as_status_t;
+
+typedef enum { AS_R32F = 0, AS_R64F = 1 } as_dtype_t;
+
+typedef struct as_matrix_s* as_matrix_t;
+typedef struct as_graph_s* as_graph_t;
+typedef struct as_plan_s* as_plan_t;
+
+/* Row statistics (§VII-C average row length nnz/n and row variance
+ * sum((len - nnz/n)^2)/n, population; "irregular" <=> variance > 100). */
+typedef struct {
+  int64_t m, n, nnz, max_row_len, min_row_len, empty_rows;
+  double avg_row_len, row_len_variance;
+  int irregular;
+} as_stats_t;
+
+/* Plan summary.  bytes_model = algorithmic HBM bytes of one as_spmv call under the plan's
+ * own traffic model (arrays read + x + y + extra passes) for beta == 0; bytes_model_beta
+ * for beta != 0; bytes_floor = nnz*(sv+4) + n*sv + m*sv (DESIGN.md §Bytes model). */
+typedef struct {
+  int64_t nnz_real, stored_slots, pads, n_parts, n_launches, prepass_rows;
+  double bytes_model, bytes_model_beta, bytes_floor;
+  char kernels[512]; /* ';'-separated kernel names in launch order */
+} as_plan_info_t;
+
+const char* as_last_error(void);
+const char* as_version(void);
+
+/* ---------------------------------------------------------------- a1: matrix (host)
+ * as_matrix_create: copies the triplets (caller may free on return).  row/col are
+ * index_base-based (0 or 1), any order; duplicates -> AS_ERR_DUPLICATE; out-of-range ->
+ * AS_ERR_INDEX_OUT_OF_RANGE.  Empty rows are accepted (reading A6).  val has dtype dt.
+ * m, n < 2^31. */
+as_status_t as_matrix_create(int64_t m, int64_t n, int64_t nnz, const int64_t* row,
+                             const int64_t* col, const void* val, as_dtype_t dt,
+                             int index_base, as_matrix_t* out);
+/* CSR ingest for very large inputs (0-based row_ptr[m+1] int64, col[nnz] int32, val[nnz]);
+ * columns must be strictly ascending within each row (checked). */
+as_status_t as_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_ptr,
+                                 const int32_t* col, const void* val, as_dtype_t dt,
+                                 as_matrix_t* out);
+/* Matrix Market 'matrix coordinate' real|integer|pattern, general|symmetric (reading A3). */
+as_status_t as_matrix_create_mtx(const char* path, as_dtype_t dt, as_matrix_t* out);
+as_status_t as_matrix_stats(as_matrix_t, as_stats_t* out);
+/* ROW_DIV band [r0, r1) as a new matrix with r1-r0 rows and the same n (global columns). */
+as_status_t as_matrix_row_slice(as_matrix_t, int64_t r0, int64_t r1, as_matrix_t* out);
+/* Host CSR view of the canonical matrix: row_ptr[m+1] int64, col[nnz] int64, val dtype. */
+as_status_t as_matrix_export_csr(as_matrix_t, int64_t* row_ptr, int64_t* col, void* val);
+void as_matrix_destroy(as_matrix_t);
+
+/* ---------------------------------------------------------------- graph
+ * Grammar (DESIGN.md §Graph DSL):
+ *   seq := op (';' op)* ;  op := NAME ['(' [arg (',' arg)*] ')'] ['{' seq ('|' seq)* '}']
+ * Validates the operator dependencies (no BMTB after BMW/BMT; full list
+ * R1..R11 = reading A16).  AS_ERR_GRAPH_PARSE | AS_ERR_GRAPH_ILLEGAL (message names the
+ * pre-order node id and the rule). */
+as_status_t as_graph_parse(const char* text, as_graph_t* out);
+/* Canonical one-line form; buf == NULL or *len too small -> *len = required bytes
+ * (incl. NUL) and AS_ERR_INVALID_ARG when buf != NULL. */
+as_status_t as_graph_print(as_graph_t, char* buf, size_t* len);
+void as_graph_destroy(as_graph_t);
+
+/* ---------------------------------------------------------------- a2-a4: plan
+ * Executes the graph on the Matrix Metadata Set (converting -> COMPRESS -> mapping ->
+ * implementing) and uploads the resulting device format to `device`
+ * (device = -1: host-only plan, usable for as_plan_export but not for as_spmv).
+ * Blocking.  The plan owns its device arrays and keeps no reference to the matrix.
+ * flags: AS_PLAN_KEEP_HOST keeps the logical metadata on the host for as_plan_export. */
+#define AS_PLAN_KEEP_HOST 1
+as_status_t as_plan(as_matrix_t, as_graph_t, int device, void* stream, as_plan_t* out);
+as_status_t as_plan_ex(as_matrix_t, as_graph_t, int device, void* stream, int flags,
+                       as_plan_t* out);
+as_status_t as_plan_info(as_plan_t, as_plan_info_t* out);
+/* Logical metadata array `key` (DESIGN.md §Export keys, e.g. "p0.bmt.bitmap"), copied to
+ * host_dst.  host_dst == NULL -> *bytes = size.  Needs a host-only plan or
+ * AS_PLAN_KEEP_HOST.  Index arrays are int64, bitmaps uint32, values the plan dtype. */
+as_status_t as_plan_export(as_plan_t, const char* key, void* host_dst, size_t* bytes);
+/* ';'-separated list of export keys present in this plan. */
+as_status_t as_plan_keys(as_plan_t, char* buf, size_t* len);
+void as_plan_destroy(as_plan_t);
+
+/* ---------------------------------------------------------------- a5-a6: SpMV
+ * y = alpha*A*x + beta*y.  x[n], y[m] device pointers of the plan's dtype and device,
+ * 16-byte aligned, non-aliasing; alpha/beta point to HOST scalars of the plan's dtype.
+ * beta == 0: y is write-only (NaN in y not propagated).  Asynchronous on `stream`;
+ * device faults surface as AS_ERR_CUDA at a later call. */
+as_status_t as_spmv(as_plan_t, const void* alpha, const void* x, const void* beta, void* y,
+                    void* stream);
+/* Same with HOST x[n] / y[m] (pinned or pageable): copies x (and y when beta != 0) to the
+ * plan's device scratch, runs as_spmv, copies y back; synchronous. */
+as_status_t as_spmv_host(as_plan_t, const void* alpha, const void* x_host, const void* beta,
+                         void* y_host, void* stream);
+
+/* ---------------------------------------------------------------- a7: search
+ * Random dependency-respecting graphs ("operators ... randomly chosen and connected
+ * behind"; P:369 step 1) over a coarse parameter grid (P:369 step 2), each planned and
+ * timed on the device (median of `reps` CUDA-event-timed calls after `warmup`, L2 flushed
+ * before each when flush_l2), keeping the fastest.  The seed graphs run first.  Stops at
+ * max_candidates or budget_seconds.  Returns the best plan and its canonical graph
+ * (size-query convention on best_graph/len).  log_path (optional): one JSON line per
+ * candidate. */
+typedef struct {
+  uint64_t seed;
+  int max_candidates;
+  double budget_seconds;
+  int warmup, reps, flush_l2;
+  const char* const* seed_graphs;
+  int n_seed_graphs;
+  const char* log_path;
+} as_search_cfg_t;
+as_status_t as_search(as_matrix_t, const as_search_cfg_t*, int device, void* stream,
+                      as_plan_t* best, char* best_graph, size_t* len);
+/* One random legal graph text for this matrix (the search's generator), for tests. */
+as_status_t as_random_graph(as_matrix_t, uint64_t seed, char* buf, size_t* len);
+
+/* ---------------------------------------------------------------- e: multi-GPU helpers
+ * nnz-balanced ROW_DIV cuts over `world` ranks (reading A35): cuts[world+1]. */
+as_status_t as_dist_row_cuts(as_matrix_t, int world, int64_t* cuts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ALPHASPARSE_AS_H */

@@ -62,9 +62,9 @@ class Csr:
 
 
 def _row_len(csr: Csr, st: State) -> np.ndarray:
-    cnt = np.add.reduceat(st.mask.astype(np.int64), csr.row_ptr[:-1]) if csr.row.shape[0] else np.zeros(csr.m, np.int64)
-    # reduceat returns the element at a for empty segments; fix those
-    cnt = np.where(np.diff(csr.row_ptr) == 0, 0, cnt)
+    """Number of entries of each branch row still present (empty rows count 0, A6)."""
+    cs = np.concatenate([[0], np.cumsum(st.mask.astype(np.int64))])
+    cnt = cs[csr.row_ptr[1:]] - cs[csr.row_ptr[:-1]]
     return cnt[st.rows]
 
 

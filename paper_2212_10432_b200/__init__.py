@@ -1,0 +1,311 @@
+"""AlphaSparse hot path on B200 (sm_100a): thin Python binding of libalphasparse.
+
+Argument marshalling only — every step of the path (ingest, graph validation, metadata
+building, device format, SpMV kernels, search) runs in the native library declared in
+include/as.h.  The binding fails loudly if the library is missing; there is no fallback.
+
+    A = Matrix.from_coo(m, n, row, col, val)           # a1 ingest (as_matrix_create)
+    g = Graph("COMPRESS; BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; GMEM_ATOM_RED")
+    P = Plan(A, g, device=0)                            # a2-a4 (as_plan)
+    P.spmv(alpha, x, beta, y)                           # a5-a6 (as_spmv), torch CUDA tensors
+    best, text = search(A, device=0, budget_seconds=20)  # a7 (as_search)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libalphasparse.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+_lib = ctypes.CDLL(LIB_PATH)
+
+AS_R32F, AS_R64F = 0, 1
+AS_PLAN_KEEP_HOST = 1
+STATUS = {0: "AS_OK", 1: "AS_ERR_INVALID_ARG", 2: "AS_ERR_MALFORMED", 3: "AS_ERR_INDEX_OUT_OF_RANGE",
+          4: "AS_ERR_DUPLICATE", 5: "AS_ERR_GRAPH_PARSE", 6: "AS_ERR_GRAPH_ILLEGAL", 7: "AS_ERR_PLAN_INFEASIBLE",
+          8: "AS_ERR_OOM", 9: "AS_ERR_CUDA", 10: "AS_ERR_NO_FEASIBLE", 11: "AS_ERR_DTYPE", 12: "AS_ERR_NOT_FOUND"}
+
+_vp, _i64, _i32, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+_P = ctypes.POINTER
+
+
+class AsStats(ctypes.Structure):
+    _fields_ = [("m", _i64), ("n", _i64), ("nnz", _i64), ("max_row_len", _i64), ("min_row_len", _i64),
+                ("empty_rows", _i64), ("avg_row_len", ctypes.c_double), ("row_len_variance", ctypes.c_double),
+                ("irregular", ctypes.c_int)]
+
+
+class AsPlanInfo(ctypes.Structure):
+    _fields_ = [("nnz_real", _i64), ("stored_slots", _i64), ("pads", _i64), ("n_parts", _i64),
+                ("n_launches", _i64), ("prepass_rows", _i64), ("bytes_model", ctypes.c_double),
+                ("bytes_model_beta", ctypes.c_double), ("bytes_floor", ctypes.c_double),
+                ("kernels", ctypes.c_char * 512)]
+
+
+class AsSearchCfg(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("max_candidates", ctypes.c_int), ("budget_seconds", ctypes.c_double),
+                ("warmup", ctypes.c_int), ("reps", ctypes.c_int), ("flush_l2", ctypes.c_int),
+                ("seed_graphs", _P(ctypes.c_char_p)), ("n_seed_graphs", ctypes.c_int), ("log_path", ctypes.c_char_p)]
+
+
+def _sig(name, args, res=ctypes.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_lib.as_last_error.restype = ctypes.c_char_p
+_lib.as_version.restype = ctypes.c_char_p
+_sig("as_matrix_create", [_i64, _i64, _i64, _vp, _vp, _vp, _i32, _i32, _P(_vp)])
+_sig("as_matrix_create_csr", [_i64, _i64, _vp, _vp, _vp, _i32, _P(_vp)])
+_sig("as_matrix_create_mtx", [ctypes.c_char_p, _i32, _P(_vp)])
+_sig("as_matrix_stats", [_vp, _P(AsStats)])
+_sig("as_matrix_row_slice", [_vp, _i64, _i64, _P(_vp)])
+_sig("as_matrix_export_csr", [_vp, _vp, _vp, _vp])
+_sig("as_matrix_destroy", [_vp], None)
+_sig("as_graph_parse", [ctypes.c_char_p, _P(_vp)])
+_sig("as_graph_print", [_vp, ctypes.c_char_p, _P(_sz)])
+_sig("as_graph_destroy", [_vp], None)
+_sig("as_plan", [_vp, _vp, _i32, _vp, _P(_vp)])
+_sig("as_plan_ex", [_vp, _vp, _i32, _vp, _i32, _P(_vp)])
+_sig("as_plan_info", [_vp, _P(AsPlanInfo)])
+_sig("as_plan_export", [_vp, ctypes.c_char_p, _vp, _P(_sz)])
+_sig("as_plan_keys", [_vp, ctypes.c_char_p, _P(_sz)])
+_sig("as_plan_destroy", [_vp], None)
+_sig("as_spmv", [_vp, _vp, _vp, _vp, _vp, _vp])
+_sig("as_spmv_host", [_vp, _vp, _vp, _vp, _vp, _vp])
+_sig("as_search", [_vp, _P(AsSearchCfg), _i32, _vp, _P(_vp), ctypes.c_char_p, _P(_sz)])
+_sig("as_random_graph", [_vp, ctypes.c_uint64, ctypes.c_char_p, _P(_sz)])
+_sig("as_dist_row_cuts", [_vp, _i32, _vp])
+
+EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create_csr", "as_matrix_create_mtx",
+            "as_matrix_stats", "as_matrix_row_slice", "as_matrix_export_csr", "as_matrix_destroy", "as_graph_parse",
+            "as_graph_print", "as_graph_destroy", "as_plan", "as_plan_ex", "as_plan_info", "as_plan_export",
+            "as_plan_keys", "as_plan_destroy", "as_spmv", "as_spmv_host", "as_search", "as_random_graph",
+            "as_dist_row_cuts"]
+
+
+class AsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = STATUS.get(status, str(status))
+
+
+def _ck(st):
+    if st:
+        raise AsError(st, _lib.as_last_error().decode())
+
+
+def _dt(dtype) -> int:
+    dtype = np.dtype(dtype)
+    if dtype == np.float64:
+        return AS_R64F
+    if dtype == np.float32:
+        return AS_R32F
+    raise AsError(11, f"unsupported dtype {dtype}")
+
+
+def _np_dt(code):
+    return np.float64 if code == AS_R64F else np.float32
+
+
+def _string(fn, *args) -> str:
+    n = _sz(0)
+    _ck(fn(*args, None, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value)
+    _ck(fn(*args, buf, ctypes.byref(n)))
+    return buf.value.decode()
+
+
+class Matrix:
+    """a1: host matrix (canonical CSR inside the library)."""
+
+    def __init__(self, handle, dtype):
+        self._h = _vp(handle)
+        self.dtype = dtype
+
+    @classmethod
+    def from_coo(cls, m, n, row, col, val, index_base=0):
+        row = np.ascontiguousarray(row, np.int64)
+        col = np.ascontiguousarray(col, np.int64)
+        val = np.ascontiguousarray(val)
+        h = _vp()
+        _ck(_lib.as_matrix_create(m, n, row.shape[0], row.ctypes.data, col.ctypes.data, val.ctypes.data,
+                                  _dt(val.dtype), index_base, ctypes.byref(h)))
+        return cls(h.value, val.dtype)
+
+    @classmethod
+    def from_csr(cls, m, n, row_ptr, col, val):
+        row_ptr = np.ascontiguousarray(row_ptr, np.int64)
+        col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val)
+        h = _vp()
+        _ck(_lib.as_matrix_create_csr(m, n, row_ptr.ctypes.data, col.ctypes.data, val.ctypes.data,
+                                      _dt(val.dtype), ctypes.byref(h)))
+        return cls(h.value, val.dtype)
+
+    @classmethod
+    def from_mtx(cls, path, dtype=np.float64):
+        h = _vp()
+        _ck(_lib.as_matrix_create_mtx(str(path).encode(), _dt(dtype), ctypes.byref(h)))
+        return cls(h.value, np.dtype(dtype))
+
+    def stats(self) -> dict:
+        s = AsStats()
+        _ck(_lib.as_matrix_stats(self._h, ctypes.byref(s)))
+        return {k: getattr(s, k) for k, _ in AsStats._fields_}
+
+    @property
+    def shape(self):
+        s = self.stats()
+        return s["m"], s["n"]
+
+    @property
+    def nnz(self):
+        return self.stats()["nnz"]
+
+    def row_slice(self, r0, r1) -> "Matrix":
+        h = _vp()
+        _ck(_lib.as_matrix_row_slice(self._h, r0, r1, ctypes.byref(h)))
+        return Matrix(h.value, self.dtype)
+
+    def export_csr(self):
+        s = self.stats()
+        rp = np.zeros(s["m"] + 1, np.int64)
+        col = np.zeros(s["nnz"], np.int64)
+        val = np.zeros(s["nnz"], self.dtype)
+        _ck(_lib.as_matrix_export_csr(self._h, rp.ctypes.data, col.ctypes.data, val.ctypes.data))
+        return rp, col, val
+
+    def row_cuts(self, world: int) -> np.ndarray:
+        cuts = np.zeros(world + 1, np.int64)
+        _ck(_lib.as_dist_row_cuts(self._h, world, cuts.ctypes.data))
+        return cuts
+
+    def random_graph(self, seed: int) -> str:
+        return _string(_lib.as_random_graph, self._h, ctypes.c_uint64(seed))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib:
+            _lib.as_matrix_destroy(self._h)
+            self._h = None
+
+
+class Graph:
+    """Operator Graph: parsed + dependency-validated (as_graph_parse)."""
+
+    def __init__(self, text: str):
+        h = _vp()
+        _ck(_lib.as_graph_parse(text.encode(), ctypes.byref(h)))
+        self._h = h
+
+    def __str__(self):
+        return _string(_lib.as_graph_print, self._h)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib:
+            _lib.as_graph_destroy(self._h)
+            self._h = None
+
+
+def _stream_handle(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _ptr(t):
+    return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
+
+
+class Plan:
+    """a2-a4: the graph executed on the Matrix Metadata Set into a device-resident format."""
+
+    def __init__(self, matrix: Matrix, graph, device: int = 0, stream=None, keep_host: bool = False, _handle=None):
+        self.dtype = np.dtype(matrix.dtype) if matrix is not None else None
+        self.device = device
+        if _handle is not None:
+            self._h = _vp(_handle)
+            return
+        if isinstance(graph, str):
+            graph = Graph(graph)
+        h = _vp()
+        s = 0 if device < 0 else _stream_handle(stream)
+        _ck(_lib.as_plan_ex(matrix._h, graph._h, device, s, AS_PLAN_KEEP_HOST if keep_host else 0, ctypes.byref(h)))
+        self._h = h
+
+    def info(self) -> dict:
+        i = AsPlanInfo()
+        _ck(_lib.as_plan_info(self._h, ctypes.byref(i)))
+        d = {k: getattr(i, k) for k, _ in AsPlanInfo._fields_}
+        d["kernels"] = i.kernels.decode()
+        return d
+
+    def keys(self):
+        return _string(_lib.as_plan_keys, self._h).split(";")
+
+    def export(self, key: str) -> np.ndarray:
+        n = _sz(0)
+        _ck(_lib.as_plan_export(self._h, key.encode(), None, ctypes.byref(n)))
+        if key.endswith("val"):
+            dt = self.dtype
+        elif key.endswith("bitmap"):
+            dt = np.uint32
+        else:
+            dt = np.int64
+        out = np.zeros(n.value // np.dtype(dt).itemsize, dt)
+        _ck(_lib.as_plan_export(self._h, key.encode(), out.ctypes.data if out.size else None, ctypes.byref(n)))
+        return out
+
+    def _scalars(self, alpha, beta):
+        if self.dtype == np.float64:
+            return ctypes.c_double(alpha), ctypes.c_double(beta)
+        return ctypes.c_float(alpha), ctypes.c_float(beta)
+
+    def spmv(self, alpha, x, beta, y, stream=None):
+        """y = alpha*A*x + beta*y on device tensors (asynchronous on `stream`)."""
+        a, b = self._scalars(alpha, beta)
+        _ck(_lib.as_spmv(self._h, ctypes.byref(a), _ptr(x), ctypes.byref(b), _ptr(y), _stream_handle(stream)))
+
+    def spmv_host(self, alpha, x: np.ndarray, beta, y: np.ndarray, stream=None):
+        """Same with host arrays (copies inside; synchronous)."""
+        a, b = self._scalars(alpha, beta)
+        _ck(_lib.as_spmv_host(self._h, ctypes.byref(a), x.ctypes.data, ctypes.byref(b), y.ctypes.data,
+                              _stream_handle(stream)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib:
+            _lib.as_plan_destroy(self._h)
+            self._h = None
+
+
+def search(matrix: Matrix, device: int = 0, stream=None, seed: int = 1, max_candidates: int = 32,
+           budget_seconds: float = 30.0, warmup: int = 3, reps: int = 10, flush_l2: bool = True,
+           seed_graphs=(), log_path: str | None = None):
+    """a7: time random legal graphs on the device, keep the fastest -> (Plan, canonical graph)."""
+    arr = (ctypes.c_char_p * max(1, len(seed_graphs)))(*[g.encode() for g in seed_graphs])
+    cfg = AsSearchCfg(seed, max_candidates, budget_seconds, warmup, reps, int(flush_l2), arr, len(seed_graphs),
+                      log_path.encode() if log_path else None)
+    h = _vp()
+    n = _sz(4096)
+    buf = ctypes.create_string_buffer(4096)
+    _ck(_lib.as_search(matrix._h, ctypes.byref(cfg), device, _stream_handle(stream), ctypes.byref(h), buf,
+                       ctypes.byref(n)))
+    if n.value > 4096:
+        text = None
+    else:
+        text = buf.value.decode()
+    p = Plan(matrix, None, device, _handle=h.value)
+    return p, text
+
+
+def version() -> str:
+    return _lib.as_version().decode()

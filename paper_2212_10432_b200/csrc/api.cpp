@@ -1,0 +1,365 @@
+// C-ABI entry points (include/as.h).  Every call converts internal exceptions to statuses.
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "internal.h"
+#include "plan.h"
+
+namespace as {
+Matrix matrix_from_coo(int64_t, int64_t, int64_t, const int64_t*, const int64_t*, const void*, as_dtype_t, int);
+Matrix matrix_from_csr(int64_t, int64_t, const int64_t*, const int32_t*, const void*, as_dtype_t);
+Matrix matrix_from_mtx(const char*, as_dtype_t);
+as_stats_t matrix_stats(const Matrix&);
+Matrix matrix_row_slice(const Matrix&, int64_t, int64_t);
+as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device, void* stream, as_plan_t* best,
+                        char* best_graph, size_t* len);
+
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+template <class F>
+as_status_t guard(F f) {
+  try {
+    f();
+    return AS_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host out of memory");
+    return AS_ERR_OOM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return AS_ERR_INVALID_ARG;
+  }
+}
+
+as_status_t copy_string(const std::string& s, char* buf, size_t* len) {
+  if (!len) {
+    set_last_error("len is NULL");
+    return AS_ERR_INVALID_ARG;
+  }
+  size_t need = s.size() + 1;
+  if (!buf || *len < need) {
+    bool had = buf != nullptr;
+    *len = need;
+    if (had) {
+      set_last_error("buffer too small");
+      return AS_ERR_INVALID_ARG;
+    }
+    return AS_OK;
+  }
+  std::memcpy(buf, s.c_str(), need);
+  *len = need;
+  return AS_OK;
+}
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(AS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Builds the plan object; device < 0 -> host-only.
+Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int device, void* stream, int flags) {
+  auto* P = new Plan();
+  try {
+    P->dt = A.dt;
+    P->m = A.m;
+    P->n = A.n;
+    P->nnz_real = A.nnz();
+    P->canon = canon;
+    P->host = build_plan(A, g);
+    P->device = device;
+    if (device >= 0) {
+      int cur = 0;
+      check_cuda(cudaGetDevice(&cur), "cudaGetDevice");
+      check_cuda(cudaSetDevice(device), "cudaSetDevice");
+      try {
+        P->upload((cudaStream_t)stream);
+      } catch (...) {
+        cudaSetDevice(cur);
+        throw;
+      }
+      cudaSetDevice(cur);
+    }
+    P->compute_model();
+    auto& info = P->info;
+    info.nnz_real = A.nnz();
+    info.n_parts = (int64_t)P->host.parts.size();
+    info.prepass_rows = (int64_t)P->host.prepass.size();
+    info.n_launches = (int64_t)P->host.launch_order.size() + (P->host.prepass.empty() ? 0 : 1);
+    int64_t slots = 0;
+    for (auto& p : P->host.parts) {
+      if (p.kind == "csr") slots += p.pad ? (int64_t)p.pad_val.size() : (int64_t)p.val.size();
+      else if (p.kind == "dia") slots += (int64_t)p.dia_val.size();
+      else slots += (int64_t)p.tile_val.size();
+    }
+    info.stored_slots = slots;
+    info.pads = slots - A.nnz();
+    std::string k;
+    if (!P->host.prepass.empty()) k = "k_prepass";
+    for (int64_t pi : P->host.launch_order) {
+      if (!k.empty()) k += ";";
+      k += P->host.parts[pi].fam_name;
+    }
+    std::strncpy(info.kernels, k.c_str(), sizeof(info.kernels) - 1);
+    P->host_kept = device < 0 || (flags & AS_PLAN_KEEP_HOST);
+    if (!P->host_kept) P->host = HostPlan();
+    return P;
+  } catch (...) {
+    delete P;
+    throw;
+  }
+}
+
+}  // namespace as
+
+using namespace as;
+
+extern "C" {
+
+const char* as_last_error(void) { return g_last_error.c_str(); }
+const char* as_version(void) { return "alphasparse-b200 0.1 (sm_100a)"; }
+
+as_status_t as_matrix_create(int64_t m, int64_t n, int64_t nnz, const int64_t* row, const int64_t* col,
+                             const void* val, as_dtype_t dt, int index_base, as_matrix_t* out) {
+  return guard([&] {
+    if (!out) fail(AS_ERR_INVALID_ARG, "out is NULL");
+    auto* M = new as_matrix_s();
+    try {
+      M->A = matrix_from_coo(m, n, nnz, row, col, val, dt, index_base);
+    } catch (...) {
+      delete M;
+      throw;
+    }
+    *out = M;
+  });
+}
+
+as_status_t as_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const void* val,
+                                 as_dtype_t dt, as_matrix_t* out) {
+  return guard([&] {
+    if (!out) fail(AS_ERR_INVALID_ARG, "out is NULL");
+    auto* M = new as_matrix_s();
+    try {
+      M->A = matrix_from_csr(m, n, row_ptr, col, val, dt);
+    } catch (...) {
+      delete M;
+      throw;
+    }
+    *out = M;
+  });
+}
+
+as_status_t as_matrix_create_mtx(const char* path, as_dtype_t dt, as_matrix_t* out) {
+  return guard([&] {
+    if (!out || !path) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    auto* M = new as_matrix_s();
+    try {
+      M->A = matrix_from_mtx(path, dt);
+    } catch (...) {
+      delete M;
+      throw;
+    }
+    *out = M;
+  });
+}
+
+as_status_t as_matrix_stats(as_matrix_t M, as_stats_t* out) {
+  return guard([&] {
+    if (!M || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    *out = matrix_stats(M->A);
+  });
+}
+
+as_status_t as_matrix_row_slice(as_matrix_t M, int64_t r0, int64_t r1, as_matrix_t* out) {
+  return guard([&] {
+    if (!M || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    auto* S = new as_matrix_s();
+    try {
+      S->A = matrix_row_slice(M->A, r0, r1);
+    } catch (...) {
+      delete S;
+      throw;
+    }
+    *out = S;
+  });
+}
+
+as_status_t as_matrix_export_csr(as_matrix_t M, int64_t* row_ptr, int64_t* col, void* val) {
+  return guard([&] {
+    if (!M) fail(AS_ERR_INVALID_ARG, "NULL matrix");
+    const Matrix& A = M->A;
+    if (row_ptr) std::memcpy(row_ptr, A.row_ptr.data(), A.row_ptr.size() * 8);
+    if (col)
+      for (int64_t i = 0; i < A.nnz(); ++i) col[i] = A.col[i];
+    if (val) {
+      if (A.dt == AS_R64F) std::memcpy(val, A.val.data(), A.val.size() * 8);
+      else
+        for (int64_t i = 0; i < A.nnz(); ++i) ((float*)val)[i] = (float)A.val[i];
+    }
+  });
+}
+
+void as_matrix_destroy(as_matrix_t M) { delete M; }
+
+as_status_t as_graph_parse(const char* text, as_graph_t* out) {
+  return guard([&] {
+    if (!text || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    auto* G = new as_graph_s();
+    try {
+      G->g = parse_graph(text);
+      G->canon = print_graph(G->g);
+    } catch (...) {
+      delete G;
+      throw;
+    }
+    *out = G;
+  });
+}
+
+as_status_t as_graph_print(as_graph_t G, char* buf, size_t* len) {
+  if (!G) {
+    set_last_error("NULL graph");
+    return AS_ERR_INVALID_ARG;
+  }
+  return copy_string(G->canon, buf, len);
+}
+
+void as_graph_destroy(as_graph_t G) { delete G; }
+
+as_status_t as_plan_ex(as_matrix_t M, as_graph_t G, int device, void* stream, int flags, as_plan_t* out) {
+  return guard([&] {
+    if (!M || !G || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    Plan* P = make_plan(M->A, G->g, G->canon, device, stream, flags);
+    auto* h = new as_plan_s();
+    h->P.reset(P);
+    *out = h;
+  });
+}
+
+as_status_t as_plan(as_matrix_t M, as_graph_t G, int device, void* stream, as_plan_t* out) {
+  return as_plan_ex(M, G, device, stream, 0, out);
+}
+
+as_status_t as_plan_info(as_plan_t P, as_plan_info_t* out) {
+  return guard([&] {
+    if (!P || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    *out = P->P->info;
+  });
+}
+
+as_status_t as_plan_export(as_plan_t P, const char* key, void* host_dst, size_t* bytes) {
+  return guard([&] {
+    if (!P || !key || !bytes) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    if (!P->P->host_kept) fail(AS_ERR_INVALID_ARG, "plan built without AS_PLAN_KEEP_HOST");
+    size_t need = 0;
+    if (!export_key(P->P->host, key, nullptr, &need)) fail(AS_ERR_NOT_FOUND, std::string("no export key ") + key);
+    if (host_dst && *bytes < need) fail(AS_ERR_INVALID_ARG, "destination too small");
+    if (host_dst) export_key(P->P->host, key, host_dst, &need);
+    *bytes = need;
+  });
+}
+
+as_status_t as_plan_keys(as_plan_t P, char* buf, size_t* len) {
+  if (!P || !P->P->host_kept) {
+    set_last_error("plan built without AS_PLAN_KEEP_HOST");
+    return AS_ERR_INVALID_ARG;
+  }
+  std::string s;
+  for (auto& k : export_keys(P->P->host)) {
+    if (!s.empty()) s += ";";
+    s += k;
+  }
+  return copy_string(s, buf, len);
+}
+
+void as_plan_destroy(as_plan_t P) { delete P; }
+
+as_status_t as_spmv(as_plan_t h, const void* alpha, const void* x, const void* beta, void* y, void* stream) {
+  return guard([&] {
+    if (!h || !alpha || !beta) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    Plan& P = *h->P;
+    if (P.device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan cannot run as_spmv");
+    if ((P.n > 0 && !x) || (P.m > 0 && !y)) fail(AS_ERR_INVALID_ARG, "NULL x or y");
+    if (((uintptr_t)x | (uintptr_t)y) & 15) fail(AS_ERR_INVALID_ARG, "x and y must be 16-byte aligned");
+    const size_t sv = P.dt == AS_R64F ? 8 : 4;
+    if (x && y && (const char*)x < (const char*)y + P.m * sv && (const char*)y < (const char*)x + P.n * sv)
+      fail(AS_ERR_INVALID_ARG, "x and y alias");
+    double a = P.dt == AS_R64F ? *(const double*)alpha : (double)*(const float*)alpha;
+    double b = P.dt == AS_R64F ? *(const double*)beta : (double)*(const float*)beta;
+    cudaError_t prior = cudaGetLastError();
+    if (prior != cudaSuccess) fail(AS_ERR_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(prior));
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != P.device) cudaSetDevice(P.device);
+    int err = 0;
+    if (P.n_prepass) err = launch_prepass(P.d_prepass, P.n_prepass, b, y, P.dt == AS_R64F ? 1 : 0, stream);
+    for (size_t i = 0; i < P.launches.size() && !err; ++i) {
+      DevPart d = P.launches[i];
+      d.alpha = a;
+      d.beta = b;
+      err = launch_part(d, x, y, stream);
+    }
+    if (cur != P.device) cudaSetDevice(cur);
+    if (err) fail(AS_ERR_CUDA, std::string("launch: ") + cudaGetErrorString((cudaError_t)err));
+  });
+}
+
+as_status_t as_spmv_host(as_plan_t h, const void* alpha, const void* x_host, const void* beta, void* y_host,
+                         void* stream) {
+  return guard([&] {
+    if (!h || !alpha || !beta) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    Plan& P = *h->P;
+    if (P.device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan");
+    const size_t sv = P.dt == AS_R64F ? 8 : 4;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    cudaSetDevice(P.device);
+    if (!P.d_x) check_cuda(cudaMalloc(&P.d_x, std::max<size_t>(16, P.n * sv)), "cudaMalloc x");
+    if (!P.d_y) check_cuda(cudaMalloc(&P.d_y, std::max<size_t>(16, P.m * sv)), "cudaMalloc y");
+    cudaStream_t s = (cudaStream_t)stream;
+    double b = P.dt == AS_R64F ? *(const double*)beta : (double)*(const float*)beta;
+    check_cuda(cudaMemcpyAsync(P.d_x, x_host, P.n * sv, cudaMemcpyHostToDevice, s), "H2D x");
+    if (b != 0.0) check_cuda(cudaMemcpyAsync(P.d_y, y_host, P.m * sv, cudaMemcpyHostToDevice, s), "H2D y");
+    cudaSetDevice(cur);
+    as_status_t st = as_spmv(h, alpha, P.d_x, beta, P.d_y, stream);
+    if (st != AS_OK) fail(st, g_last_error);
+    cudaSetDevice(P.device);
+    check_cuda(cudaMemcpyAsync(y_host, P.d_y, P.m * sv, cudaMemcpyDeviceToHost, s), "D2H y");
+    check_cuda(cudaStreamSynchronize(s), "sync");
+    cudaSetDevice(cur);
+  });
+}
+
+as_status_t as_search(as_matrix_t M, const as_search_cfg_t* cfg, int device, void* stream, as_plan_t* best,
+                      char* best_graph, size_t* len) {
+  as_status_t st = AS_OK;
+  as_status_t g = guard([&] {
+    if (!M || !cfg || !best) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    st = search_impl(M->A, cfg, device, stream, best, best_graph, len);
+  });
+  return g != AS_OK ? g : st;
+}
+
+as_status_t as_random_graph(as_matrix_t M, uint64_t seed, char* buf, size_t* len) {
+  std::string s;
+  as_status_t st = guard([&] {
+    if (!M) fail(AS_ERR_INVALID_ARG, "NULL matrix");
+    s = random_graph(M->A, seed);
+  });
+  if (st != AS_OK) return st;
+  return copy_string(s, buf, len);
+}
+
+as_status_t as_dist_row_cuts(as_matrix_t M, int world, int64_t* cuts) {
+  return guard([&] {
+    if (!M || !cuts) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    auto c = row_cuts(M->A.row_ptr, world);
+    std::memcpy(cuts, c.data(), c.size() * 8);
+  });
+}
+
+}  // extern "C"

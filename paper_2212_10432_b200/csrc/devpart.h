@@ -1,0 +1,92 @@
+// Device-resident format of one plan part + its launch geometry (POD, passed by value to
+// the sm_100a kernels).  Pointers are device pointers; a NULL index array means the array
+// is linear by construction and is computed instead of loaded (reading A17, the paper's
+// Model-Driven Format Compression example "row_offset = 64*bid").
+#pragma once
+#include <cstdint>
+
+namespace as {
+
+enum Fam {
+  FAM_NONE = 0,
+  FAM_THREAD_ROW,    // BMT_ROW_BLOCK (+ROW parents, +BMT_PAD) + THREAD_TOTAL|THREAD_BITMAP_RED_G
+  FAM_NNZ_THREAD,    // BMT_NNZ_BLOCK + THREAD_BITMAP_RED_G (row straddlers -> atomics, "_G")
+  FAM_NNZ_WARP,      // BMW_* + BMT_NNZ_BLOCK + THREAD_BITMAP_RED_G + WARP_SEG_ADD_RED|WARP_BITMAP_RED
+  FAM_WARP_ROW,      // BMW_* (single-row) [+BMT_NNZ+THREAD_TOTAL] + WARP_TOTAL_RED
+  FAM_BLOCK_TOTAL,   // BMTB_* (single-row) + SHMEM_TOTAL_RED
+  FAM_BLOCK_OFFSET,  // BMTB_* + SHMEM_OFFSET_RED (CSR-stream)
+  FAM_DIA,           // DIA part of DIA_DECOM
+  FAM_DENSE          // DENSE part of DENSE_DECOM
+};
+
+constexpr int kMaxDiags = 64;
+
+struct DevPart {
+  int fam = FAM_NONE;
+  int dtype = 1;  // AS_R32F = 0, AS_R64F = 1
+  int mode = 0;   // 0 STORE (y = a*s + b*y), 1 ADD (y += a*s); atomics always add
+  int variant = 0;
+  int64_t m_p = 0, nnz_p = 0, n = 0;
+  // COMPRESS output
+  const int32_t* origin = nullptr;  // NULL -> origin_base + row
+  int64_t origin_base = 0;
+  const int32_t* row_ptr = nullptr;
+  const int32_t* col = nullptr;
+  const void* val = nullptr;
+  // BMT level
+  int64_t n_bmt = 0;
+  int64_t k = 0;                          // BMT_NNZ size
+  int64_t s = 0;                          // BMT_ROW size
+  const int32_t* bmt_start = nullptr;     // NNZ BMTs: NULL -> t*k
+  const int32_t* bmt_row_ptr = nullptr;   // ROW BMTs: NULL -> min(t*s, m_p)
+  const int32_t* bmt_first_row = nullptr;
+  const uint32_t* bitmap = nullptr;
+  int bm_words = 0;
+  // BMW level
+  int64_t n_bmw = 0;
+  const int32_t* bmw_bmt_ptr = nullptr;   // NNZ_WARP: BMT range per BMW; NULL -> bmts_per_bmw
+  int64_t bmts_per_bmw = 0;
+  const int32_t* bmw_start = nullptr;     // WARP_ROW: nz start per BMW
+  const int32_t* bmw_first_row = nullptr; // WARP_ROW: NULL -> w
+  int bmw_all_excl = 0;
+  // BMTB level
+  int64_t n_bmtb = 0;
+  const int32_t* bmtb_start = nullptr;    // NULL -> b*k1
+  int64_t k1 = 0;
+  const int32_t* bmtb_first_row = nullptr;
+  int64_t max_block_nnz = 0;
+  // BMT_PAD (slot-major interleaved)
+  int pad = 0, vec = 1;
+  int64_t n_grp = 0, grp_regular = 0;     // BMTs per group if regular, else 0
+  const int32_t* grp_first_bmt = nullptr; // n_grp + 1
+  const int64_t* grp_base = nullptr;      // n_grp slot offsets
+  const int32_t* grp_width = nullptr;     // n_grp
+  const int32_t* pad_col = nullptr;
+  const void* pad_val = nullptr;
+  // DIA
+  int D = 0;
+  int64_t r0 = 0, mb = 0, dia_stride = 0;
+  int32_t dia_off[kMaxDiags] = {0};
+  const void* dia_val = nullptr;
+  // DENSE
+  int64_t b = 0, n_tile_rows = 0, row_lo = 0, row_hi = 0;
+  const int32_t* tile_row_id = nullptr;
+  const int32_t* tile_row_ptr = nullptr;
+  const int32_t* tile_col = nullptr;
+  const void* tile_val = nullptr;
+  // launch
+  int tpb = 256, grid = 0;
+  size_t smem = 0;
+  // scalars (filled per call)
+  double alpha = 1.0, beta = 0.0;
+};
+
+// kernels.cu
+int launch_part(const DevPart& p, const void* x, void* y, void* stream);      // returns cudaError_t
+int launch_prepass(const int32_t* rows, int64_t n, double beta, void* y, int dtype, void* stream);
+int launch_scale_all(int64_t m, double beta, void* y, int dtype, void* stream);
+int prepare_part(DevPart& p);  // per-kernel attributes (smem opt-in); returns cudaError_t
+const char* fam_kernel_name(const DevPart& p);
+int device_max_smem_optin(int device);
+
+}  // namespace as

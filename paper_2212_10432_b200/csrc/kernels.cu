@@ -1,0 +1,762 @@
+// sm_100a SpMV kernel family: one kernel per (mapping level x reduction strategy) class of
+// the implementing stage (§IV-A), plus the DIA / dense-tile kernels implied by
+// DIA_DECOM / DENSE_DECOM (P:21 draft) and the beta pre-pass of the writer rule (A22).
+//
+// Every kernel computes, for its rows, acc = sum a_ij * x_j in double (fp64 accumulation
+// for fp32 data too, reading A2) and writes
+//   exclusive rows:  STORE y = alpha*acc + beta*y   |  ADD  y += alpha*acc
+//   shared rows:     atomicAdd(y, alpha*partial)     (GMEM_ATOM_RED)
+// The path is HBM-bound (0.12-0.25 flop/B), so the kernels are written for bytes in flight:
+// streaming loads of values/indices through the non-coherent path with an evict-first L2
+// hint (the matrix is touched once per call), gathers of x through L1/L2, and grid-stride
+// loops so any SET_RESOURCE grid is legal.  No tensor cores: with one vector every dense
+// block is a GEMV (2 flops per value loaded), not a contraction.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "devpart.h"
+
+namespace as {
+
+namespace {
+
+// ---------------------------------------------------------------- load helpers
+// Matrix streams: read once per SpMV -> L1::no_allocate + an L2 evict_first cache policy.
+__device__ __forceinline__ uint64_t pol_ef() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+#define AS_LD1(T, PT, C, p)                                                                            \
+  T v;                                                                                                 \
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint." PT " %0, [%1], %2;" : "=" C(v) : "l"(p), \
+               "l"(pol_ef()));                                                                         \
+  return v;
+__device__ __forceinline__ double ld_stream(const double* p) { AS_LD1(double, "f64", "d", p) }
+__device__ __forceinline__ float ld_stream(const float* p) { AS_LD1(float, "f32", "f", p) }
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) { AS_LD1(int32_t, "s32", "r", p) }
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p), "l"(pol_ef()));
+  return v;
+}
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol_ef()));
+  return v;
+}
+__device__ __forceinline__ float2 ld_stream2(const float* p) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+               : "=f"(v.x), "=f"(v.y)
+               : "l"(p), "l"(pol_ef()));
+  return v;
+}
+__device__ __forceinline__ int2 ld_stream_i2(const int32_t* p) {
+  int2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p), "l"(pol_ef()));
+  return v;
+}
+__device__ __forceinline__ int4 ld_stream_i4(const int32_t* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol_ef()));
+  return v;
+}
+// x gathers: reused across rows -> default caching through L1 (non-coherent path).
+template <class V>
+__device__ __forceinline__ double ldx(const V* x, int64_t c) {
+  return (double)__ldg(x + c);
+}
+// metadata: small, reused by neighbours -> plain non-coherent load
+__device__ __forceinline__ int32_t ldm(const int32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ldm(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ int64_t ldm(const int64_t* p) { return __ldg(p); }
+
+// ---------------------------------------------------------------- writers
+__device__ __forceinline__ int64_t out_row(const DevPart& p, int64_t r) {
+  return p.origin ? (int64_t)ldm(p.origin + r) : p.origin_base + r;
+}
+template <class V>
+__device__ __forceinline__ void write_excl(const DevPart& p, V* y, int64_t r, double acc) {
+  int64_t g = out_row(p, r);
+  if (p.mode == 0) {
+    double v = p.alpha * acc;
+    if (p.beta != 0.0) v += p.beta * (double)y[g];
+    y[g] = (V)v;
+  } else {
+    y[g] = (V)((double)y[g] + p.alpha * acc);
+  }
+}
+template <class V>
+__device__ __forceinline__ void write_atom(const DevPart& p, V* y, int64_t r, double acc) {
+  atomicAdd(y + out_row(p, r), (V)(p.alpha * acc));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ int64_t gthreads() { return (int64_t)gridDim.x * blockDim.x; }
+
+// =====================================================================================
+// FAM_THREAD_ROW: BMT_ROW_BLOCK(s) [+ROW parents] + THREAD_TOTAL / THREAD_BITMAP_RED_G.
+// CSR-Scalar when unpadded; ELL / SELL-P (slot-major interleaved) with
+// BMT_PAD: consecutive threads read consecutive vec-chunks -> fully coalesced 128-bit loads.
+// =====================================================================================
+template <class V>
+__global__ void __launch_bounds__(1024) k_thread_row(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  const V* val = (const V*)p.val;
+  for (int64_t t = gtid(); t < p.n_bmt; t += gthreads()) {
+    int64_t r0 = p.bmt_row_ptr ? ldm(p.bmt_row_ptr + t) : t * p.s;
+    int64_t r1 = p.bmt_row_ptr ? ldm(p.bmt_row_ptr + t + 1) : min((t + 1) * p.s, p.m_p);
+    for (int64_t r = r0; r < r1; ++r) {
+      int64_t a = ldm(p.row_ptr + r), e = ldm(p.row_ptr + r + 1);
+      double acc0 = 0.0, acc1 = 0.0;
+      int64_t i = a;
+      for (; i + 1 < e; i += 2) {
+        int32_t c0 = ld_stream(p.col + i), c1 = ld_stream(p.col + i + 1);
+        double v0 = (double)ld_stream(val + i), v1 = (double)ld_stream(val + i + 1);
+        acc0 += v0 * ldx(x, c0);
+        acc1 += v1 * ldx(x, c1);
+      }
+      if (i < e) acc0 += (double)ld_stream(val + i) * ldx(x, ld_stream(p.col + i));
+      write_excl(p, y, r, acc0 + acc1);
+    }
+  }
+}
+
+template <class V, int VEC>
+struct PadLoad;
+template <>
+struct PadLoad<double, 2> {
+  static __device__ __forceinline__ void ld(const double* v, const int32_t* c, double* vo, int32_t* co) {
+    double2 a = ld_stream2(v);
+    int2 b = ld_stream_i2(c);
+    vo[0] = a.x;
+    vo[1] = a.y;
+    co[0] = b.x;
+    co[1] = b.y;
+  }
+};
+template <>
+struct PadLoad<float, 4> {
+  static __device__ __forceinline__ void ld(const float* v, const int32_t* c, double* vo, int32_t* co) {
+    float4 a = ld_stream4(v);
+    int4 b = ld_stream_i4(c);
+    vo[0] = a.x;
+    vo[1] = a.y;
+    vo[2] = a.z;
+    vo[3] = a.w;
+    co[0] = b.x;
+    co[1] = b.y;
+    co[2] = b.z;
+    co[3] = b.w;
+  }
+};
+template <>
+struct PadLoad<float, 2> {
+  static __device__ __forceinline__ void ld(const float* v, const int32_t* c, double* vo, int32_t* co) {
+    float2 a = ld_stream2(v);
+    int2 b = ld_stream_i2(c);
+    vo[0] = a.x;
+    vo[1] = a.y;
+    co[0] = b.x;
+    co[1] = b.y;
+  }
+};
+template <class V>
+struct PadLoad<V, 1> {
+  static __device__ __forceinline__ void ld(const V* v, const int32_t* c, double* vo, int32_t* co) {
+    vo[0] = (double)ld_stream(v);
+    co[0] = ld_stream(c);
+  }
+};
+template <>
+struct PadLoad<double, 4> {
+  static __device__ __forceinline__ void ld(const double* v, const int32_t* c, double* vo, int32_t* co) {
+    double2 a = ld_stream2(v), b = ld_stream2(v + 2);
+    int4 q = ld_stream_i4(c);
+    vo[0] = a.x;
+    vo[1] = a.y;
+    vo[2] = b.x;
+    vo[3] = b.y;
+    co[0] = q.x;
+    co[1] = q.y;
+    co[2] = q.z;
+    co[3] = q.w;
+  }
+};
+
+template <class V, int VEC>
+__global__ void __launch_bounds__(1024) k_thread_row_pad(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  const V* pval = (const V*)p.pad_val;
+  for (int64_t t = gtid(); t < p.n_bmt; t += gthreads()) {
+    int64_t g, t0, t1;
+    if (p.grp_regular) {
+      g = t / p.grp_regular;
+      t0 = g * p.grp_regular;
+      t1 = min(t0 + p.grp_regular, p.n_bmt);
+    } else {  // binary search the group of BMT t
+      int64_t lo = 0, hi = p.n_grp - 1;
+      while (lo < hi) {
+        int64_t mid = (lo + hi + 1) >> 1;
+        if (ldm(p.grp_first_bmt + mid) <= t) lo = mid;
+        else hi = mid - 1;
+      }
+      g = lo;
+      t0 = ldm(p.grp_first_bmt + g);
+      t1 = ldm(p.grp_first_bmt + g + 1);
+    }
+    const int64_t nt = t1 - t0, lt = t - t0;
+    const int64_t W = ldm(p.grp_width + g);
+    const int64_t base = ldm(p.grp_base + g) + lt * VEC;
+    const int64_t stride = nt * VEC;
+    int64_t r0 = p.bmt_row_ptr ? ldm(p.bmt_row_ptr + t) : t * p.s;
+    int64_t r1 = p.bmt_row_ptr ? ldm(p.bmt_row_ptr + t + 1) : min((t + 1) * p.s, p.m_p);
+    if (r1 - r0 == 1) {
+      // whole BMT is one row: read all W slots (pads have value 0, valid col)
+      double acc[VEC];
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+      const int64_t nchunk = W / VEC;
+#pragma unroll 4
+      for (int64_t c = 0; c < nchunk; ++c) {
+        double v[VEC];
+        int32_t cc[VEC];
+        PadLoad<V, VEC>::ld(pval + base + c * stride, p.pad_col + base + c * stride, v, cc);
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) acc[q] += v[q] * ldx(x, cc[q]);
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) s += acc[q];
+      write_excl(p, y, r0, s);
+    } else {
+      // several rows in one padded BMT: row boundaries from row_ptr (local offsets)
+      int64_t nz0 = ldm(p.row_ptr + r0);
+      for (int64_t r = r0; r < r1; ++r) {
+        int64_t ja = ldm(p.row_ptr + r) - nz0, je = ldm(p.row_ptr + r + 1) - nz0;
+        double acc = 0.0;
+        for (int64_t j = ja; j < je; ++j) {
+          int64_t slot = base + (j / VEC) * stride + (j % VEC);
+          acc += (double)ld_stream(pval + slot) * ldx(x, ld_stream(p.pad_col + slot));
+        }
+        write_excl(p, y, r, acc);
+      }
+    }
+  }
+}
+
+// =====================================================================================
+// FAM_NNZ_THREAD: BMT_NNZ_BLOCK(k) + THREAD_BITMAP_RED_G.  Each thread reduces its k
+// nonzeros serially, cutting at bitmap heads (bit j = element j starts a row, A20); rows
+// whose head and end lie in the BMT are exclusive, straddlers go to y by atomics ("_G").
+// =====================================================================================
+template <class V>
+__global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  const V* val = (const V*)p.val;
+  for (int64_t t = gtid(); t < p.n_bmt; t += gthreads()) {
+    int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
+    int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
+    int64_t row = ldm(p.bmt_first_row + t);
+    const uint32_t* bm = p.bitmap + t * p.bm_words;
+    uint32_t w = ldm(bm);
+    bool inside = w & 1u;  // current segment started at a head inside this BMT
+    double acc = 0.0;
+    for (int64_t j = 0; j < e - a; ++j) {
+      if ((j & 31) == 0 && j) w = ldm(bm + (j >> 5));
+      if (j && ((w >> (j & 31)) & 1u)) {
+        if (inside) write_excl(p, y, row, acc);
+        else write_atom(p, y, row, acc);
+        ++row;
+        acc = 0.0;
+        inside = true;
+      }
+      acc += (double)ld_stream(val + a + j) * ldx(x, ld_stream(p.col + a + j));
+    }
+    bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
+    if (inside && ends) write_excl(p, y, row, acc);
+    else write_atom(p, y, row, acc);
+  }
+}
+
+// =====================================================================================
+// FAM_NNZ_WARP: BMW blocks of BMT_NNZ(k) tiles; lanes take BMTs in rounds of 32.
+// Per lane: c_in (partial before its first head), c_out (partial from its last head),
+// interior rows stored directly.  Warp level:
+//   WRED == 1  WARP_SEG_ADD_RED: segmented inclusive scan over lanes (shfl_up + head flags,
+//              the "segment sum" of P:281)
+//   WRED == 2  WARP_BITMAP_RED: ballot of per-lane head flags (the lane bitmap) locates each
+//              segment's previous head lane; plain prefix sums give the segment totals.
+// Rows closed inside the BMW are exclusive; rows entering from before the BMW or leaving
+// after it are added atomically.
+// =====================================================================================
+template <class V, int WRED>
+__global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  const V* val = (const V*)p.val;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = gthreads() >> 5;
+  for (int64_t w = gtid() >> 5; w < p.n_bmw; w += nwarps) {
+    int64_t tb0 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w) : w * p.bmts_per_bmw;
+    int64_t tb1 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w + 1) : min(tb0 + p.bmts_per_bmw, p.n_bmt);
+    double carry = 0.0;
+    bool carry_inside = false;  // open segment's row started at a head inside this BMW
+    bool carry_live = false;    // an open segment exists (false only before the first element)
+    int64_t carry_row = 0;
+    for (int64_t base = tb0; base < tb1; base += 32) {
+      const int64_t t = base + lane;
+      const bool active = t < tb1;
+      const int nact = (int)min((int64_t)32, tb1 - base);
+      double cin = 0.0, cout = 0.0;
+      bool hh = false, b0 = false;
+      int64_t head_row = 0;  // row of the first head in this lane
+      int64_t last_row = 0;  // row of this lane's last element
+      if (active) {
+        int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
+        int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
+        int64_t row = ldm(p.bmt_first_row + t);
+        const uint32_t* bm = p.bitmap + t * p.bm_words;
+        uint32_t wd = ldm(bm);
+        double cur = 0.0;
+        if (wd & 1u) {
+          hh = true;
+          b0 = true;
+          head_row = row;
+        }
+        for (int64_t j = 0; j < e - a; ++j) {
+          if ((j & 31) == 0 && j) wd = ldm(bm + (j >> 5));
+          if (j && ((wd >> (j & 31)) & 1u)) {
+            if (!hh) {
+              cin = cur;
+              hh = true;
+              head_row = row + 1;
+            } else {
+              write_excl(p, y, row, cur);  // row wholly inside this lane's BMT
+            }
+            ++row;
+            cur = 0.0;
+          }
+          cur += (double)ld_stream(val + a + j) * ldx(x, ld_stream(p.col + a + j));
+        }
+        if (hh) cout = cur;
+        else cin = cur;
+        last_row = row;
+      }
+      double v_end;       // open-segment value at the end of each lane
+      bool inside_end;    // that segment started inside the BMW
+      double closing;     // for head lanes: total of the row closed at the first head
+      bool closing_inside;
+      if (WRED == 1) {
+        double v = hh ? cout : cin;
+        bool f = hh;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          double nv = __shfl_up_sync(0xffffffffu, v, d);
+          bool nf = __shfl_up_sync(0xffffffffu, (int)f, d);
+          if (lane >= d) {
+            if (!f) v += nv;
+            f = f || nf;
+          }
+        }
+        if (!f) v += carry;
+        v_end = v;
+        inside_end = f ? true : carry_inside;
+        double pv = __shfl_up_sync(0xffffffffu, v_end, 1);
+        bool pin = __shfl_up_sync(0xffffffffu, (int)inside_end, 1);
+        if (lane == 0) {
+          pv = carry;
+          pin = carry_inside;
+        }
+        closing = pv + cin;
+        closing_inside = pin;
+      } else {
+        const unsigned mask = __ballot_sync(0xffffffffu, hh);
+        double c = hh ? 0.0 : cin;  // non-head lanes contribute wholly to the open segment
+        double P = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          double nv = __shfl_up_sync(0xffffffffu, P, d);
+          if (lane >= d) P += nv;
+        }
+        // previous head lane strictly below this lane
+        const unsigned below = mask & ((1u << lane) - 1u);
+        const int h = below ? 31 - __clz(below) : -1;
+        const int hs = h < 0 ? 0 : h;
+        double cout_h = __shfl_sync(0xffffffffu, cout, hs);
+        double P_h = __shfl_sync(0xffffffffu, P, hs);
+        double P_prev = __shfl_up_sync(0xffffffffu, P, 1);
+        if (lane == 0) P_prev = 0.0;
+        if (h >= 0) {
+          closing = cout_h + (P_prev - P_h) + cin;
+          closing_inside = true;
+        } else {
+          closing = carry + P_prev + cin;
+          closing_inside = carry_inside;
+        }
+        // open segment at the end of this lane
+        const unsigned upto = mask & (lane == 31 ? 0xffffffffu : ((1u << (lane + 1)) - 1u));
+        const int h2 = upto ? 31 - __clz(upto) : -1;
+        const int h2s = h2 < 0 ? 0 : h2;
+        double cout_h2 = __shfl_sync(0xffffffffu, cout, h2s);
+        double P_h2 = __shfl_sync(0xffffffffu, P, h2s);
+        if (h2 >= 0) {
+          v_end = cout_h2 + (P - P_h2);
+          inside_end = true;
+        } else {
+          v_end = carry + P;
+          inside_end = carry_inside;
+        }
+      }
+      if (active && hh) {
+        // the row closed at this lane's first head; none only when the BMW itself starts
+        // with a head (lane 0 of the first round, element 0 is a row start)
+        bool exists = !(lane == 0 && !carry_live && b0);
+        if (exists) {
+          if (closing_inside) write_excl(p, y, head_row - 1, closing);
+          else write_atom(p, y, head_row - 1, closing);
+        }
+      }
+      carry = __shfl_sync(0xffffffffu, v_end, nact - 1);
+      carry_inside = __shfl_sync(0xffffffffu, (int)inside_end, nact - 1);
+      carry_row = __shfl_sync(0xffffffffu, last_row, nact - 1);
+      carry_live = true;
+    }
+    if (lane == 0 && carry_live) {
+      // final open segment: the row of the BMW's last element
+      bool ends = (tb1 >= p.n_bmt) ? true : (ldm(p.bitmap + tb1 * p.bm_words) & 1u);
+      if (carry_inside && ends) write_excl(p, y, carry_row, carry);
+      else write_atom(p, y, carry_row, carry);
+    }
+  }
+}
+
+// =====================================================================================
+// FAM_WARP_ROW: single-row BMWs + WARP_TOTAL_RED (CSR-Vector).  Lanes stride over
+// the BMW's nonzeros (coalesced), or over its BMT_NNZ(k) chunks with THREAD_TOTAL_RED;
+// butterfly shuffle reduction; lane 0 writes.
+// =====================================================================================
+template <class V>
+__global__ void __launch_bounds__(1024) k_warp_row(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  const V* val = (const V*)p.val;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = gthreads() >> 5;
+  for (int64_t w = gtid() >> 5; w < p.n_bmw; w += nwarps) {
+    int64_t a = ldm(p.bmw_start + w), e = ldm(p.bmw_start + w + 1);
+    int64_t row = p.bmw_first_row ? ldm(p.bmw_first_row + w) : w;
+    double acc = 0.0;
+    if (p.k <= 0) {
+      for (int64_t i = a + lane; i < e; i += 32) acc += (double)ld_stream(val + i) * ldx(x, ld_stream(p.col + i));
+    } else {
+      for (int64_t c = a + lane * p.k; c < e; c += 32 * p.k) {
+        int64_t ce = min(c + p.k, e);
+        for (int64_t i = c; i < ce; ++i) acc += (double)ld_stream(val + i) * ldx(x, ld_stream(p.col + i));
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      bool excl = p.bmw_all_excl || (a == ldm(p.row_ptr + row) && e == ldm(p.row_ptr + row + 1));
+      if (excl) write_excl(p, y, row, acc);
+      else write_atom(p, y, row, acc);
+    }
+  }
+}
+
+// =====================================================================================
+// FAM_BLOCK_TOTAL: single-row BMTBs + SHMEM_TOTAL_RED ("adds up all intermediate results
+// of a thread block to a result"): CTA-wide sum, one store/atomic per CTA.
+// =====================================================================================
+template <class V>
+__global__ void __launch_bounds__(1024) k_block_total(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  __shared__ double red[32];
+  const V* val = (const V*)p.val;
+  for (int64_t b = blockIdx.x; b < p.n_bmtb; b += gridDim.x) {
+    int64_t a = p.bmtb_start ? ldm(p.bmtb_start + b) : b * p.k1;
+    int64_t e = p.bmtb_start ? ldm(p.bmtb_start + b + 1) : min(a + p.k1, p.nnz_p);
+    double acc = 0.0;
+    for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x)
+      acc += (double)ld_stream(val + i) * ldx(x, ld_stream(p.col + i));
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+      s = warp_sum(s);
+      if (threadIdx.x == 0) {
+        int64_t row = ldm(p.bmtb_first_row + b);
+        if (a == ldm(p.row_ptr + row) && e == ldm(p.row_ptr + row + 1)) write_excl(p, y, row, s);
+        else write_atom(p, y, row, s);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// =====================================================================================
+// FAM_BLOCK_OFFSET: BMTB + SHMEM_OFFSET_RED (CSR-Stream).  The CTA stages the products of
+// its nonzeros in shared memory (coalesced pass; the "adapter" of P:322 copying register
+// results to shared memory), then reduces its row fragments in parallel using the CSR-like
+// row offsets ("reduce_row_offsets") = the block's slice of row_ptr.
+// =====================================================================================
+template <class V>
+__global__ void __launch_bounds__(1024) k_block_offset(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* prod = (double*)smem_raw;  // max_block_nnz products
+  const V* val = (const V*)p.val;
+  for (int64_t b = blockIdx.x; b < p.n_bmtb; b += gridDim.x) {
+    int64_t a = p.bmtb_start ? ldm(p.bmtb_start + b) : b * p.k1;
+    int64_t e = p.bmtb_start ? ldm(p.bmtb_start + b + 1) : min(a + p.k1, p.nnz_p);
+    for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x)
+      prod[i - a] = (double)ld_stream(val + i) * ldx(x, ld_stream(p.col + i));
+    __syncthreads();
+    int64_t r0 = ldm(p.bmtb_first_row + b);
+    for (int64_t r = r0 + threadIdx.x; r < p.m_p; r += blockDim.x) {
+      int64_t ra = ldm(p.row_ptr + r);
+      if (ra >= e) break;
+      int64_t re = ldm(p.row_ptr + r + 1);
+      int64_t fa = max(ra, a), fe = min(re, e);
+      double s = 0.0;
+      for (int64_t i = fa; i < fe; ++i) s += prod[i - a];
+      if (fa == ra && fe == re) write_excl(p, y, r, s);
+      else write_atom(p, y, r, s);
+    }
+    __syncthreads();
+  }
+}
+
+// =====================================================================================
+// FAM_DIA: y_r = sum_d dia_val[d*stride + i] * x[r + off_d]  (DIA root format).
+// R consecutive rows per thread -> one 16-byte load per diagonal; offsets in the kernel
+// parameter space (constant bank).
+// =====================================================================================
+template <class V, int R>
+__global__ void __launch_bounds__(1024) k_dia(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  const V* dv = (const V*)p.dia_val;
+  for (int64_t i0 = gtid() * R; i0 < p.mb; i0 += gthreads() * R) {
+    double acc[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) acc[q] = 0.0;
+    const int64_t r = p.r0 + i0;
+#pragma unroll 4
+    for (int d = 0; d < p.D; ++d) {
+      const int64_t o = p.dia_off[d];
+      double v[R];
+      if constexpr (R == 2 && sizeof(V) == 8) {
+        double2 t = ld_stream2((const double*)dv + d * p.dia_stride + i0);
+        v[0] = t.x;
+        v[1] = t.y;
+      } else if constexpr (R == 4 && sizeof(V) == 4) {
+        float4 t = ld_stream4((const float*)dv + d * p.dia_stride + i0);
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = (double)ld_stream(dv + d * p.dia_stride + i0 + q);
+      }
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        int64_t c = r + q + o;
+        if (c >= 0 && c < p.n) acc[q] += v[q] * ldx(x, c);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (i0 + q < p.mb) write_excl(p, y, i0 + q, acc[q]);
+  }
+}
+
+// =====================================================================================
+// FAM_DENSE: BSR-like b x b tiles (column-major) of DENSE_DECOM.  One warp per tile row;
+// lane owns rows i = lane + 32q; for each tile column j the warp reads b contiguous values
+// (coalesced) and one broadcast x element.  CUDA cores: a single right-hand side makes
+// every tile a GEMV, not a contraction.
+// =====================================================================================
+template <class V, int RPL>
+__global__ void __launch_bounds__(1024) k_dense(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  const V* tv = (const V*)p.tile_val;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = gthreads() >> 5;
+  const int64_t b = p.b, bb = b * b;
+  for (int64_t tr = gtid() >> 5; tr < p.n_tile_rows; tr += nwarps) {
+    int64_t I = ldm(p.tile_row_id + tr);
+    int64_t t0 = ldm(p.tile_row_ptr + tr), t1 = ldm(p.tile_row_ptr + tr + 1);
+    double acc[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) acc[q] = 0.0;
+    for (int64_t t = t0; t < t1; ++t) {
+      int64_t J = ldm(p.tile_col + t);
+      const V* tile = tv + t * bb;
+#pragma unroll 4
+      for (int64_t j = 0; j < b; ++j) {
+        int64_t c = J * b + j;
+        double xj = c < p.n ? ldx(x, c) : 0.0;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          int64_t i = lane + 32 * q;
+          if (i < b) acc[q] += (double)ld_stream(tile + j * b + i) * xj;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      int64_t i = lane + 32 * q;
+      int64_t row = I * b + i;
+      if (i < b && row >= p.row_lo && row < p.row_hi) write_excl(p, y, row, acc[q]);
+    }
+  }
+}
+
+// =====================================================================================
+// beta pre-pass of the writer rule (A22): y[r] = beta * y[r] (0 when beta == 0)
+// =====================================================================================
+template <class V>
+__global__ void k_prepass(const int32_t* __restrict__ rows, int64_t n, double beta, V* __restrict__ y) {
+  for (int64_t i = gtid(); i < n; i += gthreads()) {
+    int64_t r = ldm(rows + i);
+    y[r] = beta == 0.0 ? (V)0 : (V)(beta * (double)y[r]);
+  }
+}
+template <class V>
+__global__ void k_scale_all(int64_t m, double beta, V* __restrict__ y) {
+  for (int64_t i = gtid(); i < m; i += gthreads()) y[i] = beta == 0.0 ? (V)0 : (V)(beta * (double)y[i]);
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int64_t grid_for(const DevPart& p, int64_t units, int64_t units_per_cta) {
+  if (p.grid > 0) return (int64_t)p.grid * sm_count();
+  int64_t g = (units + units_per_cta - 1) / units_per_cta;
+  if (g < 1) g = 1;
+  if (g > (int64_t(1) << 31) - 1) g = (int64_t(1) << 31) - 1;
+  return g;
+}
+
+template <class V>
+int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
+  const int tpb = p.tpb > 0 ? p.tpb : 256;
+  switch (p.fam) {
+    case FAM_THREAD_ROW:
+      if (!p.pad) {
+        k_thread_row<V><<<grid_for(p, p.n_bmt, tpb), tpb, 0, s>>>(p, x, y);
+      } else {
+        int64_t g = grid_for(p, p.n_bmt, tpb);
+        if (p.vec == 1) k_thread_row_pad<V, 1><<<g, tpb, 0, s>>>(p, x, y);
+        else if (p.vec == 2) k_thread_row_pad<V, 2><<<g, tpb, 0, s>>>(p, x, y);
+        else k_thread_row_pad<V, 4><<<g, tpb, 0, s>>>(p, x, y);
+      }
+      break;
+    case FAM_NNZ_THREAD:
+      k_nnz_thread<V><<<grid_for(p, p.n_bmt, tpb), tpb, 0, s>>>(p, x, y);
+      break;
+    case FAM_NNZ_WARP:
+      if (p.variant == 1) k_nnz_warp<V, 1><<<grid_for(p, p.n_bmw, tpb / 32), tpb, 0, s>>>(p, x, y);
+      else k_nnz_warp<V, 2><<<grid_for(p, p.n_bmw, tpb / 32), tpb, 0, s>>>(p, x, y);
+      break;
+    case FAM_WARP_ROW:
+      k_warp_row<V><<<grid_for(p, p.n_bmw, tpb / 32), tpb, 0, s>>>(p, x, y);
+      break;
+    case FAM_BLOCK_TOTAL:
+      k_block_total<V><<<grid_for(p, p.n_bmtb, 1), tpb, 0, s>>>(p, x, y);
+      break;
+    case FAM_BLOCK_OFFSET:
+      k_block_offset<V><<<grid_for(p, p.n_bmtb, 1), tpb, p.smem, s>>>(p, x, y);
+      break;
+    case FAM_DIA: {
+      constexpr int R = 16 / sizeof(V);
+      k_dia<V, R><<<grid_for(p, (p.mb + R - 1) / R, tpb), tpb, 0, s>>>(p, x, y);
+      break;
+    }
+    case FAM_DENSE: {
+      int64_t g = grid_for(p, p.n_tile_rows, tpb / 32);
+      int rpl = (int)((p.b + 31) / 32);
+      if (rpl <= 1) k_dense<V, 1><<<g, tpb, 0, s>>>(p, x, y);
+      else if (rpl == 2) k_dense<V, 2><<<g, tpb, 0, s>>>(p, x, y);
+      else if (rpl <= 4) k_dense<V, 4><<<g, tpb, 0, s>>>(p, x, y);
+      else return (int)cudaErrorInvalidValue;
+      break;
+    }
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int launch_part(const DevPart& p, const void* x, void* y, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p.dtype == 1) return launch_typed<double>(p, (const double*)x, (double*)y, s);
+  return launch_typed<float>(p, (const float*)x, (float*)y, s);
+}
+
+int launch_prepass(const int32_t* rows, int64_t n, double beta, void* y, int dtype, void* stream) {
+  if (n <= 0) return 0;
+  int64_t g = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (dtype == 1) k_prepass<double><<<g, 256, 0, (cudaStream_t)stream>>>(rows, n, beta, (double*)y);
+  else k_prepass<float><<<g, 256, 0, (cudaStream_t)stream>>>(rows, n, beta, (float*)y);
+  return (int)cudaGetLastError();
+}
+
+int launch_scale_all(int64_t m, double beta, void* y, int dtype, void* stream) {
+  if (m <= 0) return 0;
+  int64_t g = std::min<int64_t>((m + 255) / 256, 148 * 16);
+  if (dtype == 1) k_scale_all<double><<<g, 256, 0, (cudaStream_t)stream>>>(m, beta, (double*)y);
+  else k_scale_all<float><<<g, 256, 0, (cudaStream_t)stream>>>(m, beta, (float*)y);
+  return (int)cudaGetLastError();
+}
+
+int prepare_part(DevPart& p) {
+  if (p.fam == FAM_BLOCK_OFFSET) {
+    p.smem = (size_t)p.max_block_nnz * sizeof(double);
+    if (p.smem > 48 * 1024) {
+      cudaError_t e = p.dtype == 1
+                          ? cudaFuncSetAttribute(k_block_offset<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem)
+                          : cudaFuncSetAttribute(k_block_offset<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      return (int)e;
+    }
+  }
+  return 0;
+}
+
+int device_max_smem_optin(int device) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  return v;
+}
+
+const char* fam_kernel_name(const DevPart& p) {
+  switch (p.fam) {
+    case FAM_THREAD_ROW: return p.pad ? "k_thread_row_pad" : "k_thread_row";
+    case FAM_NNZ_THREAD: return "k_nnz_thread";
+    case FAM_NNZ_WARP: return p.variant == 1 ? "k_nnz_warp<seg>" : "k_nnz_warp<bitmap>";
+    case FAM_WARP_ROW: return "k_warp_row";
+    case FAM_BLOCK_TOTAL: return "k_block_total";
+    case FAM_BLOCK_OFFSET: return "k_block_offset";
+    case FAM_DIA: return "k_dia";
+    case FAM_DENSE: return "k_dense";
+    default: return "?";
+  }
+}
+
+}  // namespace as

@@ -1,0 +1,296 @@
+// Plan = the built format made device-resident + its precomputed launch list.
+// Uploads only the arrays the chosen kernel reads ("All arrays of a format are extracted
+// from Matrix Metadata Set by choosing the metadata needed by the kernel") and
+// replaces arrays that are linear by construction by arithmetic (A17).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "internal.h"
+#include "plan.h"
+
+namespace as {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      fail(AS_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+    fail(AS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <class T>
+bool is_affine(const std::vector<T>& v, int64_t step, int64_t base = 0, int64_t cap = INT64_MAX) {
+  for (size_t i = 0; i < v.size(); ++i)
+    if ((int64_t)v[i] != std::min(base + (int64_t)i * step, cap)) return false;
+  return true;
+}
+
+std::vector<int32_t> to_i32(const std::vector<int64_t>& v, const char* what) {
+  std::vector<int32_t> o(v.size());
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (v[i] > INT32_MAX || v[i] < INT32_MIN) fail(AS_ERR_PLAN_INFEASIBLE, std::string(what) + " exceeds int32 (reading A36)");
+    o[i] = (int32_t)v[i];
+  }
+  return o;
+}
+
+}  // namespace
+
+void* Plan::up(const void* h, size_t bytes, cudaStream_t s, size_t pad_to) {
+  size_t alloc = std::max<size_t>(std::max(bytes, pad_to), 16);
+  void* d = nullptr;
+  ck(cudaMalloc(&d, alloc), "cudaMalloc");
+  allocs.push_back(d);
+  dev_bytes += alloc;
+  if (alloc > bytes) ck(cudaMemsetAsync(d, 0, alloc, s), "cudaMemsetAsync");
+  if (bytes) ck(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync");
+  return d;
+}
+
+const int32_t* Plan::up_i32(const std::vector<int64_t>& v, cudaStream_t s, const char* what) {
+  auto t = to_i32(v, what);
+  const int32_t* d = (const int32_t*)up(t.data(), t.size() * 4, s);
+  cudaStreamSynchronize(s);  // host temporary dies here
+  return d;
+}
+
+const void* Plan::up_vals(const std::vector<double>& v, cudaStream_t s, size_t pad_elems) {
+  size_t n = std::max(v.size(), pad_elems);
+  if (dt == AS_R64F) {
+    std::vector<double> t(n, 0.0);
+    std::copy(v.begin(), v.end(), t.begin());
+    const void* d = up(t.data(), n * 8, s);
+    cudaStreamSynchronize(s);
+    return d;
+  }
+  std::vector<float> t(n, 0.0f);
+  for (size_t i = 0; i < v.size(); ++i) t[i] = (float)v[i];
+  const void* d = up(t.data(), n * 4, s);
+  cudaStreamSynchronize(s);
+  return d;
+}
+
+Plan::~Plan() {
+  if (device >= 0) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    for (void* p : allocs) cudaFree(p);
+    if (d_x) cudaFree(d_x);
+    if (d_y) cudaFree(d_y);
+    cudaSetDevice(cur);
+  }
+}
+
+void Plan::upload(cudaStream_t s) {
+  const int64_t sv = dt == AS_R64F ? 8 : 4;
+  int max_smem = device_max_smem_optin(device);
+  for (int64_t pi : host.launch_order) {
+    const HostPart& h = host.parts[pi];
+    DevPart d;
+    d.fam = h.fam;
+    d.dtype = dt == AS_R64F ? 1 : 0;
+    d.mode = h.mode;
+    d.tpb = h.tpb > 0 ? h.tpb : 256;
+    d.grid = h.grid;
+    d.n = host.n;
+    if (h.kind == "dia") {
+      d.D = (int)h.dia_off.size();
+      if (d.D > kMaxDiags) fail(AS_ERR_PLAN_INFEASIBLE, "DIA part with more than 64 diagonals");
+      for (int i = 0; i < d.D; ++i) d.dia_off[i] = (int32_t)h.dia_off[i];
+      d.r0 = h.r0;
+      d.mb = h.mb;
+      d.origin_base = h.r0;
+      const int64_t R = 16 / sv;
+      d.dia_stride = (h.mb + R - 1) / R * R;
+      std::vector<double> padded((size_t)(d.D * d.dia_stride), 0.0);
+      for (int i = 0; i < d.D; ++i)
+        std::copy(h.dia_val.begin() + (size_t)i * h.mb, h.dia_val.begin() + (size_t)(i + 1) * h.mb,
+                  padded.begin() + (size_t)i * d.dia_stride);
+      d.dia_val = up_vals(padded, s);
+      bytes_model += (double)(d.D * h.mb * sv);
+    } else if (h.kind == "dense") {
+      d.b = h.b;
+      d.n_tile_rows = (int64_t)h.tile_row_id.size();
+      d.row_lo = h.r0;
+      d.row_hi = h.r0 + h.mb;
+      d.tile_row_id = up_i32(h.tile_row_id, s, "tile_row_id");
+      d.tile_row_ptr = up_i32(h.tile_row_ptr, s, "tile_row_ptr");
+      d.tile_col = up_i32(h.tile_col, s, "tile_col");
+      d.tile_val = up_vals(h.tile_val, s);
+      if (d.b > 128) fail(AS_ERR_PLAN_INFEASIBLE, "DENSE tiles larger than 128 are not implemented");
+      bytes_model += (double)(h.tile_val.size() * sv + (h.tile_col.size() + 2 * h.tile_row_id.size() + 1) * 4);
+    } else {
+      const int64_t mp = (int64_t)h.origin.size(), nnz = h.row_ptr.back();
+      if (nnz >= INT32_MAX) fail(AS_ERR_PLAN_INFEASIBLE, "part nnz exceeds int32 (reading A36)");
+      d.m_p = mp;
+      d.nnz_p = nnz;
+      // origin_rows: implicit when affine (A17)
+      if (mp && is_affine(h.origin, 1, h.origin[0])) {
+        d.origin_base = h.origin[0];
+      } else {
+        d.origin = up_i32(h.origin, s, "origin_rows");
+        bytes_model += (double)(mp * 4);
+      }
+      const Level &B = h.lv[0], &W = h.lv[1], &T = h.lv[2];
+      bool need_rowptr = true, need_colval = true;
+      switch (h.fam) {
+        case FAM_THREAD_ROW: {
+          d.n_bmt = T.count();
+          d.s = T.size;
+          if (!is_affine(T.first_row, T.size, 0)) {
+            std::vector<int64_t> brp = T.first_row;
+            brp.push_back(mp);
+            d.bmt_row_ptr = up_i32(brp, s, "bmt_row_ptr");
+            bytes_model += (double)(brp.size() * 4);
+          }
+          if (h.pad) {
+            d.pad = 1;
+            d.vec = h.vec;
+            d.n_grp = (int64_t)h.pad_width.size();
+            // regular groups: every group (but the last) holds the same number of BMTs
+            int64_t per = d.n_grp ? h.grp_first_bmt[1] - h.grp_first_bmt[0] : 0;
+            bool reg = per > 0;
+            for (int64_t g = 0; g < d.n_grp && reg; ++g)
+              if (h.grp_first_bmt[g] != g * per) reg = false;
+            d.grp_regular = reg ? per : 0;
+            d.grp_first_bmt = up_i32(h.grp_first_bmt, s, "grp_first_bmt");
+            d.grp_base = (const int64_t*)up(h.grp_base.data(), h.grp_base.size() * 8, s);
+            d.grp_width = up_i32(h.pad_width, s, "pad_width");
+            d.pad_col = (const int32_t*)up(h.pad_col.data(), h.pad_col.size() * 4, s);
+            cudaStreamSynchronize(s);
+            d.pad_val = up_vals(h.pad_val, s);
+            need_colval = false;
+            // row_ptr only for multi-row padded BMTs
+            bool multi = false;
+            for (int64_t t = 0; t < T.count() && !multi; ++t)
+              multi = (t + 1 < T.count() ? T.first_row[t + 1] : mp) - T.first_row[t] > 1;
+            need_rowptr = multi;
+            bytes_model += (double)(h.pad_col.size() * 4 + h.pad_val.size() * sv + d.n_grp * 16);
+          }
+          break;
+        }
+        case FAM_NNZ_THREAD:
+        case FAM_NNZ_WARP: {
+          d.n_bmt = T.count();
+          d.k = T.size;
+          std::vector<int64_t> st(T.start.begin(), T.start.end() - 1);
+          if (!is_affine(st, T.size, 0)) {
+            d.bmt_start = up_i32(T.start, s, "bmt_start");
+            bytes_model += (double)(T.start.size() * 4);
+          }
+          d.bmt_first_row = up_i32(T.first_row, s, "bmt_first_row");
+          d.bm_words = h.bm_words;
+          d.bitmap = (const uint32_t*)up(h.bitmap.data(), h.bitmap.size() * 4, s);
+          bytes_model += (double)(T.first_row.size() * 4 + h.bitmap.size() * 4);
+          if (h.fam == FAM_NNZ_WARP) {
+            d.variant = h.red[1] == RED_SEG ? 1 : 2;
+            d.n_bmw = W.count();
+            // BMT index range of each BMW (BMTs restart at BMW boundaries)
+            std::vector<int64_t> ptr(W.count() + 1, 0);
+            int64_t t = 0;
+            for (int64_t w = 0; w < W.count(); ++w) {
+              ptr[w] = t;
+              while (t < T.count() && T.start[t] < W.start[w + 1]) ++t;
+            }
+            ptr[W.count()] = t;
+            int64_t per = W.count() ? ptr[1] - ptr[0] : 0;
+            if (per > 0 && is_affine(ptr, per, 0, T.count())) {
+              d.bmts_per_bmw = per;
+            } else {
+              d.bmw_bmt_ptr = up_i32(ptr, s, "bmw_bmt_ptr");
+              bytes_model += (double)(ptr.size() * 4);
+            }
+          }
+          need_rowptr = false;
+          break;
+        }
+        case FAM_WARP_ROW: {
+          d.n_bmw = W.count();
+          d.k = T.present ? T.size : 0;
+          bool rowblocks = !W.nnz && (!B.present || !B.nnz);
+          d.bmw_all_excl = rowblocks ? 1 : 0;
+          if (rowblocks && W.size == 1 && is_affine(W.first_row, 1, 0)) {
+            d.bmw_start = nullptr;  // == row_ptr
+          } else {
+            d.bmw_start = up_i32(W.start, s, "bmw_start");
+            d.bmw_first_row = up_i32(W.first_row, s, "bmw_first_row");
+            bytes_model += (double)((W.start.size() + W.first_row.size()) * 4);
+          }
+          break;
+        }
+        case FAM_BLOCK_TOTAL:
+        case FAM_BLOCK_OFFSET: {
+          d.n_bmtb = B.count();
+          std::vector<int64_t> st(B.start.begin(), B.start.end() - 1);
+          if (B.nnz && is_affine(st, B.size, 0)) {
+            d.k1 = B.size;
+          } else {
+            d.bmtb_start = up_i32(B.start, s, "bmtb_start");
+            bytes_model += (double)(B.start.size() * 4);
+          }
+          d.bmtb_first_row = up_i32(B.first_row, s, "bmtb_first_row");
+          bytes_model += (double)(B.first_row.size() * 4);
+          int64_t mx = 0;
+          for (int64_t b = 0; b < B.count(); ++b) mx = std::max(mx, B.start[b + 1] - B.start[b]);
+          d.max_block_nnz = mx;
+          if (h.fam == FAM_BLOCK_OFFSET && (int64_t)mx * 8 > max_smem)
+            fail(AS_ERR_PLAN_INFEASIBLE, "P2: SHMEM_OFFSET_RED block of " + std::to_string(mx) +
+                                             " nonzeros exceeds the shared-memory opt-in limit");
+          break;
+        }
+        default:
+          fail(AS_ERR_PLAN_INFEASIBLE, "part without a kernel");
+      }
+      if (need_rowptr) {
+        d.row_ptr = up_i32(h.row_ptr, s, "row_ptr");
+        bytes_model += (double)((mp + 1) * 4);
+      }
+      if (h.fam == FAM_WARP_ROW && !d.bmw_start) d.bmw_start = d.row_ptr;
+      if (need_colval) {
+        d.col = (const int32_t*)up(h.col.data(), h.col.size() * 4, s);
+        d.val = up_vals(h.val, s);
+        bytes_model += (double)(nnz * (4 + sv));
+      }
+    }
+    ck((cudaError_t)prepare_part(d), "kernel attributes");
+    launches.push_back(d);
+  }
+  if (!host.prepass.empty()) {
+    d_prepass = up_i32(host.prepass, s, "prepass");
+    n_prepass = (int64_t)host.prepass.size();
+  }
+  ck(cudaStreamSynchronize(s), "upload");
+}
+
+void Plan::compute_model() {
+  const double sv = dt == AS_R64F ? 8 : 4;
+  // x: compulsory distinct columns; y per writer rule
+  double ybytes0 = 0, ybytes1 = 0;
+  for (int64_t pi : host.launch_order) {
+    const HostPart& h = host.parts[pi];
+    double ex = (double)h.excl.size(), at = (double)h.atom.size();
+    if (h.mode == 0) {
+      ybytes0 += ex * sv;
+      ybytes1 += 2 * ex * sv;
+    } else {
+      ybytes0 += 2 * ex * sv;
+      ybytes1 += 2 * ex * sv;
+    }
+    ybytes0 += 2 * at * sv;
+    ybytes1 += 2 * at * sv;
+  }
+  double pre = (double)host.prepass.size();
+  double prebytes0 = pre * (4 + sv), prebytes1 = pre * (4 + 2 * sv);
+  info.bytes_model = bytes_model + host.distinct_cols * sv + ybytes0 + (pre ? prebytes0 : 0);
+  info.bytes_model_beta = bytes_model + host.distinct_cols * sv + ybytes1 + (pre ? prebytes1 : 0);
+  info.bytes_floor = nnz_real * (sv + 4) + host.n * sv + host.m * sv;
+}
+
+}  // namespace as

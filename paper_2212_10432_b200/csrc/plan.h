@@ -1,0 +1,38 @@
+// Plan object (internal): device-resident format + launch list.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace as {
+
+struct Plan {
+  int device = -1;
+  as_dtype_t dt = AS_R64F;
+  int64_t m = 0, n = 0, nnz_real = 0;
+  HostPlan host;                 // logical metadata (kept for host-only plans / AS_PLAN_KEEP_HOST)
+  bool host_kept = false;
+  std::vector<DevPart> launches; // in launch order
+  const int32_t* d_prepass = nullptr;
+  int64_t n_prepass = 0;
+  std::vector<void*> allocs;
+  size_t dev_bytes = 0;
+  double bytes_model = 0;        // bytes of the device arrays the kernels read
+  as_plan_info_t info{};
+  void* d_x = nullptr;           // scratch for as_spmv_host
+  void* d_y = nullptr;
+  std::string canon;
+
+  ~Plan();
+  void* up(const void* h, size_t bytes, cudaStream_t s, size_t pad_to = 0);
+  const int32_t* up_i32(const std::vector<int64_t>& v, cudaStream_t s, const char* what);
+  const void* up_vals(const std::vector<double>& v, cudaStream_t s, size_t pad_elems = 0);
+  void upload(cudaStream_t s);
+  void compute_model();
+};
+
+}  // namespace as
+
+struct as_plan_s {
+  std::unique_ptr<as::Plan> P;
+};

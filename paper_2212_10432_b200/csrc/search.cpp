@@ -1,0 +1,345 @@
+// a7 Search Engine: random dependency-respecting Operator Graphs ("operators which can
+// satisfy the dependencies with graph existing operators would be randomly chosen and
+// connected behind"; P:369 step 1) with parameters drawn from a coarse grid (P:369 step 2),
+// each planned and timed on the device; the fastest is kept.  8 h cap -> budget_seconds.
+//
+// Pruning ("a ban list for pruned operators, according to already existing operators
+// of graph and sparsity patterns"): the generator only proposes mapping/implementing
+// combinations the sm_100a kernel family implements, and adapts block sizes to the row
+// statistics (short-row matrices do not try block-per-row reductions, etc.).  ROW_DIV / BIN
+// parameters use a DIV_IN_ROW_LEN_MUTATION-style discretisation: cuts where the row
+// length jumps.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+
+#include "internal.h"
+#include "plan.h"
+
+namespace as {
+
+Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int device, void* stream, int flags);
+void check_cuda(cudaError_t e, const char* what);
+
+namespace {
+
+struct Rng {
+  uint64_t s;
+  explicit Rng(uint64_t seed) : s(seed * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull) {}
+  uint64_t next() {  // splitmix64
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  int64_t uni(int64_t n) { return n <= 1 ? 0 : (int64_t)(next() % (uint64_t)n); }
+  template <class T>
+  T pick(const std::vector<T>& v) { return v[uni((int64_t)v.size())]; }
+  bool coin(double p) { return (double)(next() >> 11) * (1.0 / 9007199254740992.0) < p; }
+};
+
+struct Stats {
+  int64_t m, n, nnz, maxlen;
+  double avg, var;
+  std::vector<int64_t> mutation_cuts;  // rows where the row length jumps
+};
+
+Stats stats_of(const Matrix& A) {
+  Stats s{A.m, A.n, A.nnz(), 0, 0, 0, {}};
+  s.avg = A.m ? (double)s.nnz / A.m : 0;
+  double acc = 0;
+  for (int64_t r = 0; r < A.m; ++r) {
+    int64_t L = A.row_ptr[r + 1] - A.row_ptr[r];
+    s.maxlen = std::max(s.maxlen, L);
+    acc += ((double)L - s.avg) * ((double)L - s.avg);
+  }
+  s.var = A.m ? acc / A.m : 0;
+  // DIV_IN_ROW_LEN_MUTATION-lite: |len[r] - len[r-1]| >= 8 * avg, at most 7 cuts, spaced
+  double thr = std::max(8.0, 8.0 * s.avg);
+  for (int64_t r = 1; r < A.m && s.mutation_cuts.size() < 7; ++r) {
+    int64_t a = A.row_ptr[r] - A.row_ptr[r - 1], b = A.row_ptr[r + 1] - A.row_ptr[r];
+    if (std::fabs((double)(b - a)) >= thr && (s.mutation_cuts.empty() || r - s.mutation_cuts.back() >= 1024))
+      s.mutation_cuts.push_back(r);
+  }
+  return s;
+}
+
+std::string join_list(const std::vector<int64_t>& v) {
+  std::string o = "[";
+  for (size_t i = 0; i < v.size(); ++i) o += (i ? "," : "") + std::to_string(v[i]);
+  return o + "]";
+}
+
+// mapping + implementing stage for one COMPRESSed branch
+std::string gen_kernel(Rng& r, const Stats& st) {
+  std::vector<int> fams = {0, 0, 1, 2, 3, 5};  // thread_row x2, nnz_thread, nnz_warp, warp_row, block_offset
+  if (st.avg > 24) fams = {2, 2, 3, 3, 4, 5, 0};
+  if (st.maxlen > 4096) fams.push_back(4);     // block_total only helps long rows
+  int f = r.pick(fams);
+  std::string s = "COMPRESS; ";
+  std::string tpb = r.coin(0.5) ? "" : "SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{128, 256, 512})) + "); ";
+  switch (f) {
+    case 0: {  // CSR-scalar / ELL / SELL-P family
+      int64_t rows = r.pick(std::vector<int64_t>{32, 64, 128, 256});
+      bool bmtb = r.coin(0.5), bmw = !bmtb && r.coin(0.3);
+      if (bmtb) s += "BMTB_ROW_BLOCK(" + std::to_string(rows) + "); ";
+      if (bmtb && r.coin(0.3)) s += "SORT_BMTB; ";
+      if (bmw) s += "BMW_ROW_BLOCK(32); ";
+      s += "BMT_ROW_BLOCK(1); ";
+      if (r.coin(0.6)) {
+        std::string scope = bmtb ? (r.coin(0.7) ? "BMTB" : "GLOBAL") : bmw ? "BMW" : "GLOBAL";
+        if (scope == "GLOBAL" && st.var > 16) scope = bmtb ? "BMTB" : scope;
+        s += "BMT_PAD(scope=" + scope + "); ";
+      }
+      s += "THREAD_TOTAL_RED; ";
+      break;
+    }
+    case 1: {  // nnz-split, thread bitmap reduction (C1 graph family)
+      int64_t k = r.pick(std::vector<int64_t>{4, 8, 16, 32});
+      s += "BMT_NNZ_BLOCK(" + std::to_string(k) + "); THREAD_BITMAP_RED_G; ";
+      break;
+    }
+    case 2: {  // CSR5-like: warp tiles of nnz + segmented sum
+      int64_t k = r.pick(std::vector<int64_t>{4, 8, 16});
+      int64_t c = r.pick(std::vector<int64_t>{1, 2, 4});
+      s += "BMW_NNZ_BLOCK(" + std::to_string(32 * k * c) + "); BMT_NNZ_BLOCK(" + std::to_string(k) +
+           "); THREAD_BITMAP_RED_G; " + (r.coin(0.5) ? "WARP_SEG_ADD_RED; " : "WARP_BITMAP_RED; ");
+      break;
+    }
+    case 3: {  // CSR-vector
+      s += "BMW_ROW_BLOCK(1); ";
+      if (r.coin(0.5)) s += "BMT_NNZ_BLOCK(" + std::to_string(r.pick(std::vector<int64_t>{2, 4, 8})) + "); THREAD_TOTAL_RED; ";
+      s += "WARP_TOTAL_RED; ";
+      break;
+    }
+    case 4: {  // block per row (long rows)
+      s += "BMTB_ROW_BLOCK(1); SHMEM_TOTAL_RED; ";
+      break;
+    }
+    default: {  // CSR-stream
+      if (r.coin(0.5)) s += "BMTB_ROW_BLOCK(" + std::to_string(r.pick(std::vector<int64_t>{16, 32, 64, 128})) + "); ";
+      else s += "BMTB_NNZ_BLOCK(" + std::to_string(r.pick(std::vector<int64_t>{256, 512, 1024, 2048})) + "); ";
+      s += "SHMEM_OFFSET_RED; ";
+      break;
+    }
+  }
+  return s + tpb + "GMEM_ATOM_RED";
+}
+
+std::string gen_path(Rng& r, const Stats& st, bool can_decom, bool can_sort, bool can_div, int depth) {
+  std::vector<int> ops = {0, 0, 0};  // 0 = straight to COMPRESS
+  if (can_sort) {
+    ops.push_back(1);  // SORT
+    ops.push_back(2);  // SORT_SUB
+    if (st.maxlen > 8) ops.push_back(3);  // BIN
+  }
+  if (can_div && depth < 2 && st.m > 4096) ops.push_back(4);  // ROW_DIV
+  if (can_decom && depth < 2) {
+    ops.push_back(5);  // DIA_DECOM
+    ops.push_back(6);  // DENSE_DECOM
+  }
+  int op = r.pick(ops);
+  switch (op) {
+    case 1:
+      return "SORT; " + gen_kernel(r, st);
+    case 2:
+      return "SORT_SUB(g=" + std::to_string(r.pick(std::vector<int64_t>{32, 256, 4096})) + "); " + gen_kernel(r, st);
+    case 3: {
+      std::vector<int64_t> cand;
+      for (int64_t t : {4, 8, 16, 32, 64, 128, 512, 2048})
+        if (t < st.maxlen) cand.push_back(t);
+      std::vector<int64_t> t = {r.pick(cand)};
+      if (cand.size() > 1 && r.coin(0.5)) {
+        int64_t u = r.pick(cand);
+        if (u != t[0]) t.push_back(u);
+      }
+      std::sort(t.begin(), t.end());
+      std::string s = "BIN(t=" + join_list(t) + ") { ";
+      for (size_t b = 0; b <= t.size(); ++b) s += (b ? " | " : "") + gen_kernel(r, st);
+      return s + " }";
+    }
+    case 4: {
+      std::vector<int64_t> cuts = st.mutation_cuts;
+      if (cuts.empty() || r.coin(0.3)) {
+        int64_t k = 2 + r.uni(3);
+        cuts.clear();
+        for (int64_t i = 1; i < k; ++i) cuts.push_back(st.m * i / k);
+      }
+      std::string s = "ROW_DIV(cuts=" + join_list(cuts) + ") { ";
+      for (size_t b = 0; b <= cuts.size(); ++b)
+        s += (b ? " | " : "") + gen_path(r, st, can_decom, can_sort, false, depth + 1);
+      return s + " }";
+    }
+    case 5: {
+      std::string s = "DIA_DECOM(theta=" + std::string(r.pick(std::vector<const char*>{"0.5", "0.7", "0.9"})) +
+                      ",max=" + std::to_string(r.pick(std::vector<int64_t>{4, 8, 16, 32})) + ") { DIA";
+      if (r.coin(0.5)) s += "; SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{128, 256, 512})) + ")";
+      return s + " | " + gen_path(r, st, false, can_sort, false, depth + 1) + " }";
+    }
+    case 6: {
+      std::string s = "DENSE_DECOM(b=" + std::to_string(r.pick(std::vector<int64_t>{16, 32, 64, 128})) +
+                      ",theta=" + std::string(r.pick(std::vector<const char*>{"0.5", "0.75", "0.9"})) + ") { DENSE | " +
+                      gen_path(r, st, false, can_sort, false, depth + 1) + " }";
+      return s;
+    }
+    default:
+      return gen_kernel(r, st);
+  }
+}
+
+double median(std::vector<float> v) {
+  std::sort(v.begin(), v.end());
+  if (v.empty()) return 0;
+  return v.size() % 2 ? v[v.size() / 2] : 0.5 * (v[v.size() / 2 - 1] + v[v.size() / 2]);
+}
+
+std::string json_escape(const std::string& s) {
+  std::string o;
+  for (char c : s) {
+    if (c == '"' || c == '\\') o += '\\';
+    o += c;
+  }
+  return o;
+}
+
+}  // namespace
+
+std::string random_graph(const Matrix& A, uint64_t seed) {
+  Rng r(seed);
+  Stats st = stats_of(A);
+  return gen_path(r, st, true, true, true, 0);
+}
+
+as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device, void* stream, as_plan_t* best,
+                        char* best_graph, size_t* len) {
+  using clk = std::chrono::steady_clock;
+  auto t_start = clk::now();
+  int cur = 0;
+  check_cuda(cudaGetDevice(&cur), "cudaGetDevice");
+  check_cuda(cudaSetDevice(device), "cudaSetDevice");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sv = A.dt == AS_R64F ? 8 : 4;
+  void *dx = nullptr, *dy = nullptr, *flush = nullptr;
+  size_t flush_bytes = 0;
+  {
+    std::vector<double> xd(A.n);
+    uint64_t z = cfg->seed | 1;
+    for (auto& v : xd) {
+      z ^= z << 13;
+      z ^= z >> 7;
+      z ^= z << 17;
+      v = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    }
+    check_cuda(cudaMalloc(&dx, std::max<size_t>(16, A.n * sv)), "cudaMalloc x");
+    check_cuda(cudaMalloc(&dy, std::max<size_t>(16, A.m * sv)), "cudaMalloc y");
+    if (sv == 8) {
+      check_cuda(cudaMemcpy(dx, xd.data(), A.n * 8, cudaMemcpyHostToDevice), "H2D x");
+    } else {
+      std::vector<float> xf(xd.begin(), xd.end());
+      check_cuda(cudaMemcpy(dx, xf.data(), A.n * 4, cudaMemcpyHostToDevice), "H2D x");
+    }
+    if (cfg->flush_l2) {
+      int l2 = 0;
+      cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+      flush_bytes = (size_t)std::max(l2, 1 << 20) * 2;
+      check_cuda(cudaMalloc(&flush, flush_bytes), "cudaMalloc flush");
+    }
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  FILE* log = cfg->log_path ? std::fopen(cfg->log_path, "w") : nullptr;
+  Plan* best_plan = nullptr;
+  double best_t = 1e300, best_bytes = 0;
+  std::string best_canon;
+  int tried = 0;
+  const int maxc = cfg->max_candidates > 0 ? cfg->max_candidates : 64;
+  const int reps = std::max(1, cfg->reps), warm = std::max(0, cfg->warmup);
+  double one = 1.0, zero = 0.0;
+  float onef = 1.0f, zerof = 0.0f;
+  const void* alpha = sv == 8 ? (const void*)&one : (const void*)&onef;
+  const void* beta = sv == 8 ? (const void*)&zero : (const void*)&zerof;
+  Rng seq(cfg->seed);
+  for (int i = 0; i < maxc + cfg->n_seed_graphs; ++i) {
+    double el = std::chrono::duration<double>(clk::now() - t_start).count();
+    if (cfg->budget_seconds > 0 && el > cfg->budget_seconds && tried > 0) break;
+    if (i >= cfg->n_seed_graphs && tried >= maxc) break;
+    std::string text = i < cfg->n_seed_graphs ? std::string(cfg->seed_graphs[i]) : random_graph(A, seq.next());
+    std::string status = "ok", canon;
+    double t_med = -1;
+    Plan* P = nullptr;
+    try {
+      Seq g = parse_graph(text);
+      canon = print_graph(g);
+      P = make_plan(A, g, canon, device, stream, 0);
+      as_plan_s h;
+      h.P.reset(P);
+      for (int w = 0; w < warm; ++w)
+        if (as_spmv(&h, alpha, dx, beta, dy, stream) != AS_OK) fail(AS_ERR_CUDA, as_last_error());
+      std::vector<float> ts;
+      for (int rep = 0; rep < reps; ++rep) {
+        if (flush) cudaMemsetAsync(flush, rep & 0xff, flush_bytes, s);
+        cudaEventRecord(e0, s);
+        if (as_spmv(&h, alpha, dx, beta, dy, stream) != AS_OK) fail(AS_ERR_CUDA, as_last_error());
+        cudaEventRecord(e1, s);
+        check_cuda(cudaEventSynchronize(e1), "event sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ts.push_back(ms);
+      }
+      t_med = median(ts);
+      h.P.release();
+      ++tried;
+      bool better = t_med < best_t * 0.99 ||
+                    (t_med <= best_t * 1.01 && (P->info.bytes_model < best_bytes ||
+                                                (P->info.bytes_model == best_bytes && canon < best_canon)));
+      if (!best_plan || better) {
+        delete best_plan;
+        best_plan = P;
+        best_t = std::min(best_t, t_med);
+        best_t = t_med;
+        best_bytes = P->info.bytes_model;
+        best_canon = canon;
+      } else {
+        delete P;
+      }
+    } catch (const Error& e) {
+      status = e.st == AS_ERR_PLAN_INFEASIBLE ? "infeasible" : e.st == AS_ERR_CUDA ? "cuda_error" : "rejected";
+      if (e.st == AS_ERR_CUDA) cudaGetLastError();
+      if (canon.empty()) canon = text;
+      set_last_error(e.msg);
+    }
+    if (log) {
+      std::fprintf(log, "{\"i\": %d, \"graph\": \"%s\", \"status\": \"%s\", \"median_ms\": %.6f}\n", i,
+                   json_escape(canon).c_str(), status.c_str(), t_med);
+      std::fflush(log);
+    }
+  }
+  if (log) std::fclose(log);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(dx);
+  cudaFree(dy);
+  if (flush) cudaFree(flush);
+  cudaSetDevice(cur);
+  if (!best_plan) {
+    set_last_error("as_search: no candidate could be planned");
+    return AS_ERR_NO_FEASIBLE;
+  }
+  auto* h = new as_plan_s();
+  h->P.reset(best_plan);
+  *best = h;
+  if (len) {
+    size_t need = best_canon.size() + 1;
+    if (best_graph && *len >= need) std::memcpy(best_graph, best_canon.c_str(), need);
+    *len = need;
+  }
+  return AS_OK;
+}
+
+}  // namespace as

@@ -1,0 +1,203 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the long-double oracle.
+
+Tolerance (north_star, reading A2/O2): |y - yref| <= tol * (|alpha| sum_j |a_ij x_j| +
+|beta y0_i|) per row, tol = 1e-12 (fp64) / 1e-5 (fp32).  Integer-exact mode: bit-identical.
+Metadata of device plans (AS_PLAN_KEEP_HOST) equals the oracle's byte for byte."""
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import builder_ref as B
+from oracle import graph_ref as G
+from oracle import spmv as S
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+asp = pytest.importorskip("paper_2212_10432_b200")
+
+from test_host import FAMILY_GRAPHS, compare_export  # noqa: E402
+
+
+def _mat(coo):
+    return asp.Matrix.from_coo(coo.m, coo.n, coo.row, coo.col, coo.val)
+
+
+def run_check(coo, graph, alpha=1.0, beta=0.0, int_mode=False, seed=0, keep_host=False, y_nan=False, plan=None):
+    dt = coo.val.dtype
+    x, y0 = synth.vectors(coo.n, coo.m, seed, dt, int_mode)
+    if y_nan:
+        y0[:] = np.nan
+    P = plan or asp.Plan(_mat(coo), graph, device=0, keep_host=keep_host)
+    dx = torch.from_numpy(x).cuda()
+    dy = torch.from_numpy(y0.copy()).cuda()
+    P.spmv(alpha, dx, beta, dy)
+    torch.cuda.synchronize()
+    y = dy.cpu().numpy()
+    yref, bound = S.spmv_coo(coo.m, coo.row, coo.col, coo.val.astype(np.float64), x.astype(np.float64),
+                             alpha, beta, y0.astype(np.float64))
+    if int_mode:
+        assert np.array_equal(y.astype(np.float64), yref.astype(np.float64)), \
+            (graph, np.nonzero(y.astype(np.float64) != yref.astype(np.float64))[0][:10])
+    ok, ratio = S.check(y, yref, bound, dt)
+    assert ok, (graph, ratio)
+    return P, ratio
+
+
+@pytest.mark.parametrize("graph", FAMILY_GRAPHS)
+@pytest.mark.parametrize("seed", range(3))
+def test_family_integer_exact(graph, seed):
+    coo = synth.random_matrix(33 + 40 * seed, 29 + 17 * seed, 0.12 + 0.06 * seed, seed, int_mode=True,
+                              dense_rows=seed % 2)
+    ab = [(1.0, 0.0), (2.0, -1.0), (-0.5, 0.5)][seed]
+    try:
+        P, _ = run_check(coo, graph, *ab, int_mode=True, seed=seed, keep_host=True)
+    except asp.AsError as e:
+        assert e.status == "AS_ERR_PLAN_INFEASIBLE"
+        return
+    compare_export(P, coo, graph)
+
+
+@pytest.mark.parametrize("graph", FAMILY_GRAPHS)
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_family_real(graph, dtype):
+    coo = synth.random_powerlaw(700, 650, 3, 300).astype(dtype)
+    try:
+        run_check(coo, graph, 1.5, -0.5, seed=3)
+    except asp.AsError as e:
+        assert e.status == "AS_ERR_PLAN_INFEASIBLE"
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_random_graphs(seed):
+    """as_search's random legal graphs on ragged matrices spanning many tiles."""
+    dt = np.float64 if seed % 2 == 0 else np.float32
+    coo = synth.random_powerlaw(3000 + 37 * seed, 2500, seed, 1500, int_mode=seed % 3 == 0).astype(dt)
+    text = _mat(coo).random_graph(seed)
+    try:
+        run_check(coo, text, 1.0 if seed % 4 else 2.0, 0.0 if seed % 3 else 1.0, int_mode=seed % 3 == 0, seed=seed)
+    except asp.AsError as e:
+        assert e.status == "AS_ERR_PLAN_INFEASIBLE", (text, e)
+
+
+def test_beta_zero_ignores_nan():
+    coo = synth.random_matrix(50, 40, 0.2, 1)
+    for g in FAMILY_GRAPHS[:4]:
+        run_check(coo, g, 1.0, 0.0, y_nan=True)
+
+
+def test_empty_and_degenerate():
+    # all rows empty
+    coo = synth.Coo(5, 5, np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    run_check(coo, "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED", 1.0, 0.5)
+    # single dense row, single column
+    coo = synth.random_matrix(1, 300, 1.0, 2)
+    for g in FAMILY_GRAPHS:
+        try:
+            run_check(coo, g, 1.0, -1.0)
+        except asp.AsError as e:
+            assert e.status == "AS_ERR_PLAN_INFEASIBLE"
+    coo = synth.random_matrix(300, 1, 1.0, 2)
+    run_check(coo, "COMPRESS; BMT_NNZ_BLOCK(7); THREAD_BITMAP_RED_G; GMEM_ATOM_RED", 1.0, -1.0)
+
+
+def test_preconditions():
+    coo = synth.random_matrix(8, 8, 0.5, 1)
+    P = asp.Plan(_mat(coo), FAMILY_GRAPHS[0], device=0)
+    buf = torch.zeros(64, dtype=torch.float64, device="cuda")
+    with pytest.raises(asp.AsError):
+        P.spmv(1.0, buf[0:8], 0.0, buf[4:12])       # alias
+    with pytest.raises(asp.AsError):
+        P.spmv(1.0, buf[1:9], 0.0, buf[32:40])      # misaligned x
+    hp = asp.Plan(_mat(coo), FAMILY_GRAPHS[0], device=-1)
+    with pytest.raises(asp.AsError):
+        hp.spmv(1.0, buf[0:8], 0.0, buf[32:40])     # host-only plan
+
+
+def test_spmv_host_path():
+    coo = synth.c1_uniform()
+    x, y0 = synth.vectors(coo.n, coo.m, 1)
+    P = asp.Plan(_mat(coo), "COMPRESS; BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; GMEM_ATOM_RED", device=0)
+    y = y0.copy()
+    P.spmv_host(2.0, x, 0.5, y)
+    yref, bound = S.spmv_coo(coo.m, coo.row, coo.col, coo.val, x, 2.0, 0.5, y0)
+    assert S.check(y, yref, bound, np.float64)[0]
+
+
+# ------------------------------------------------------------------ BASELINE configs
+C1_GRAPH = "COMPRESS; BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; SET_RESOURCE(128); GMEM_ATOM_RED"
+
+
+@pytest.mark.parametrize("int_mode", [False, True])
+def test_c1_full(int_mode):
+    coo = synth.c1_uniform(int_mode=int_mode)
+    P, ratio = run_check(coo, C1_GRAPH, 1.5, -0.5, int_mode=int_mode, seed=1, keep_host=True)
+    compare_export(P, coo, C1_GRAPH)
+
+
+C2_GRAPHS = [
+    "DIA_DECOM(theta=0.5,max=8) { DIA; SET_RESOURCE(256) }",
+    "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED",
+    "COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED",
+    "COMPRESS; BMTB_ROW_BLOCK(128); SHMEM_OFFSET_RED; GMEM_ATOM_RED",
+]
+
+
+@pytest.fixture(scope="module")
+def c2():
+    return synth.c2_lap2d(2048)
+
+
+@pytest.mark.parametrize("graph", C2_GRAPHS)
+def test_c2_closed_form(c2, graph):
+    """Full-size C2 (4,194,304 rows): A*1 = number of missing neighbours, exact in fp64."""
+    P = asp.Plan(_mat(c2), graph, device=0)
+    dx = torch.ones(c2.n, dtype=torch.float64, device="cuda")
+    dy = torch.full((c2.m,), 7.0, dtype=torch.float64, device="cuda")
+    P.spmv(1.0, dx, 0.0, dy)
+    torch.cuda.synchronize()
+    g = 2048
+    i = np.arange(c2.m)
+    gx, gy = i % g, i // g
+    want = (gx == 0).astype(float) + (gx == g - 1) + (gy == 0) + (gy == g - 1)
+    assert np.array_equal(dy.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("graph", C2_GRAPHS)
+def test_c2_real_sampled(c2, graph):
+    """Full-size C2 in real mode, alpha/beta != trivial: sampled rows vs the oracle row by row."""
+    x, y0 = synth.vectors(c2.n, c2.m, 2)
+    P = asp.Plan(_mat(c2), graph, device=0)
+    dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y0.copy()).cuda()
+    P.spmv(1.5, dx, -0.5, dy)
+    torch.cuda.synchronize()
+    y = dy.cpu().numpy()
+    rows = np.unique(np.concatenate([np.arange(0, 4096), np.arange(c2.m - 4096, c2.m),
+                                     np.random.default_rng(0).integers(0, c2.m, 20000)]))
+    rp = np.searchsorted(c2.row, np.arange(c2.m + 1))
+    sel = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows])
+    srp = np.concatenate([[0], np.cumsum(rp[rows + 1] - rp[rows])])
+    yref, bound = S.spmv_csr(srp, c2.col[sel], c2.val[sel], x, 1.5, -0.5, y0[rows])
+    ok, ratio = S.check(y[rows], yref, bound, np.float64)
+    assert ok, ratio
+
+
+def test_c2_dia_metadata_closed_form(c2):
+    P = asp.Plan(_mat(c2), C2_GRAPHS[0], device=0, keep_host=True)
+    assert P.export("p0.dia.off").tolist() == [-2048, -1, 0, 1, 2048]
+    dv = P.export("p0.dia.val")
+    assert dv.shape[0] == 5 * c2.m and int((dv == 0).sum()) == 8192
+    info = P.info()
+    assert info["pads"] == 8192 and info["prepass_rows"] == 0
+
+
+def test_search_small():
+    coo = synth.random_powerlaw(4000, 4000, 5, 2000)
+    A = _mat(coo)
+    best, text = asp.search(A, device=0, seed=7, max_candidates=12, budget_seconds=60, warmup=2, reps=5,
+                            seed_graphs=["COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED"])
+    assert G.is_legal(text), text
+    run_check(coo, text, 1.0, 0.0, plan=best)
