@@ -539,7 +539,8 @@ struct Builder {
     } else {
       fail(AS_ERR_PLAN_INFEASIBLE, "no kernel in the sm_100a family implements this mapping/reduction combination");
     }
-    if (P.pad && P.fam != FAM_THREAD_ROW) fail(AS_ERR_PLAN_INFEASIBLE, "BMT_PAD is implemented for THREAD_ROW kernels only");
+    if (P.pad && P.fam != FAM_THREAD_ROW && P.fam != FAM_NNZ_THREAD && P.fam != FAM_NNZ_WARP)
+      fail(AS_ERR_PLAN_INFEASIBLE, "BMT_PAD is implemented for the THREAD_ROW and NNZ kernels only");
   }
 };
 

@@ -259,32 +259,134 @@ __global__ void __launch_bounds__(1024) k_thread_row_pad(DevPart p, const V* __r
 }
 
 // =====================================================================================
-// FAM_NNZ_THREAD: BMT_NNZ_BLOCK(k) + THREAD_BITMAP_RED_G.  Each thread reduces its k
-// nonzeros serially, cutting at bitmap heads (bit j = element j starts a row, A20); rows
-// whose head and end lie in the BMT are exclusive, straddlers go to y by atomics ("_G").
+// BMT element source for the nonzero-split kernels.
+//   PAD = false: the CSR order of COMPRESS; a thread walks k consecutive nonzeros, so the
+//                loads allocate in L1 (the warp's 32*k-element window is reused across j).
+//   PAD = true:  BMT_PAD slot-major layout (reading A18): element j of BMT t sits at
+//                base_g + (j/VEC)*n_t*VEC + lt*VEC + j%VEC, so at every step the 32 lanes of
+//                a warp read 32 consecutive VEC-chunks: fully coalesced streaming loads (the
+//                CSR5 tile transpose expressed with the paper's own padding operator).
 // =====================================================================================
-template <class V>
-__global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
-  const V* val = (const V*)p.val;
-  for (int64_t t = gtid(); t < p.n_bmt; t += gthreads()) {
-    int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
-    int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
-    int64_t row = ldm(p.bmt_first_row + t);
-    const uint32_t* bm = p.bitmap + t * p.bm_words;
-    uint32_t w = ldm(bm);
-    bool inside = w & 1u;  // current segment started at a head inside this BMT
-    double acc = 0.0;
-    for (int64_t j = 0; j < e - a; ++j) {
-      if ((j & 31) == 0 && j) w = ldm(bm + (j >> 5));
-      if (j && ((w >> (j & 31)) & 1u)) {
-        if (inside) write_excl(p, y, row, acc);
-        else write_atom(p, y, row, acc);
+__device__ __forceinline__ double ld_seq(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol_ef()));
+  return v;
+}
+__device__ __forceinline__ float ld_seq(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol_ef()));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_seq(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_ef()));
+  return v;
+}
+
+struct PadPos {
+  int64_t base, stride;
+};
+template <int VEC>
+__device__ __forceinline__ PadPos pad_pos(const DevPart& p, int64_t t) {
+  int64_t g, t0, t1;
+  if (p.grp_regular) {
+    g = t / p.grp_regular;
+    t0 = g * p.grp_regular;
+    t1 = min(t0 + p.grp_regular, p.n_bmt);
+  } else {
+    int64_t lo = 0, hi = p.n_grp - 1;
+    while (lo < hi) {
+      int64_t mid = (lo + hi + 1) >> 1;
+      if (ldm(p.grp_first_bmt + mid) <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    g = lo;
+    t0 = ldm(p.grp_first_bmt + g);
+    t1 = ldm(p.grp_first_bmt + g + 1);
+  }
+  return {ldm(p.grp_base + g) + (t - t0) * VEC, (t1 - t0) * VEC};
+}
+
+// Serial pass over one BMT (THREAD_BITMAP_RED_G): calls seg(row, partial, head_inside) at
+// every bitmap head after element 0; returns the open (last) segment in acc/row/inside.
+template <class V, bool PAD, int VEC, class Seg>
+__device__ __forceinline__ void bmt_pass(const DevPart& p, const V* __restrict__ x, int64_t t, int64_t a, int64_t len,
+                                         int64_t& row, double& acc, bool& inside, Seg seg) {
+  // Batches of KB elements: all value/column loads of a batch are issued, then all x
+  // gathers, then the bitmap-segmented accumulation -> KB independent loads in flight per
+  // thread instead of one element behind each head test.
+  constexpr int KB = 8;  // divides 32, multiple of VEC
+  const uint32_t* bm = p.bitmap + t * p.bm_words;
+  inside = ldm(bm) & 1u;
+  acc = 0.0;
+  PadPos pp{0, 0};
+  if constexpr (PAD) pp = pad_pos<VEC>(p, t);
+  const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;
+  const int32_t* pc = PAD ? p.pad_col + pp.base : p.col + a;
+  for (int64_t j0 = 0; j0 < len; j0 += KB) {
+    double v[KB];
+    int32_t c[KB];
+    if constexpr (PAD) {
+#pragma unroll
+      for (int q = 0; q < KB; q += VEC) {
+        if (j0 + q < len) {
+          PadLoad<V, VEC>::ld(pv + ((j0 + q) / VEC) * pp.stride, pc + ((j0 + q) / VEC) * pp.stride, v + q, c + q);
+        } else {
+#pragma unroll
+          for (int r = 0; r < VEC; ++r) {
+            v[q + r] = 0.0;
+            c[q + r] = 0;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        if (j0 + q < len) {
+          v[q] = (double)ld_seq(pv + j0 + q);
+          c[q] = ld_seq(pc + j0 + q);
+        } else {
+          v[q] = 0.0;
+          c[q] = 0;
+        }
+      }
+    }
+    double xv[KB];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) xv[q] = (j0 + q < len) ? ldx(x, c[q]) : 0.0;
+    const uint32_t wd = ldm(bm + (j0 >> 5)) >> (j0 & 31);
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      const int64_t j = j0 + q;
+      if (j >= len) break;
+      if (j && ((wd >> q) & 1u)) {
+        seg(row, acc, inside);
         ++row;
         acc = 0.0;
         inside = true;
       }
-      acc += (double)ld_stream(val + a + j) * ldx(x, ld_stream(p.col + a + j));
+      acc += v[q] * xv[q];
     }
+  }
+}
+
+// =====================================================================================
+// FAM_NNZ_THREAD: BMT_NNZ_BLOCK(k) + THREAD_BITMAP_RED_G.  Each thread reduces its k
+// nonzeros serially, cutting at bitmap heads (bit j = element j starts a row, A20); rows
+// whose head and end lie in the BMT are exclusive, straddlers go to y by atomics ("_G").
+// =====================================================================================
+template <class V, bool PAD, int VEC>
+__global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  for (int64_t t = gtid(); t < p.n_bmt; t += gthreads()) {
+    int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
+    int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
+    int64_t row = ldm(p.bmt_first_row + t);
+    double acc;
+    bool inside;
+    bmt_pass<V, PAD, VEC>(p, x, t, a, e - a, row, acc, inside, [&](int64_t r, double s, bool in) {
+      if (in) write_excl(p, y, r, s);
+      else write_atom(p, y, r, s);
+    });
     bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
     if (inside && ends) write_excl(p, y, row, acc);
     else write_atom(p, y, row, acc);
@@ -302,9 +404,8 @@ __global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restr
 // Rows closed inside the BMW are exclusive; rows entering from before the BMW or leaving
 // after it are added atomically.
 // =====================================================================================
-template <class V, int WRED>
+template <class V, int WRED, bool PAD, int VEC>
 __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
-  const V* val = (const V*)p.val;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = gthreads() >> 5;
   for (int64_t w = gtid() >> 5; w < p.n_bmw; w += nwarps) {
@@ -326,29 +427,21 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
         int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
         int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
         int64_t row = ldm(p.bmt_first_row + t);
-        const uint32_t* bm = p.bitmap + t * p.bm_words;
-        uint32_t wd = ldm(bm);
-        double cur = 0.0;
-        if (wd & 1u) {
-          hh = true;
-          b0 = true;
-          head_row = row;
-        }
-        for (int64_t j = 0; j < e - a; ++j) {
-          if ((j & 31) == 0 && j) wd = ldm(bm + (j >> 5));
-          if (j && ((wd >> (j & 31)) & 1u)) {
-            if (!hh) {
-              cin = cur;
-              hh = true;
-              head_row = row + 1;
-            } else {
-              write_excl(p, y, row, cur);  // row wholly inside this lane's BMT
-            }
-            ++row;
-            cur = 0.0;
+        head_row = row;
+        double cur;
+        bool in;
+        bool first_open = true;
+        bmt_pass<V, PAD, VEC>(p, x, t, a, e - a, row, cur, in, [&](int64_t r, double s, bool inside) {
+          if (!inside && first_open) {  // continuation of a row begun in an earlier lane
+            cin = s;
+            head_row = r + 1;
+          } else {
+            write_excl(p, y, r, s);  // row wholly inside this lane's BMT
           }
-          cur += (double)ld_stream(val + a + j) * ldx(x, ld_stream(p.col + a + j));
-        }
+          first_open = false;
+        });
+        b0 = ldm(p.bitmap + t * p.bm_words) & 1u;
+        hh = in;
         if (hh) cout = cur;
         else cin = cur;
         last_row = row;
@@ -536,39 +629,105 @@ __global__ void __launch_bounds__(1024) k_block_offset(DevPart p, const V* __res
 
 // =====================================================================================
 // FAM_DIA: y_r = sum_d dia_val[d*stride + i] * x[r + off_d]  (DIA root format).
-// R consecutive rows per thread -> one 16-byte load per diagonal; offsets in the kernel
-// parameter space (constant bank).
+// Each thread owns R = 32 B / sizeof(V) consecutive rows: one 256-bit load per diagonal
+// (sm_100 `ld.global.nc.L2::evict_first.v4.b64` / `.v8.b32`), all D diagonals issued before
+// the first FMA (D templated for D <= 8) so 32*D bytes per thread are in flight; offsets
+// live in the kernel parameter space (constant bank); x gathers hit L1 (the +-1 diagonals
+// reuse the lines of the main diagonal).
 // =====================================================================================
+template <class V>
+struct Ld32;
+template <>
+struct Ld32<double> {
+  static constexpr int R = 4;
+  static __device__ __forceinline__ void ld(const double* p, double* o) {
+    unsigned long long a, b, c, d;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.b64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(p));
+    o[0] = __longlong_as_double((long long)a);
+    o[1] = __longlong_as_double((long long)b);
+    o[2] = __longlong_as_double((long long)c);
+    o[3] = __longlong_as_double((long long)d);
+  }
+};
+template <>
+struct Ld32<float> {
+  static constexpr int R = 8;
+  static __device__ __forceinline__ void ld(const float* p, double* o) {
+    unsigned r[8];
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = (double)__int_as_float((int)r[q]);
+  }
+};
+
 template <class V, int R>
+__device__ __forceinline__ void dia_rows_fma(const DevPart& p, const V* __restrict__ x, int64_t r, int64_t o,
+                                             const double* v, double* acc) {
+  if (r + o >= 0 && r + o + R <= p.n) {  // interior: no bounds checks
+#pragma unroll
+    for (int q = 0; q < R; ++q) acc[q] += v[q] * ldx(x, r + q + o);
+  } else {
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      int64_t c = r + q + o;
+      if (c >= 0 && c < p.n) acc[q] += v[q] * ldx(x, c);
+    }
+  }
+}
+
+template <class V, int BYTES>
+struct LdN;
+template <class V>
+struct LdN<V, 32> {
+  static constexpr int R = Ld32<V>::R;
+  static __device__ __forceinline__ void ld(const V* p, double* o) { Ld32<V>::ld(p, o); }
+};
+template <>
+struct LdN<double, 16> {
+  static constexpr int R = 2;
+  static __device__ __forceinline__ void ld(const double* p, double* o) {
+    double2 t = ld_stream2(p);
+    o[0] = t.x;
+    o[1] = t.y;
+  }
+};
+template <>
+struct LdN<float, 16> {
+  static constexpr int R = 4;
+  static __device__ __forceinline__ void ld(const float* p, double* o) {
+    float4 t = ld_stream4(p);
+    o[0] = t.x;
+    o[1] = t.y;
+    o[2] = t.z;
+    o[3] = t.w;
+  }
+};
+
+template <class V, int DT, int BYTES>
 __global__ void __launch_bounds__(1024) k_dia(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  constexpr int R = LdN<V, BYTES>::R;
   const V* dv = (const V*)p.dia_val;
   for (int64_t i0 = gtid() * R; i0 < p.mb; i0 += gthreads() * R) {
     double acc[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) acc[q] = 0.0;
     const int64_t r = p.r0 + i0;
-#pragma unroll 4
-    for (int d = 0; d < p.D; ++d) {
-      const int64_t o = p.dia_off[d];
-      double v[R];
-      if constexpr (R == 2 && sizeof(V) == 8) {
-        double2 t = ld_stream2((const double*)dv + d * p.dia_stride + i0);
-        v[0] = t.x;
-        v[1] = t.y;
-      } else if constexpr (R == 4 && sizeof(V) == 4) {
-        float4 t = ld_stream4((const float*)dv + d * p.dia_stride + i0);
-        v[0] = t.x;
-        v[1] = t.y;
-        v[2] = t.z;
-        v[3] = t.w;
-      } else {
+    if constexpr (DT > 0) {
+      double v[DT][R];
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = (double)ld_stream(dv + d * p.dia_stride + i0 + q);
-      }
+      for (int d = 0; d < DT; ++d) LdN<V, BYTES>::ld(dv + d * p.dia_stride + i0, v[d]);
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        int64_t c = r + q + o;
-        if (c >= 0 && c < p.n) acc[q] += v[q] * ldx(x, c);
+      for (int d = 0; d < DT; ++d) dia_rows_fma<V, R>(p, x, r, p.dia_off[d], v[d], acc);
+    } else {
+#pragma unroll 2
+      for (int d = 0; d < p.D; ++d) {
+        double v[R];
+        LdN<V, BYTES>::ld(dv + d * p.dia_stride + i0, v);
+        dia_rows_fma<V, R>(p, x, r, p.dia_off[d], v, acc);
       }
     }
 #pragma unroll
@@ -666,13 +825,29 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
         else k_thread_row_pad<V, 4><<<g, tpb, 0, s>>>(p, x, y);
       }
       break;
-    case FAM_NNZ_THREAD:
-      k_nnz_thread<V><<<grid_for(p, p.n_bmt, tpb), tpb, 0, s>>>(p, x, y);
+    case FAM_NNZ_THREAD: {
+      int64_t g = grid_for(p, p.n_bmt, tpb);
+      if (!p.pad) k_nnz_thread<V, false, 1><<<g, tpb, 0, s>>>(p, x, y);
+      else if (p.vec == 1) k_nnz_thread<V, true, 1><<<g, tpb, 0, s>>>(p, x, y);
+      else if (p.vec == 2) k_nnz_thread<V, true, 2><<<g, tpb, 0, s>>>(p, x, y);
+      else k_nnz_thread<V, true, 4><<<g, tpb, 0, s>>>(p, x, y);
       break;
-    case FAM_NNZ_WARP:
-      if (p.variant == 1) k_nnz_warp<V, 1><<<grid_for(p, p.n_bmw, tpb / 32), tpb, 0, s>>>(p, x, y);
-      else k_nnz_warp<V, 2><<<grid_for(p, p.n_bmw, tpb / 32), tpb, 0, s>>>(p, x, y);
+    }
+    case FAM_NNZ_WARP: {
+      int64_t g = grid_for(p, p.n_bmw, tpb / 32);
+#define AS_NW(WR)                                                              \
+  if (!p.pad) k_nnz_warp<V, WR, false, 1><<<g, tpb, 0, s>>>(p, x, y);          \
+  else if (p.vec == 1) k_nnz_warp<V, WR, true, 1><<<g, tpb, 0, s>>>(p, x, y);  \
+  else if (p.vec == 2) k_nnz_warp<V, WR, true, 2><<<g, tpb, 0, s>>>(p, x, y);  \
+  else k_nnz_warp<V, WR, true, 4><<<g, tpb, 0, s>>>(p, x, y);
+      if (p.variant == 1) {
+        AS_NW(1)
+      } else {
+        AS_NW(2)
+      }
+#undef AS_NW
       break;
+    }
     case FAM_WARP_ROW:
       k_warp_row<V><<<grid_for(p, p.n_bmw, tpb / 32), tpb, 0, s>>>(p, x, y);
       break;
@@ -683,8 +858,22 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       k_block_offset<V><<<grid_for(p, p.n_bmtb, 1), tpb, p.smem, s>>>(p, x, y);
       break;
     case FAM_DIA: {
-      constexpr int R = 16 / sizeof(V);
-      k_dia<V, R><<<grid_for(p, (p.mb + R - 1) / R, tpb), tpb, 0, s>>>(p, x, y);
+      // variant 0: 16-byte row groups (higher occupancy), 1: 32-byte (sm_100 256-bit loads)
+      const int R = p.variant == 1 ? LdN<V, 32>::R : LdN<V, 16>::R;
+      int64_t g = grid_for(p, (p.mb + R - 1) / R, tpb);
+#define AS_DIA_CASE(K)                                                          \
+  case K:                                                                       \
+    if (p.variant == 1) k_dia<V, K, 32><<<g, tpb, 0, s>>>(p, x, y);            \
+    else k_dia<V, K, 16><<<g, tpb, 0, s>>>(p, x, y);                           \
+    break;
+      switch (p.D) {
+        AS_DIA_CASE(1) AS_DIA_CASE(2) AS_DIA_CASE(3) AS_DIA_CASE(4)
+        AS_DIA_CASE(5) AS_DIA_CASE(6) AS_DIA_CASE(7) AS_DIA_CASE(8)
+        default:
+          if (p.variant == 1) k_dia<V, 0, 32><<<g, tpb, 0, s>>>(p, x, y);
+          else k_dia<V, 0, 16><<<g, tpb, 0, s>>>(p, x, y);
+      }
+#undef AS_DIA_CASE
       break;
     }
     case FAM_DENSE: {

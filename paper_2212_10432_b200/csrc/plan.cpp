@@ -76,6 +76,27 @@ const void* Plan::up_vals(const std::vector<double>& v, cudaStream_t s, size_t p
   return d;
 }
 
+// BMT_PAD arrays (A18): slot-major values/columns + per-group first BMT, slot base, width.
+void Plan::upload_pad(const HostPart& h, DevPart& d, cudaStream_t s) {
+  const int64_t sv = dt == AS_R64F ? 8 : 4;
+  d.pad = 1;
+  d.vec = h.vec;
+  d.n_grp = (int64_t)h.pad_width.size();
+  // regular groups: every group (but the last) holds the same number of BMTs
+  int64_t per = d.n_grp ? h.grp_first_bmt[1] - h.grp_first_bmt[0] : 0;
+  bool reg = per > 0;
+  for (int64_t g = 0; g < d.n_grp && reg; ++g)
+    if (h.grp_first_bmt[g] != g * per) reg = false;
+  d.grp_regular = reg ? per : 0;
+  d.grp_first_bmt = up_i32(h.grp_first_bmt, s, "grp_first_bmt");
+  d.grp_base = (const int64_t*)up(h.grp_base.data(), h.grp_base.size() * 8, s);
+  d.grp_width = up_i32(h.pad_width, s, "pad_width");
+  d.pad_col = (const int32_t*)up(h.pad_col.data(), h.pad_col.size() * 4, s);
+  cudaStreamSynchronize(s);
+  d.pad_val = up_vals(h.pad_val, s);
+  bytes_model += (double)(h.pad_col.size() * 4 + h.pad_val.size() * sv + d.n_grp * (reg ? 12 : 16));
+}
+
 Plan::~Plan() {
   if (device >= 0) {
     int cur = 0;
@@ -97,7 +118,7 @@ void Plan::upload(cudaStream_t s) {
     d.fam = h.fam;
     d.dtype = dt == AS_R64F ? 1 : 0;
     d.mode = h.mode;
-    d.tpb = h.tpb > 0 ? h.tpb : 256;
+    d.tpb = h.tpb > 0 ? h.tpb : (h.kind == "dia" ? 128 : 256);  // family defaults (C2 sweep)
     d.grid = h.grid;
     d.n = host.n;
     if (h.kind == "dia") {
@@ -107,7 +128,8 @@ void Plan::upload(cudaStream_t s) {
       d.r0 = h.r0;
       d.mb = h.mb;
       d.origin_base = h.r0;
-      const int64_t R = 16 / sv;
+      if (const char* v = std::getenv("AS_DIA_VARIANT")) d.variant = std::atoi(v);  // tuning knob
+      const int64_t R = 32 / sv;  // k_dia reads 32-byte row groups
       d.dia_stride = (h.mb + R - 1) / R * R;
       std::vector<double> padded((size_t)(d.D * d.dia_stride), 0.0);
       for (int i = 0; i < d.D; ++i)
@@ -151,28 +173,13 @@ void Plan::upload(cudaStream_t s) {
             bytes_model += (double)(brp.size() * 4);
           }
           if (h.pad) {
-            d.pad = 1;
-            d.vec = h.vec;
-            d.n_grp = (int64_t)h.pad_width.size();
-            // regular groups: every group (but the last) holds the same number of BMTs
-            int64_t per = d.n_grp ? h.grp_first_bmt[1] - h.grp_first_bmt[0] : 0;
-            bool reg = per > 0;
-            for (int64_t g = 0; g < d.n_grp && reg; ++g)
-              if (h.grp_first_bmt[g] != g * per) reg = false;
-            d.grp_regular = reg ? per : 0;
-            d.grp_first_bmt = up_i32(h.grp_first_bmt, s, "grp_first_bmt");
-            d.grp_base = (const int64_t*)up(h.grp_base.data(), h.grp_base.size() * 8, s);
-            d.grp_width = up_i32(h.pad_width, s, "pad_width");
-            d.pad_col = (const int32_t*)up(h.pad_col.data(), h.pad_col.size() * 4, s);
-            cudaStreamSynchronize(s);
-            d.pad_val = up_vals(h.pad_val, s);
+            upload_pad(h, d, s);
             need_colval = false;
             // row_ptr only for multi-row padded BMTs
             bool multi = false;
             for (int64_t t = 0; t < T.count() && !multi; ++t)
               multi = (t + 1 < T.count() ? T.first_row[t + 1] : mp) - T.first_row[t] > 1;
             need_rowptr = multi;
-            bytes_model += (double)(h.pad_col.size() * 4 + h.pad_val.size() * sv + d.n_grp * 16);
           }
           break;
         }
@@ -189,6 +196,10 @@ void Plan::upload(cudaStream_t s) {
           d.bm_words = h.bm_words;
           d.bitmap = (const uint32_t*)up(h.bitmap.data(), h.bitmap.size() * 4, s);
           bytes_model += (double)(T.first_row.size() * 4 + h.bitmap.size() * 4);
+          if (h.pad) {  // CSR5-like slot-major tiles (BMT_PAD over NNZ BMTs)
+            upload_pad(h, d, s);
+            need_colval = false;
+          }
           if (h.fam == FAM_NNZ_WARP) {
             d.variant = h.red[1] == RED_SEG ? 1 : 2;
             d.n_bmw = W.count();

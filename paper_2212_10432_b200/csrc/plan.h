@@ -28,6 +28,7 @@ struct Plan {
   const int32_t* up_i32(const std::vector<int64_t>& v, cudaStream_t s, const char* what);
   const void* up_vals(const std::vector<double>& v, cudaStream_t s, size_t pad_elems = 0);
   void upload(cudaStream_t s);
+  void upload_pad(const HostPart& h, DevPart& d, cudaStream_t s);
   void compute_model();
 };
 

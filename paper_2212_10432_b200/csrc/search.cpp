@@ -82,7 +82,9 @@ std::string gen_kernel(Rng& r, const Stats& st) {
   if (st.maxlen > 4096) fams.push_back(4);     // block_total only helps long rows
   int f = r.pick(fams);
   std::string s = "COMPRESS; ";
-  std::string tpb = r.coin(0.5) ? "" : "SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{128, 256, 512})) + "); ";
+  std::string tpb = r.coin(0.5) ? ""
+                                : "SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{128, 256, 512})) +
+                                      ",grid=" + std::to_string(r.pick(std::vector<int>{0, 0, 8, 16})) + "); ";
   switch (f) {
     case 0: {  // CSR-scalar / ELL / SELL-P family
       int64_t rows = r.pick(std::vector<int64_t>{32, 64, 128, 256});
@@ -94,21 +96,24 @@ std::string gen_kernel(Rng& r, const Stats& st) {
       if (r.coin(0.6)) {
         std::string scope = bmtb ? (r.coin(0.7) ? "BMTB" : "GLOBAL") : bmw ? "BMW" : "GLOBAL";
         if (scope == "GLOBAL" && st.var > 16) scope = bmtb ? "BMTB" : scope;
-        s += "BMT_PAD(scope=" + scope + "); ";
+        s += "BMT_PAD(scope=" + scope + (r.coin(0.5) ? ",vec=1" : "") + "); ";
       }
       s += "THREAD_TOTAL_RED; ";
       break;
     }
     case 1: {  // nnz-split, thread bitmap reduction (C1 graph family)
       int64_t k = r.pick(std::vector<int64_t>{4, 8, 16, 32});
-      s += "BMT_NNZ_BLOCK(" + std::to_string(k) + "); THREAD_BITMAP_RED_G; ";
+      s += "BMT_NNZ_BLOCK(" + std::to_string(k) + "); ";
+      if (r.coin(0.6)) s += std::string("BMT_PAD(scope=GLOBAL,vec=") + (r.coin(0.5) ? "1" : "0") + "); ";
+      s += "THREAD_BITMAP_RED_G; ";
       break;
     }
     case 2: {  // CSR5-like: warp tiles of nnz + segmented sum
       int64_t k = r.pick(std::vector<int64_t>{4, 8, 16});
       int64_t c = r.pick(std::vector<int64_t>{1, 2, 4});
-      s += "BMW_NNZ_BLOCK(" + std::to_string(32 * k * c) + "); BMT_NNZ_BLOCK(" + std::to_string(k) +
-           "); THREAD_BITMAP_RED_G; " + (r.coin(0.5) ? "WARP_SEG_ADD_RED; " : "WARP_BITMAP_RED; ");
+      s += "BMW_NNZ_BLOCK(" + std::to_string(32 * k * c) + "); BMT_NNZ_BLOCK(" + std::to_string(k) + "); ";
+      if (r.coin(0.6)) s += std::string("BMT_PAD(scope=BMW,vec=") + (r.coin(0.5) ? "1" : "0") + "); ";
+      s += std::string("THREAD_BITMAP_RED_G; ") + (r.coin(0.5) ? "WARP_SEG_ADD_RED; " : "WARP_BITMAP_RED; ");
       break;
     }
     case 3: {  // CSR-vector
@@ -178,7 +183,9 @@ std::string gen_path(Rng& r, const Stats& st, bool can_decom, bool can_sort, boo
     case 5: {
       std::string s = "DIA_DECOM(theta=" + std::string(r.pick(std::vector<const char*>{"0.5", "0.7", "0.9"})) +
                       ",max=" + std::to_string(r.pick(std::vector<int64_t>{4, 8, 16, 32})) + ") { DIA";
-      if (r.coin(0.5)) s += "; SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{128, 256, 512})) + ")";
+      if (r.coin(0.7))
+        s += "; SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{64, 128, 256, 512})) +
+             ",grid=" + std::to_string(r.pick(std::vector<int>{0, 4, 8, 16})) + ")";
       return s + " | " + gen_path(r, st, false, can_sort, false, depth + 1) + " }";
     }
     case 6: {
