@@ -337,3 +337,102 @@ def _fill_band_rows(g, r0, r1, L, lo, hi, row_ptr, col):
 def csr_to_coo(m, n, row_ptr, col, val, name="") -> Coo:
     row = np.repeat(np.arange(m, dtype=np.int64), np.diff(row_ptr))
     return Coo(m, n, row, col.astype(np.int64), val, name)
+
+
+# ----------------------------------------------------------------------------------
+# Fast multithreaded C generators for the full-size configs (synth/gen.c)
+# ----------------------------------------------------------------------------------
+@dataclasses.dataclass
+class Csr:
+    m: int
+    n: int
+    row_ptr: np.ndarray  # int64[m+1]
+    col: np.ndarray      # int32[nnz], ascending within a row
+    val: np.ndarray
+    name: str = ""
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1])
+
+    def to_coo(self) -> Coo:
+        return csr_to_coo(self.m, self.n, self.row_ptr, self.col, self.val, self.name)
+
+    def rows(self, rows):
+        """Sub-CSR of the given rows (for sampled oracle checks)."""
+        rows = np.asarray(rows, np.int64)
+        a, e = self.row_ptr[rows], self.row_ptr[rows + 1]
+        rp = np.concatenate([[0], np.cumsum(e - a)])
+        idx = np.concatenate([np.arange(x, y) for x, y in zip(a, e)]) if rows.shape[0] else np.zeros(0, np.int64)
+        return rp, self.col[idx].astype(np.int64), self.val[idx]
+
+
+_GEN = None
+
+
+def _gen():
+    global _GEN
+    if _GEN is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        src, lib = os.path.join(here, "gen.c"), os.path.join(here, "libsynth.so")
+        if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(src):
+            subprocess.check_call(["gcc", "-O3", "-shared", "-fPIC", "-pthread", src, "-o", lib])
+        L = ctypes.CDLL(lib)
+        i64, vp, u64 = ctypes.c_int64, ctypes.c_void_p, ctypes.c_uint64
+        L.synth_values.argtypes = [u64, i64, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int]
+        L.synth_c5.argtypes = [i64, i64, i64, u64, vp, vp, ctypes.c_int]
+        L.synth_c4.argtypes = [i64, i64, i64, i64, u64, vp, vp, vp, ctypes.c_int]
+        L.synth_c3.argtypes = [ctypes.c_int, i64, ctypes.c_double, ctypes.c_double, ctypes.c_double, u64, vp, vp,
+                               ctypes.c_int]
+        _GEN = L
+    return _GEN
+
+
+def _nth():
+    import os
+    return os.cpu_count() or 1
+
+
+def _fast_values(seed, nnz, dtype, int_mode):
+    val = np.empty(nnz, dtype)
+    _gen().synth_values(seed, nnz, int(int_mode), int(np.dtype(dtype) == np.float32), val.ctypes.data, _nth())
+    return val
+
+
+def c5_band_csr(m: int = 67_108_864, nnz: int = 1 << 30, band: int = 4096, seed: int = 5,
+                dtype=np.float64, int_mode: bool = False) -> Csr:
+    """C5 band-irreg-64m (BASELINE configs[4]) via synth/gen.c."""
+    rp = np.empty(m + 1, np.int64)
+    col = np.empty(nnz, np.int32)
+    rc = _gen().synth_c5(m, nnz, band, seed, rp.ctypes.data, col.ctypes.data, _nth())
+    if rc:
+        raise ValueError("C5 row-length adjustment failed (nnz not reachable)")
+    return Csr(m, m, rp, col, _fast_values(seed, nnz, dtype, int_mode), "band-irreg")
+
+
+def c4_blockdense_csr(m: int = 8_388_608, b: int = 64, n_tiles: int = 24_576, nnz: int = 200_000_000,
+                      seed: int = 4, dtype=np.float64, int_mode: bool = False):
+    """C4 blockdense-8m (BASELINE configs[3]) via synth/gen.c -> (Csr, tiles[(I, J)] sorted)."""
+    rp = np.empty(m + 1, np.int64)
+    col = np.empty(nnz, np.int32)
+    tiles = np.empty((n_tiles, 2), np.int64)
+    rc = _gen().synth_c4(m, b, n_tiles, nnz, seed, tiles.ctypes.data, rp.ctypes.data, col.ctypes.data, _nth())
+    if rc:
+        raise ValueError(f"C4 generation failed ({rc})")
+    tiles = tiles[np.lexsort((tiles[:, 1], tiles[:, 0]))]
+    return Csr(m, m, rp, col, _fast_values(seed, nnz, dtype, int_mode), "blockdense"), tiles
+
+
+def c3_rmat_csr(scale: int = 24, nnz: int = 1 << 28, seed: int = 3, dtype=np.float32, int_mode: bool = False,
+                abcd=(0.57, 0.19, 0.19, 0.05)) -> Csr:
+    """C3 rmat-24 (BASELINE configs[2]) via synth/gen.c."""
+    n = 1 << scale
+    rp = np.empty(n + 1, np.int64)
+    col = np.empty(nnz, np.int32)
+    rc = _gen().synth_c3(scale, nnz, abcd[0], abcd[1], abcd[2], seed, rp.ctypes.data, col.ctypes.data, _nth())
+    if rc:
+        raise ValueError(f"C3 generation failed ({rc})")
+    return Csr(n, n, rp, col, _fast_values(seed, nnz, dtype, int_mode), f"rmat-{scale}")
