@@ -95,19 +95,35 @@ def load_config(name, int_mode=False):
         return synth.c1_uniform(int_mode=int_mode), "uniform-1k", [
             "COMPRESS; BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; SET_RESOURCE(128); GMEM_ATOM_RED"]
     if name == "c4":
-        coo, _ = synth.c4_blockdense()
+        coo, _ = synth.c4_blockdense_csr()
         return coo, "blockdense-8m", [
             "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }"]
     if name == "c3":
-        return synth.c3_rmat(), "rmat-24", [
-            "BIN(t=[32,2048]) { COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED | COMPRESS; BMTB_NNZ_BLOCK(2048); SHMEM_OFFSET_RED; GMEM_ATOM_RED | COMPRESS; BMTB_NNZ_BLOCK(2048); SHMEM_TOTAL_RED; GMEM_ATOM_RED }"]
+        return synth.c3_rmat_csr(), "rmat-24", [
+            "BIN(t=[32,2048]) { COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED"
+            " | COMPRESS; BMTB_NNZ_BLOCK(2048); SHMEM_OFFSET_RED; GMEM_ATOM_RED"
+            " | COMPRESS; BMTB_ROW_BLOCK(1); BMW_NNZ_BLOCK(2048); WARP_TOTAL_RED; GMEM_ATOM_RED }",
+            "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,1); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED"]
+    if name == "c5":
+        return synth.c5_band_csr(), "band-irreg-64m", [
+            "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
+            "COMPRESS; BMTB_ROW_BLOCK(256); SORT_BMTB; BMW_ROW_BLOCK(32); BMT_ROW_BLOCK(1); BMT_PAD(BMW); THREAD_TOTAL_RED; GMEM_ATOM_RED"]
     raise SystemExit(f"unknown config {name}")
 
 
 def csr_of(coo):
+    """row_ptr of a synth.Coo or synth.Csr."""
+    if isinstance(coo, synth.Csr):
+        return coo.row_ptr
     rp = np.zeros(coo.m + 1, np.int64)
     np.add.at(rp, coo.row + 1, 1)
     return np.cumsum(rp)
+
+
+def to_csr(obj):
+    if isinstance(obj, synth.Csr):
+        return obj
+    return synth.Csr(obj.m, obj.n, csr_of(obj), obj.col.astype(np.int32), obj.val, obj.name)
 
 
 def reference_arm(args, coo, wl):
@@ -179,6 +195,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     coo, wl, seeds = load_config(args.config)
+    coo = to_csr(coo)
     if args.impl == "reference":
         if rank == 0:
             reference_arm(args, coo, wl)
@@ -193,7 +210,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    A_full = asp.Matrix.from_coo(coo.m, coo.n, coo.row, coo.col, coo.val)
+    A_full = asp.Matrix.from_csr(coo.m, coo.n, coo.row_ptr, coo.col, coo.val)
     cuts = A_full.row_cuts(world)
     r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
     A = A_full if world == 1 else A_full.row_slice(r0, r1)

@@ -127,7 +127,8 @@ void as_plan_destroy(as_plan_t);
 
 /* ---------------------------------------------------------------- a5-a6: SpMV
  * y = alpha*A*x + beta*y.  x[n], y[m] device pointers of the plan's dtype and device,
- * 16-byte aligned, non-aliasing; alpha/beta point to HOST scalars of the plan's dtype.
+ * aligned to the value size, non-aliasing (a ROW_DIV band may write into a slice of a
+ * larger y); alpha/beta point to HOST scalars of the plan's dtype.
  * beta == 0: y is write-only (NaN in y not propagated).  Asynchronous on `stream`;
  * device faults surface as AS_ERR_CUDA at a later call. */
 as_status_t as_spmv(as_plan_t, const void* alpha, const void* x, const void* beta, void* y,

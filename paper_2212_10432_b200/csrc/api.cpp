@@ -284,8 +284,8 @@ as_status_t as_spmv(as_plan_t h, const void* alpha, const void* x, const void* b
     Plan& P = *h->P;
     if (P.device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan cannot run as_spmv");
     if ((P.n > 0 && !x) || (P.m > 0 && !y)) fail(AS_ERR_INVALID_ARG, "NULL x or y");
-    if (((uintptr_t)x | (uintptr_t)y) & 15) fail(AS_ERR_INVALID_ARG, "x and y must be 16-byte aligned");
     const size_t sv = P.dt == AS_R64F ? 8 : 4;
+    if (((uintptr_t)x | (uintptr_t)y) & (sv - 1)) fail(AS_ERR_INVALID_ARG, "x and y must be aligned to the value size");
     if (x && y && (const char*)x < (const char*)y + P.m * sv && (const char*)y < (const char*)x + P.n * sv)
       fail(AS_ERR_INVALID_ARG, "x and y alias");
     double a = P.dt == AS_R64F ? *(const double*)alpha : (double)*(const float*)alpha;

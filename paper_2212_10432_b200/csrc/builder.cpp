@@ -492,6 +492,12 @@ struct Builder {
       base += (t - t0) * W;
     }
     P.grp_first_bmt.push_back(t);
+    // P4b: the padded layout may not exceed 4x the nonzeros (+1M slots); an
+    // ELL over a power-law matrix would otherwise need max_len x rows slots.
+    const int64_t nnz = bt.start.empty() ? 0 : bt.start.back();
+    if (base > 4 * nnz + (int64_t(1) << 20))
+      fail(AS_ERR_PLAN_INFEASIBLE, "P4b: BMT_PAD would store " + std::to_string(base) + " slots for " +
+                                       std::to_string(nnz) + " nonzeros (padding rate above 4x)");
     P.pad_col.assign((size_t)base, 0);
     P.pad_val.assign((size_t)base, 0.0);
     for (int64_t g = 0; g < ng; ++g) {

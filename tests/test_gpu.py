@@ -111,7 +111,7 @@ def test_preconditions():
     with pytest.raises(asp.AsError):
         P.spmv(1.0, buf[0:8], 0.0, buf[4:12])       # alias
     with pytest.raises(asp.AsError):
-        P.spmv(1.0, buf[1:9], 0.0, buf[32:40])      # misaligned x
+        P.spmv(1.0, buf.data_ptr() + 4, 0.0, buf[32:40])  # x not aligned to 8 bytes
     hp = asp.Plan(_mat(coo), FAMILY_GRAPHS[0], device=-1)
     with pytest.raises(asp.AsError):
         hp.spmv(1.0, buf[0:8], 0.0, buf[32:40])     # host-only plan

@@ -26,7 +26,8 @@ def main():
     import synth
     import paper_2212_10432_b200 as asp
     coo, wl, _ = bench.load_config(args.config)
-    A = asp.Matrix.from_coo(coo.m, coo.n, coo.row, coo.col, coo.val)
+    coo = bench.to_csr(coo)
+    A = asp.Matrix.from_csr(coo.m, coo.n, coo.row_ptr, coo.col, coo.val)
     x, y0 = synth.vectors(coo.n, coo.m, 2, coo.val.dtype)
     dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y0).cuda()
     flush = torch.empty(2 * torch.cuda.get_device_properties(0).L2_cache_size, dtype=torch.uint8, device="cuda")
