@@ -8,6 +8,9 @@
 // ROW/COL_DIV, A12 DIA_DECOM, A13 DENSE_DECOM, A14 COMPRESS, A15 block cutting, A16 P1
 // checks, A17 implicit arrays, A18 BMT_PAD, A19 SORT_BMTB, A20 bitmaps, A22 writer rule.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -47,6 +50,15 @@ std::vector<int64_t> row_lengths(const Matrix& A, const BState& st) {
 // Stable permutation by descending length within [a, e) of idx (A7).
 void stable_desc(std::vector<int64_t>& idx, const std::vector<int64_t>& len, size_t a, size_t e) {
   std::stable_sort(idx.begin() + a, idx.begin() + e, [&](int64_t x, int64_t y) { return len[x] > len[y]; });
+}
+
+// AS_TRACE=1: phase timings of the builder on stderr (developer aid)
+void trace(const char* phase) {
+  static const bool on = std::getenv("AS_TRACE") != nullptr;
+  static auto last = std::chrono::steady_clock::now();
+  auto now = std::chrono::steady_clock::now();
+  if (on) std::fprintf(stderr, "[as_plan] %-24s %8.3f s\n", phase, std::chrono::duration<double>(now - last).count());
+  last = now;
 }
 
 int64_t row_of(const std::vector<int64_t>& rp, int64_t e) {
@@ -316,6 +328,7 @@ struct Builder {
       }
     });
 
+    trace("compress");
     // collect the mapping / implementing operators
     std::vector<int> order;
     const Op* pad = nullptr;
@@ -353,14 +366,17 @@ struct Builder {
       if (l == 0 && P.sort_bmtb) sort_bmtb(P);
       parent = lv.start;
     }
+    trace("cut+sort_bmtb");
     for (int l : order) first_rows(P.row_ptr, P.lv[l]);
+    trace("first_rows");
 
     // P1 (A16): X_TOTAL_RED needs every level-X block inside one row
     for (int l = 0; l < 3; ++l) {
       if (P.red[l] != RED_TOTAL) continue;
       Level& lv = P.lv[l];
+      // a block [a, e) lies in one row iff its last element is before the next row start
       for (int64_t t = 0; t < lv.count(); ++t)
-        if (row_of(P.row_ptr, lv.start[t + 1] - 1) != lv.first_row[t])
+        if (lv.start[t + 1] > P.row_ptr[lv.first_row[t] + 1])
           fail(AS_ERR_PLAN_INFEASIBLE, std::string("P1: ") + (l == 0 ? "SHMEM" : l == 1 ? "WARP" : "THREAD") +
                                            "_TOTAL_RED but a block spans rows");
     }
@@ -370,16 +386,20 @@ struct Builder {
       Level& bt = P.lv[2];
       P.bm_words = (int)((bt.size + 31) / 32);
       P.bitmap.assign((size_t)(bt.count() * P.bm_words), 0u);
-      int64_t t = 0;
-      for (int64_t r = 0; r < mp; ++r) {
-        int64_t h = P.row_ptr[r];
-        while (bt.start[t + 1] <= h) ++t;
-        int64_t j = h - bt.start[t];
-        P.bitmap[(size_t)(t * P.bm_words + j / 32)] |= 1u << (j % 32);
-      }
+      parallel_for(mp, [&](int64_t ra, int64_t re) {
+        int64_t t = ra < mp ? std::upper_bound(bt.start.begin(), bt.start.end(), P.row_ptr[ra]) - bt.start.begin() - 1 : 0;
+        for (int64_t r = ra; r < re; ++r) {
+          int64_t h = P.row_ptr[r];
+          while (bt.start[t + 1] <= h) ++t;
+          int64_t j = h - bt.start[t];
+          __atomic_fetch_or(&P.bitmap[(size_t)(t * P.bm_words + j / 32)], 1u << (j % 32), __ATOMIC_RELAXED);
+        }
+      });
     }
 
+    trace("p1+bitmap");
     if (pad) build_pad(P, *pad);
+    trace("pad");
 
     // writer units: blocks of the highest level carrying a reduction (A21/A22)
     int top = -1;
@@ -401,6 +421,7 @@ struct Builder {
         (ex ? P.excl : P.atom).push_back(P.origin[r]);
       }
     }
+    trace("writer_units");
     lower(P);
     hp.parts.push_back(std::move(P));
   }
@@ -445,20 +466,29 @@ struct Builder {
     std::vector<int64_t> len(mp), perm(mp);
     for (int64_t r = 0; r < mp; ++r) len[r] = P.row_ptr[r + 1] - P.row_ptr[r];
     std::iota(perm.begin(), perm.end(), 0);
-    for (int64_t b = 0; b < bt.count(); ++b) {
-      int64_t ra = row_of(P.row_ptr, bt.start[b]), re = row_of(P.row_ptr, bt.start[b + 1] - 1) + 1;
-      stable_desc(perm, len, ra, re);
-    }
+    parallel_for(
+        bt.count(),
+        [&](int64_t b0, int64_t b1) {
+          for (int64_t b = b0; b < b1; ++b) {
+            int64_t ra = row_of(P.row_ptr, bt.start[b]), re = row_of(P.row_ptr, bt.start[b + 1] - 1) + 1;
+            stable_desc(perm, len, ra, re);
+          }
+        },
+        1 << 10);
     std::vector<int64_t> org(mp), rp(mp + 1, 0);
     std::vector<int32_t> col(P.col.size());
     std::vector<double> val(P.val.size());
     for (int64_t i = 0; i < mp; ++i) {
-      int64_t r = perm[i];
-      org[i] = P.origin[r];
-      rp[i + 1] = rp[i] + len[r];
-      std::copy(P.col.begin() + P.row_ptr[r], P.col.begin() + P.row_ptr[r + 1], col.begin() + rp[i]);
-      std::copy(P.val.begin() + P.row_ptr[r], P.val.begin() + P.row_ptr[r + 1], val.begin() + rp[i]);
+      org[i] = P.origin[perm[i]];
+      rp[i + 1] = rp[i] + len[perm[i]];
     }
+    parallel_for(mp, [&](int64_t a, int64_t e) {
+      for (int64_t i = a; i < e; ++i) {
+        int64_t r = perm[i];
+        std::copy(P.col.begin() + P.row_ptr[r], P.col.begin() + P.row_ptr[r + 1], col.begin() + rp[i]);
+        std::copy(P.val.begin() + P.row_ptr[r], P.val.begin() + P.row_ptr[r + 1], val.begin() + rp[i]);
+      }
+    });
     P.origin.swap(org);
     P.row_ptr.swap(rp);
     P.col.swap(col);
@@ -500,9 +530,10 @@ struct Builder {
                                        std::to_string(nnz) + " nonzeros (padding rate above 4x)");
     P.pad_col.assign((size_t)base, 0);
     P.pad_val.assign((size_t)base, 0.0);
-    for (int64_t g = 0; g < ng; ++g) {
-      int64_t t0 = P.grp_first_bmt[g], t1 = P.grp_first_bmt[g + 1], nt = t1 - t0, W = P.pad_width[g];
-      for (int64_t tt = t0; tt < t1; ++tt) {
+    // fill: groups are independent; GLOBAL scope (one group) splits over its BMTs
+    auto fill = [&](int64_t g, int64_t ta, int64_t te) {
+      int64_t t0 = P.grp_first_bmt[g], nt = P.grp_first_bmt[g + 1] - t0, W = P.pad_width[g];
+      for (int64_t tt = ta; tt < te; ++tt) {
         int64_t a = bt.start[tt], e = bt.start[tt + 1], lt = tt - t0;
         for (int64_t j = 0; j < W; ++j) {
           int64_t slot = P.grp_base[g] + (j / vec) * nt * vec + lt * vec + (j % vec);
@@ -514,6 +545,16 @@ struct Builder {
           }
         }
       }
+    };
+    if (ng == 1) {
+      parallel_for(P.grp_first_bmt[1], [&](int64_t a, int64_t e) { fill(0, a, e); }, 1 << 12);
+    } else {
+      parallel_for(
+          ng,
+          [&](int64_t a, int64_t e) {
+            for (int64_t g = a; g < e; ++g) fill(g, P.grp_first_bmt[g], P.grp_first_bmt[g + 1]);
+          },
+          1 << 8);
     }
   }
 
@@ -594,7 +635,9 @@ HostPlan build_plan(const Matrix& A, const Seq& g) {
   b.run(g, std::move(st));
   writer_rule(hp);
   std::vector<uint8_t> seen(A.n, 0);
-  for (auto c : A.col) seen[c] = 1;
+  parallel_for(A.nnz(), [&](int64_t a, int64_t e) {
+    for (int64_t i = a; i < e; ++i) __atomic_store_n(&seen[A.col[i]], (uint8_t)1, __ATOMIC_RELAXED);
+  });
   hp.distinct_cols = std::accumulate(seen.begin(), seen.end(), (int64_t)0);
   return hp;
 }

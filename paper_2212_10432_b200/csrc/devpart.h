@@ -42,6 +42,8 @@ struct DevPart {
   const int32_t* bmt_first_row = nullptr;
   const uint32_t* bitmap = nullptr;
   int bm_words = 0;
+  const uint32_t* bits = nullptr;         // tile form: packed head bits, 1 per nonzero
+  int tile = 0;                           // NNZ_WARP tile kernel (k in {1,2,4})
   // BMW level
   int64_t n_bmw = 0;
   const int32_t* bmw_bmt_ptr = nullptr;   // NNZ_WARP: BMT range per BMW; NULL -> bmts_per_bmw
@@ -58,6 +60,7 @@ struct DevPart {
   // BMT_PAD (slot-major interleaved)
   int pad = 0, vec = 1;
   int64_t n_grp = 0, grp_regular = 0;     // BMTs per group if regular, else 0
+  int pad_grp_bmw = 0;                    // pad groups are exactly the BMWs (scope=BMW)
   const int32_t* grp_first_bmt = nullptr; // n_grp + 1
   const int64_t* grp_base = nullptr;      // n_grp slot offsets
   const int32_t* grp_width = nullptr;     // n_grp

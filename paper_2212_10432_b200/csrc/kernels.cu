@@ -70,10 +70,23 @@ __device__ __forceinline__ int4 ld_stream_i4(const int32_t* p) {
                : "l"(p), "l"(pol_ef()));
   return v;
 }
-// x gathers: reused across rows -> default caching through L1 (non-coherent path).
-template <class V>
-__device__ __forceinline__ double ldx(const V* x, int64_t c) {
-  return (double)__ldg(x + c);
+// x gathers: reused across rows -> cached in L1 (non-coherent path) and kept in L2 with an
+// evict_last policy while the evict_first matrix streams pass through (the "L2 persistence
+// window for x" of north_star, expressed per load).
+__device__ __forceinline__ uint64_t pol_el() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ldx(const double* x, int64_t c) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
+  return v;
+}
+__device__ __forceinline__ double ldx(const float* x, int64_t c) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  return (double)v;
 }
 // metadata: small, reused by neighbours -> plain non-coherent load
 __device__ __forceinline__ int32_t ldm(const int32_t* p) { return __ldg(p); }
@@ -109,6 +122,24 @@ __device__ __forceinline__ double warp_sum(double v) {
 __device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int64_t gthreads() { return (int64_t)gridDim.x * blockDim.x; }
 
+// Unit distribution for persistent grids: CTA-blocked (CTA c owns a contiguous range of
+// units), interleaved inside the CTA (consecutive warps / threads take consecutive units).
+// All warps of an SM then work on neighbouring rows, so their x windows share L1; with one
+// unit per warp / thread (grid = 0) this is the plain one-to-one mapping.
+struct Units {
+  int64_t begin, end, step;
+};
+__device__ __forceinline__ Units warp_units(int64_t n) {
+  const int64_t wpc = blockDim.x >> 5, per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b = (int64_t)blockIdx.x * per;
+  return {b + (threadIdx.x >> 5), min(b + per, n), wpc};
+}
+__device__ __forceinline__ Units thread_units(int64_t n) {
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b = (int64_t)blockIdx.x * per;
+  return {b + threadIdx.x, min(b + per, n), (int64_t)blockDim.x};
+}
+
 // =====================================================================================
 // FAM_THREAD_ROW: BMT_ROW_BLOCK(s) [+ROW parents] + THREAD_TOTAL / THREAD_BITMAP_RED_G.
 // CSR-Scalar when unpadded; ELL / SELL-P (slot-major interleaved) with
@@ -117,7 +148,7 @@ __device__ __forceinline__ int64_t gthreads() { return (int64_t)gridDim.x * bloc
 template <class V>
 __global__ void __launch_bounds__(1024) k_thread_row(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const V* val = (const V*)p.val;
-  for (int64_t t = gtid(); t < p.n_bmt; t += gthreads()) {
+  for (int64_t t = thread_units(p.n_bmt).begin, t_e = thread_units(p.n_bmt).end; t < t_e; t += blockDim.x) {
     int64_t r0 = p.bmt_row_ptr ? ldm(p.bmt_row_ptr + t) : t * p.s;
     int64_t r1 = p.bmt_row_ptr ? ldm(p.bmt_row_ptr + t + 1) : min((t + 1) * p.s, p.m_p);
     for (int64_t r = r0; r < r1; ++r) {
@@ -201,7 +232,7 @@ struct PadLoad<double, 4> {
 template <class V, int VEC>
 __global__ void __launch_bounds__(1024) k_thread_row_pad(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const V* pval = (const V*)p.pad_val;
-  for (int64_t t = gtid(); t < p.n_bmt; t += gthreads()) {
+  for (int64_t t = thread_units(p.n_bmt).begin, t_e = thread_units(p.n_bmt).end; t < t_e; t += blockDim.x) {
     int64_t g, t0, t1;
     if (p.grp_regular) {
       g = t / p.grp_regular;
@@ -310,20 +341,18 @@ __device__ __forceinline__ PadPos pad_pos(const DevPart& p, int64_t t) {
 // Serial pass over one BMT (THREAD_BITMAP_RED_G): calls seg(row, partial, head_inside) at
 // every bitmap head after element 0; returns the open (last) segment in acc/row/inside.
 template <class V, bool PAD, int VEC, class Seg>
-__device__ __forceinline__ void bmt_pass(const DevPart& p, const V* __restrict__ x, int64_t t, int64_t a, int64_t len,
-                                         int64_t& row, double& acc, bool& inside, Seg seg) {
+__device__ __forceinline__ void bmt_pass(const DevPart& p, const V* __restrict__ x, const uint32_t* bm, PadPos pp,
+                                         int64_t a, int len, int64_t& row, double& acc, bool& inside, Seg seg) {
   // Batches of KB elements: all value/column loads of a batch are issued, then all x
   // gathers, then the bitmap-segmented accumulation -> KB independent loads in flight per
-  // thread instead of one element behind each head test.
+  // thread instead of one element behind each head test.  pp: slot base/stride of this
+  // BMT in the padded layout, computed by the caller (no per-BMT division).
   constexpr int KB = 8;  // divides 32, multiple of VEC
-  const uint32_t* bm = p.bitmap + t * p.bm_words;
   inside = ldm(bm) & 1u;
   acc = 0.0;
-  PadPos pp{0, 0};
-  if constexpr (PAD) pp = pad_pos<VEC>(p, t);
   const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;
   const int32_t* pc = PAD ? p.pad_col + pp.base : p.col + a;
-  for (int64_t j0 = 0; j0 < len; j0 += KB) {
+  for (int j0 = 0; j0 < len; j0 += KB) {
     double v[KB];
     int32_t c[KB];
     if constexpr (PAD) {
@@ -377,16 +406,19 @@ __device__ __forceinline__ void bmt_pass(const DevPart& p, const V* __restrict__
 // =====================================================================================
 template <class V, bool PAD, int VEC>
 __global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
-  for (int64_t t = gtid(); t < p.n_bmt; t += gthreads()) {
+  for (int64_t t = thread_units(p.n_bmt).begin, t_e = thread_units(p.n_bmt).end; t < t_e; t += blockDim.x) {
     int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
     int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
     int64_t row = ldm(p.bmt_first_row + t);
     double acc;
     bool inside;
-    bmt_pass<V, PAD, VEC>(p, x, t, a, e - a, row, acc, inside, [&](int64_t r, double s, bool in) {
-      if (in) write_excl(p, y, r, s);
-      else write_atom(p, y, r, s);
-    });
+    PadPos pp{0, 0};
+    if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
+    bmt_pass<V, PAD, VEC>(p, x, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, acc, inside,
+                          [&](int64_t r, double s, bool in) {
+                            if (in) write_excl(p, y, r, s);
+                            else write_atom(p, y, r, s);
+                          });
     bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
     if (inside && ends) write_excl(p, y, row, acc);
     else write_atom(p, y, row, acc);
@@ -404,11 +436,207 @@ __global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restr
 // Rows closed inside the BMW are exclusive; rows entering from before the BMW or leaving
 // after it are added atomically.
 // =====================================================================================
+// Warp-level combine of per-lane partials (one round of 32 consecutive BMTs).
+//   hh: lane holds a row head; cin: partial before its first head (all of it if none);
+//   cout: partial from its last head to its end; carry: open segment entering the round.
+// Outputs per lane: closing = total of the row closed at the lane's first head (+ whether
+// that row started inside the BMW), v_end = open segment value at the lane's end.
+template <int WRED>
+__device__ __forceinline__ void warp_combine(int lane, bool hh, double cin, double cout, double carry,
+                                             bool carry_inside, double& closing, bool& closing_inside,
+                                             double& v_end, bool& inside_end) {
+  if (WRED == 1) {  // WARP_SEG_ADD_RED: segmented inclusive scan (Blelloch segment sum)
+    double v = hh ? cout : cin;
+    bool f = hh;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      double nv = __shfl_up_sync(0xffffffffu, v, d);
+      bool nf = __shfl_up_sync(0xffffffffu, (int)f, d);
+      if (lane >= d) {
+        if (!f) v += nv;
+        f = f || nf;
+      }
+    }
+    if (!f) v += carry;
+    v_end = v;
+    inside_end = f ? true : carry_inside;
+    double pv = __shfl_up_sync(0xffffffffu, v_end, 1);
+    bool pin = __shfl_up_sync(0xffffffffu, (int)inside_end, 1);
+    if (lane == 0) {
+      pv = carry;
+      pin = carry_inside;
+    }
+    closing = pv + cin;
+    closing_inside = pin;
+  } else {  // WARP_BITMAP_RED: lane head bitmap (ballot) + plain prefix sums
+    const unsigned mask = __ballot_sync(0xffffffffu, hh);
+    double P = hh ? 0.0 : cin;  // non-head lanes contribute wholly to the open segment
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      double nv = __shfl_up_sync(0xffffffffu, P, d);
+      if (lane >= d) P += nv;
+    }
+    const unsigned below = mask & ((1u << lane) - 1u);  // previous head lane strictly below
+    const int h = below ? 31 - __clz(below) : -1;
+    const int hs = h < 0 ? 0 : h;
+    double cout_h = __shfl_sync(0xffffffffu, cout, hs);
+    double P_h = __shfl_sync(0xffffffffu, P, hs);
+    double P_prev = __shfl_up_sync(0xffffffffu, P, 1);
+    if (lane == 0) P_prev = 0.0;
+    if (h >= 0) {
+      closing = cout_h + (P_prev - P_h) + cin;
+      closing_inside = true;
+    } else {
+      closing = carry + P_prev + cin;
+      closing_inside = carry_inside;
+    }
+    const unsigned upto = mask & (lane == 31 ? 0xffffffffu : ((1u << (lane + 1)) - 1u));
+    const int h2 = upto ? 31 - __clz(upto) : -1;
+    const int h2s = h2 < 0 ? 0 : h2;
+    double cout_h2 = __shfl_sync(0xffffffffu, cout, h2s);
+    double P_h2 = __shfl_sync(0xffffffffu, P, h2s);
+    if (h2 >= 0) {
+      v_end = cout_h2 + (P - P_h2);
+      inside_end = true;
+    } else {
+      v_end = carry + P;
+      inside_end = carry_inside;
+    }
+  }
+}
+
+// Vector load of KL consecutive values / columns (one chunk per lane; adjacent lanes read
+// adjacent chunks, so a warp reads 32*KL contiguous elements per instruction).
+template <class V, int KL>
+__device__ __forceinline__ void ld_chunk(const V* v, const int32_t* c, double* vo, int32_t* co) {
+  if constexpr (KL == 1) {
+    vo[0] = (double)ld_stream(v);
+    co[0] = ld_stream(c);
+  } else {
+    PadLoad<V, KL>::ld(v, c, vo, co);
+  }
+}
+
+// =====================================================================================
+// FAM_NNZ_WARP, tile form (BMT_NNZ_BLOCK(k) with k in {1,2,4}, uniform BMW_NNZ_BLOCK of a
+// multiple of 32k, no padding): a round is 32*k contiguous nonzeros read with one vector
+// load per lane (coalesced, no per-BMT metadata).  Row heads come from a packed bitmap (1
+// bit per nonzero: the per-BMT bitmaps of A20 concatenated in lane order) and the row of
+// every lane from the BMW's first row plus a warp prefix count of heads (the first_row of
+// each BMT is linear in the head count, so it is computed, not stored; reading A17).
+// =====================================================================================
+template <class V, int KL, int WRED>
+__global__ void __launch_bounds__(512) k_warp_tile(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  const V* val = (const V*)p.val;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = gthreads() >> 5;
+  const int64_t k2 = p.bmts_per_bmw * KL;  // nonzeros per BMW
+  for (int64_t w = warp_units(p.n_bmw).begin, w_e = warp_units(p.n_bmw).end; w < w_e; w += blockDim.x >> 5) {
+    const int64_t a = w * k2, e = min(a + k2, p.nnz_p);
+    const uint32_t w0 = ldm(p.bits + (a >> 5));
+    const bool head_a = w0 & (1u << (a & 31));
+    int64_t rb = (int64_t)ldm(p.bmw_first_row + w) - (head_a ? 1 : 0);  // row before the round
+    double carry = 0.0;
+    bool carry_inside = false, carry_live = false;
+    int64_t carry_row = 0;
+    // 2-stage software pipeline: the vector loads of round r+1 are in flight while round r
+    // gathers x and runs its segmented combine.
+    auto load_round = [&](int64_t eb, double* v, int32_t* c, uint32_t& hb) {
+      const int64_t i0 = eb + lane * KL;
+      const bool active = i0 < e;
+      if (active && i0 + KL <= e) {
+        ld_chunk<V, KL>(val + i0, p.col + i0, v, c);
+      } else {
+#pragma unroll
+        for (int q = 0; q < KL; ++q) {
+          v[q] = (active && i0 + q < e) ? (double)ld_stream(val + i0 + q) : 0.0;
+          c[q] = (active && i0 + q < e) ? ld_stream(p.col + i0 + q) : 0;
+        }
+      }
+      hb = 0;
+      if (active) {
+        hb = (ldm(p.bits + (i0 >> 5)) >> (i0 & 31)) & ((1u << KL) - 1u);
+        if (e - i0 < KL) hb &= (1u << (e - i0)) - 1u;
+      }
+    };
+    double vn[KL];
+    int32_t cn[KL];
+    uint32_t hbn;
+    load_round(a, vn, cn, hbn);
+    for (int64_t eb = a; eb < e; eb += 32 * KL) {
+      const int64_t i0 = eb + lane * KL;
+      const bool active = i0 < e;
+      const int nact = (int)min((int64_t)32, (e - eb + KL - 1) / KL);
+      double v[KL];
+      int32_t c[KL];
+#pragma unroll
+      for (int q = 0; q < KL; ++q) {
+        v[q] = vn[q];
+        c[q] = cn[q];
+      }
+      const uint32_t hb = hbn;
+      if (eb + 32 * KL < e) load_round(eb + 32 * KL, vn, cn, hbn);
+      double xv[KL];
+#pragma unroll
+      for (int q = 0; q < KL; ++q) xv[q] = (active && i0 + q < e) ? ldx(x, c[q]) : 0.0;
+      // exclusive prefix of head counts over lanes -> this lane's starting row
+      int cnt = __popc(hb), pre = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        int n = __shfl_up_sync(0xffffffffu, pre, d);
+        if (lane >= d) pre += n;
+      }
+      const int total = __shfl_sync(0xffffffffu, pre, 31);
+      int64_t row = rb + (pre - cnt);  // row of the element before this lane's chunk
+      // serial pass over the lane's KL elements
+      double cin = 0.0, cout = 0.0, cur = 0.0;
+      bool hh = false;
+      int64_t head_row = row + 1;
+#pragma unroll
+      for (int q = 0; q < KL; ++q) {
+        if (hb & (1u << q)) {
+          if (!hh) {
+            cin = cur;
+            hh = true;
+          } else {
+            write_excl(p, y, row, cur);  // row wholly inside this lane's chunk
+          }
+          ++row;
+          cur = 0.0;
+        }
+        cur += v[q] * xv[q];
+      }
+      if (hh) cout = cur;
+      else cin = cur;
+      double v_end, closing;
+      bool inside_end, closing_inside;
+      warp_combine<WRED>(lane, hh, cin, cout, carry, carry_inside, closing, closing_inside, v_end, inside_end);
+      if (active && hh) {
+        bool exists = !(lane == 0 && !carry_live && (hb & 1u));
+        if (exists) {
+          if (closing_inside) write_excl(p, y, head_row - 1, closing);
+          else write_atom(p, y, head_row - 1, closing);
+        }
+      }
+      carry = __shfl_sync(0xffffffffu, v_end, nact - 1);
+      carry_inside = __shfl_sync(0xffffffffu, (int)inside_end, nact - 1);
+      carry_row = __shfl_sync(0xffffffffu, row, nact - 1);
+      carry_live = true;
+      rb += total;
+    }
+    if (lane == 0 && carry_live) {
+      bool ends = e >= p.nnz_p ? true : ((ldm(p.bits + (e >> 5)) >> (e & 31)) & 1u);
+      if (carry_inside && ends) write_excl(p, y, carry_row, carry);
+      else write_atom(p, y, carry_row, carry);
+    }
+  }
+}
+
 template <class V, int WRED, bool PAD, int VEC>
 __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = gthreads() >> 5;
-  for (int64_t w = gtid() >> 5; w < p.n_bmw; w += nwarps) {
+  for (int64_t w = warp_units(p.n_bmw).begin, w_e = warp_units(p.n_bmw).end; w < w_e; w += blockDim.x >> 5) {
     int64_t tb0 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w) : w * p.bmts_per_bmw;
     int64_t tb1 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w + 1) : min(tb0 + p.bmts_per_bmw, p.n_bmt);
     double carry = 0.0;
@@ -431,7 +659,14 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
         double cur;
         bool in;
         bool first_open = true;
-        bmt_pass<V, PAD, VEC>(p, x, t, a, e - a, row, cur, in, [&](int64_t r, double s, bool inside) {
+        PadPos pp{0, 0};
+        if constexpr (PAD) {
+          if (p.pad_grp_bmw) pp = PadPos{ldm(p.grp_base + w) + (t - tb0) * VEC, (tb1 - tb0) * VEC};
+          else if (p.n_grp == 1) pp = PadPos{t * VEC, p.n_bmt * VEC};
+          else pp = pad_pos<VEC>(p, t);
+        }
+        bmt_pass<V, PAD, VEC>(p, x, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, cur, in,
+                              [&](int64_t r, double s, bool inside) {
           if (!inside && first_open) {  // continuation of a row begun in an earlier lane
             cin = s;
             head_row = r + 1;
@@ -446,71 +681,9 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
         else cin = cur;
         last_row = row;
       }
-      double v_end;       // open-segment value at the end of each lane
-      bool inside_end;    // that segment started inside the BMW
-      double closing;     // for head lanes: total of the row closed at the first head
-      bool closing_inside;
-      if (WRED == 1) {
-        double v = hh ? cout : cin;
-        bool f = hh;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          double nv = __shfl_up_sync(0xffffffffu, v, d);
-          bool nf = __shfl_up_sync(0xffffffffu, (int)f, d);
-          if (lane >= d) {
-            if (!f) v += nv;
-            f = f || nf;
-          }
-        }
-        if (!f) v += carry;
-        v_end = v;
-        inside_end = f ? true : carry_inside;
-        double pv = __shfl_up_sync(0xffffffffu, v_end, 1);
-        bool pin = __shfl_up_sync(0xffffffffu, (int)inside_end, 1);
-        if (lane == 0) {
-          pv = carry;
-          pin = carry_inside;
-        }
-        closing = pv + cin;
-        closing_inside = pin;
-      } else {
-        const unsigned mask = __ballot_sync(0xffffffffu, hh);
-        double c = hh ? 0.0 : cin;  // non-head lanes contribute wholly to the open segment
-        double P = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          double nv = __shfl_up_sync(0xffffffffu, P, d);
-          if (lane >= d) P += nv;
-        }
-        // previous head lane strictly below this lane
-        const unsigned below = mask & ((1u << lane) - 1u);
-        const int h = below ? 31 - __clz(below) : -1;
-        const int hs = h < 0 ? 0 : h;
-        double cout_h = __shfl_sync(0xffffffffu, cout, hs);
-        double P_h = __shfl_sync(0xffffffffu, P, hs);
-        double P_prev = __shfl_up_sync(0xffffffffu, P, 1);
-        if (lane == 0) P_prev = 0.0;
-        if (h >= 0) {
-          closing = cout_h + (P_prev - P_h) + cin;
-          closing_inside = true;
-        } else {
-          closing = carry + P_prev + cin;
-          closing_inside = carry_inside;
-        }
-        // open segment at the end of this lane
-        const unsigned upto = mask & (lane == 31 ? 0xffffffffu : ((1u << (lane + 1)) - 1u));
-        const int h2 = upto ? 31 - __clz(upto) : -1;
-        const int h2s = h2 < 0 ? 0 : h2;
-        double cout_h2 = __shfl_sync(0xffffffffu, cout, h2s);
-        double P_h2 = __shfl_sync(0xffffffffu, P, h2s);
-        if (h2 >= 0) {
-          v_end = cout_h2 + (P - P_h2);
-          inside_end = true;
-        } else {
-          v_end = carry + P;
-          inside_end = carry_inside;
-        }
-      }
+      double v_end, closing;
+      bool inside_end, closing_inside;
+      warp_combine<WRED>(lane, hh, cin, cout, carry, carry_inside, closing, closing_inside, v_end, inside_end);
       if (active && hh) {
         // the row closed at this lane's first head; none only when the BMW itself starts
         // with a head (lane 0 of the first round, element 0 is a row start)
@@ -544,7 +717,7 @@ __global__ void __launch_bounds__(1024) k_warp_row(DevPart p, const V* __restric
   const V* val = (const V*)p.val;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = gthreads() >> 5;
-  for (int64_t w = gtid() >> 5; w < p.n_bmw; w += nwarps) {
+  for (int64_t w = warp_units(p.n_bmw).begin, w_e = warp_units(p.n_bmw).end; w < w_e; w += blockDim.x >> 5) {
     int64_t a = ldm(p.bmw_start + w), e = ldm(p.bmw_start + w + 1);
     int64_t row = p.bmw_first_row ? ldm(p.bmw_first_row + w) : w;
     double acc = 0.0;
@@ -838,6 +1011,22 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
     }
     case FAM_NNZ_WARP: {
       int64_t g = grid_for(p, p.n_bmw, tpb / 32);
+      if (p.tile) {
+        const int tt = tpb > 512 ? 512 : tpb;  // launch bound of k_warp_tile
+        g = grid_for(p, p.n_bmw, tt / 32);
+#define AS_TILE(KL)                                                                 \
+  if (p.variant == 1) k_warp_tile<V, KL, 1><<<g, tt, 0, s>>>(p, x, y);             \
+  else k_warp_tile<V, KL, 2><<<g, tt, 0, s>>>(p, x, y);
+        if (p.k == 1) {
+          AS_TILE(1)
+        } else if (p.k == 2) {
+          AS_TILE(2)
+        } else {
+          AS_TILE(4)
+        }
+#undef AS_TILE
+        break;
+      }
 #define AS_NW(WR)                                                              \
   if (!p.pad) k_nnz_warp<V, WR, false, 1><<<g, tpb, 0, s>>>(p, x, y);          \
   else if (p.vec == 1) k_nnz_warp<V, WR, true, 1><<<g, tpb, 0, s>>>(p, x, y);  \

@@ -62,6 +62,11 @@ const int32_t* Plan::up_i32(const std::vector<int64_t>& v, cudaStream_t s, const
 
 const void* Plan::up_vals(const std::vector<double>& v, cudaStream_t s, size_t pad_elems) {
   size_t n = std::max(v.size(), pad_elems);
+  if (dt == AS_R64F && n == v.size()) {
+    const void* d = up(v.data(), n * 8, s);
+    cudaStreamSynchronize(s);
+    return d;
+  }
   if (dt == AS_R64F) {
     std::vector<double> t(n, 0.0);
     std::copy(v.begin(), v.end(), t.begin());
@@ -70,7 +75,9 @@ const void* Plan::up_vals(const std::vector<double>& v, cudaStream_t s, size_t p
     return d;
   }
   std::vector<float> t(n, 0.0f);
-  for (size_t i = 0; i < v.size(); ++i) t[i] = (float)v[i];
+  parallel_for((int64_t)v.size(), [&](int64_t a, int64_t e) {
+    for (int64_t i = a; i < e; ++i) t[i] = (float)v[i];
+  });
   const void* d = up(t.data(), n * 4, s);
   cudaStreamSynchronize(s);
   return d;
@@ -187,6 +194,23 @@ void Plan::upload(cudaStream_t s) {
         case FAM_NNZ_WARP: {
           d.n_bmt = T.count();
           d.k = T.size;
+          if (h.fam == FAM_NNZ_WARP && !h.pad && (T.size == 1 || T.size == 2 || T.size == 4) && W.nnz &&
+              !B.present && W.size % (32 * T.size) == 0) {
+            // tile form: packed 1-bit heads + BMW first rows; BMT starts and first rows
+            // are computed from them (k_warp_tile)
+            d.tile = 1;
+            d.variant = h.red[1] == RED_SEG ? 1 : 2;
+            d.n_bmw = W.count();
+            d.bmts_per_bmw = W.size / T.size;
+            std::vector<uint32_t> bits((size_t)(nnz / 32 + 2), 0u);
+            for (int64_t r = 0; r < mp; ++r) bits[(size_t)(h.row_ptr[r] >> 5)] |= 1u << (h.row_ptr[r] & 31);
+            d.bits = (const uint32_t*)up(bits.data(), bits.size() * 4, s);
+            cudaStreamSynchronize(s);
+            d.bmw_first_row = up_i32(W.first_row, s, "bmw_first_row");
+            bytes_model += (double)(bits.size() * 4 + W.first_row.size() * 4);
+            need_rowptr = false;
+            break;
+          }
           std::vector<int64_t> st(T.start.begin(), T.start.end() - 1);
           if (!is_affine(st, T.size, 0)) {
             d.bmt_start = up_i32(T.start, s, "bmt_start");
@@ -199,6 +223,7 @@ void Plan::upload(cudaStream_t s) {
           if (h.pad) {  // CSR5-like slot-major tiles (BMT_PAD over NNZ BMTs)
             upload_pad(h, d, s);
             need_colval = false;
+            d.pad_grp_bmw = (h.fam == FAM_NNZ_WARP && h.pad_scope == 1) ? 1 : 0;
           }
           if (h.fam == FAM_NNZ_WARP) {
             d.variant = h.red[1] == RED_SEG ? 1 : 2;

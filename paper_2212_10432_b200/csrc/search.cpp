@@ -109,10 +109,11 @@ std::string gen_kernel(Rng& r, const Stats& st) {
       break;
     }
     case 2: {  // CSR5-like: warp tiles of nnz + segmented sum
-      int64_t k = r.pick(std::vector<int64_t>{4, 8, 16});
-      int64_t c = r.pick(std::vector<int64_t>{1, 2, 4});
+      int64_t k = r.pick(std::vector<int64_t>{1, 2, 4, 4, 8, 16});
+      const bool tile = k <= 4;  // coalesced tile kernel: many rounds per warp, no padding
+      int64_t c = tile ? r.pick(std::vector<int64_t>{8, 32, 128}) : r.pick(std::vector<int64_t>{1, 2, 4});
       s += "BMW_NNZ_BLOCK(" + std::to_string(32 * k * c) + "); BMT_NNZ_BLOCK(" + std::to_string(k) + "); ";
-      if (r.coin(0.6)) s += std::string("BMT_PAD(scope=BMW,vec=") + (r.coin(0.5) ? "1" : "0") + "); ";
+      if (!tile && r.coin(0.6)) s += std::string("BMT_PAD(scope=BMW,vec=") + (r.coin(0.5) ? "1" : "0") + "); ";
       s += std::string("THREAD_BITMAP_RED_G; ") + (r.coin(0.5) ? "WARP_SEG_ADD_RED; " : "WARP_BITMAP_RED; ");
       break;
     }

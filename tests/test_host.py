@@ -196,6 +196,10 @@ FAMILY_GRAPHS = [
     "COMPRESS; BMW_NNZ_BLOCK(64); BMT_NNZ_BLOCK(2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
     "COMPRESS; BMW_NNZ_BLOCK(50); BMT_NNZ_BLOCK(3); THREAD_BITMAP_RED_G; WARP_BITMAP_RED; GMEM_ATOM_RED",
     "COMPRESS; BMW_ROW_BLOCK(3); BMT_NNZ_BLOCK(2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
+    "COMPRESS; BMW_NNZ_BLOCK(64); BMT_NNZ_BLOCK(2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
+    "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; WARP_BITMAP_RED; GMEM_ATOM_RED",
+    "COMPRESS; BMW_NNZ_BLOCK(32); BMT_NNZ_BLOCK(1); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
+    "COMPRESS; BMW_NNZ_BLOCK(96); BMT_NNZ_BLOCK(1); THREAD_BITMAP_RED_G; WARP_BITMAP_RED; GMEM_ATOM_RED",
     "COMPRESS; BMT_NNZ_BLOCK(5); BMT_PAD(GLOBAL,1); THREAD_BITMAP_RED_G; GMEM_ATOM_RED",
     "COMPRESS; BMTB_NNZ_BLOCK(40); BMT_NNZ_BLOCK(4); BMT_PAD(BMTB,2); THREAD_BITMAP_RED_G; GMEM_ATOM_RED",
     "COMPRESS; BMW_NNZ_BLOCK(96); BMT_NNZ_BLOCK(3); BMT_PAD(BMW,1); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
