@@ -336,7 +336,7 @@ def main():
     if os.path.exists(prof):
         try:
             tj = json.load(open(prof))
-            if tj.get("graph") == graph:
+            if tj.get("kernels") == info["kernels"]:
                 traffic = tj["dram_bytes_per_launch"]
         except Exception:
             pass
