@@ -340,14 +340,14 @@ __device__ __forceinline__ PadPos pad_pos(const DevPart& p, int64_t t) {
 
 // Serial pass over one BMT (THREAD_BITMAP_RED_G): calls seg(row, partial, head_inside) at
 // every bitmap head after element 0; returns the open (last) segment in acc/row/inside.
-template <class V, bool PAD, int VEC, class Seg>
+template <class V, bool PAD, int VEC, int KB, class Seg>
 __device__ __forceinline__ void bmt_pass(const DevPart& p, const V* __restrict__ x, const uint32_t* bm, PadPos pp,
                                          int64_t a, int len, int64_t& row, double& acc, bool& inside, Seg seg) {
   // Batches of KB elements: all value/column loads of a batch are issued, then all x
   // gathers, then the bitmap-segmented accumulation -> KB independent loads in flight per
   // thread instead of one element behind each head test.  pp: slot base/stride of this
   // BMT in the padded layout, computed by the caller (no per-BMT division).
-  constexpr int KB = 8;  // divides 32, multiple of VEC
+  static_assert(32 % KB == 0 && KB % VEC == 0, "KB divides 32 and is a multiple of VEC");
   inside = ldm(bm) & 1u;
   acc = 0.0;
   const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;
@@ -404,8 +404,8 @@ __device__ __forceinline__ void bmt_pass(const DevPart& p, const V* __restrict__
 // nonzeros serially, cutting at bitmap heads (bit j = element j starts a row, A20); rows
 // whose head and end lie in the BMT are exclusive, straddlers go to y by atomics ("_G").
 // =====================================================================================
-template <class V, bool PAD, int VEC>
-__global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+template <class V, bool PAD, int VEC, int KB>
+__global__ void __launch_bounds__(512) k_nnz_thread(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   for (int64_t t = thread_units(p.n_bmt).begin, t_e = thread_units(p.n_bmt).end; t < t_e; t += blockDim.x) {
     int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
     int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restr
     bool inside;
     PadPos pp{0, 0};
     if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
-    bmt_pass<V, PAD, VEC>(p, x, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, acc, inside,
+    bmt_pass<V, PAD, VEC, KB>(p, x, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, acc, inside,
                           [&](int64_t r, double s, bool in) {
                             if (in) write_excl(p, y, r, s);
                             else write_atom(p, y, r, s);
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
           else if (p.n_grp == 1) pp = PadPos{t * VEC, p.n_bmt * VEC};
           else pp = pad_pos<VEC>(p, t);
         }
-        bmt_pass<V, PAD, VEC>(p, x, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, cur, in,
+        bmt_pass<V, PAD, VEC, 8>(p, x, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, cur, in,
                               [&](int64_t r, double s, bool inside) {
           if (!inside && first_open) {  // continuation of a row begun in an earlier lane
             cin = s;
@@ -910,6 +910,47 @@ __global__ void __launch_bounds__(1024) k_dia(DevPart p, const V* __restrict__ x
 }
 
 // =====================================================================================
+// FAM_DENSE, b = 64, fp64: one warp per tile row; half-warp h takes tile columns j = h,
+// h+2, ...; lane owns 4 consecutive tile rows and reads them with one 256-bit load per
+// column (a half-warp reads one whole 512-byte column), 4 columns in flight; the halves
+// combine with one shuffle.
+// =====================================================================================
+template <class V>
+__global__ void __launch_bounds__(1024) k_dense64(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  const double* tv = (const double*)p.tile_val;
+  const int lane = threadIdx.x & 31, half = lane >> 4, r4 = (lane & 15) * 4;
+  for (int64_t tr = warp_units(p.n_tile_rows).begin, tr_e = warp_units(p.n_tile_rows).end; tr < tr_e;
+       tr += blockDim.x >> 5) {
+    const int64_t I = ldm(p.tile_row_id + tr);
+    const int64_t t0 = ldm(p.tile_row_ptr + tr), t1 = ldm(p.tile_row_ptr + tr + 1);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t t = t0; t < t1; ++t) {
+      const int64_t J = ldm(p.tile_col + t);
+      const double* tile = tv + t * 4096 + r4;
+      const bool full = J * 64 + 64 <= p.n;
+#pragma unroll 4
+      for (int j = half; j < 64; j += 2) {
+        double v[4];
+        Ld32<double>::ld(tile + j * 64, v);
+        const int64_t c = J * 64 + j;
+        const double xj = (full || c < p.n) ? ldx((const V*)x, c) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += v[q] * xj;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 16);
+    if (half == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t row = I * 64 + r4 + q;
+        if (row >= p.row_lo && row < p.row_hi) write_excl(p, y, row, acc[q]);
+      }
+    }
+  }
+}
+
+// =====================================================================================
 // FAM_DENSE: BSR-like b x b tiles (column-major) of DENSE_DECOM.  One warp per tile row;
 // lane owns rows i = lane + 32q; for each tile column j the warp reads b contiguous values
 // (coalesced) and one broadcast x element.  CUDA cores: a single right-hand side makes
@@ -1003,10 +1044,22 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       break;
     case FAM_NNZ_THREAD: {
       int64_t g = grid_for(p, p.n_bmt, tpb);
-      if (!p.pad) k_nnz_thread<V, false, 1><<<g, tpb, 0, s>>>(p, x, y);
-      else if (p.vec == 1) k_nnz_thread<V, true, 1><<<g, tpb, 0, s>>>(p, x, y);
-      else if (p.vec == 2) k_nnz_thread<V, true, 2><<<g, tpb, 0, s>>>(p, x, y);
-      else k_nnz_thread<V, true, 4><<<g, tpb, 0, s>>>(p, x, y);
+      const int tt = tpb > 512 ? 512 : tpb;  // launch bound of k_nnz_thread
+      g = grid_for(p, p.n_bmt, tt);
+      // batch of 16 loads per thread for long BMTs (k >= 16), else 8
+#define AS_NT(PADV, VECV)                                                                         \
+  if (p.k >= 16) k_nnz_thread<V, PADV, VECV, 16><<<g, tt, 0, s>>>(p, x, y);                      \
+  else k_nnz_thread<V, PADV, VECV, 8><<<g, tt, 0, s>>>(p, x, y);
+      if (!p.pad) {
+        AS_NT(false, 1)
+      } else if (p.vec == 1) {
+        AS_NT(true, 1)
+      } else if (p.vec == 2) {
+        AS_NT(true, 2)
+      } else {
+        AS_NT(true, 4)
+      }
+#undef AS_NT
       break;
     }
     case FAM_NNZ_WARP: {
@@ -1071,6 +1124,12 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
     case FAM_DENSE: {
       int64_t g = grid_for(p, p.n_tile_rows, tpb / 32);
       int rpl = (int)((p.b + 31) / 32);
+      if constexpr (sizeof(V) == 8) {
+        if (p.b == 64) {
+          k_dense64<V><<<g, tpb, 0, s>>>(p, x, y);
+          break;
+        }
+      }
       if (rpl <= 1) k_dense<V, 1><<<g, tpb, 0, s>>>(p, x, y);
       else if (rpl == 2) k_dense<V, 2><<<g, tpb, 0, s>>>(p, x, y);
       else if (rpl <= 4) k_dense<V, 4><<<g, tpb, 0, s>>>(p, x, y);
