@@ -55,7 +55,7 @@ SCHEMA: dict[str, list[tuple[str, str, Any]]] = {
     "BMT_NNZ_BLOCK": [("nnz", "int", None)],
     "BMT_PAD": [("scope", "scope", "GLOBAL"), ("vec", "int", 0)],
     "SORT_BMTB": [],
-    "SET_RESOURCE": [("tpb", "int", 256), ("grid", "int", 0)],
+    "SET_RESOURCE": [("tpb", "int", 256), ("grid", "int", 0), ("stages", "int", 2)],
     **{r: [] for r in REDUCTIONS},
 }
 ALIASES = {"WARP_SEG_RED": "WARP_SEG_ADD_RED", "THREAD_BITMAP_RED": "THREAD_BITMAP_RED_G",
@@ -312,8 +312,8 @@ def _check_params(op: Op, nid: int):
         if p["vec"] not in (0, 1, 2, 4):
             bad("vec in {0,1,2,4}")
     elif op.name == "SET_RESOURCE":
-        if p["tpb"] < 32 or p["tpb"] > 1024 or p["tpb"] % 32 or p["grid"] < 0:
-            bad("tpb multiple of 32 in [32,1024], grid >= 0")
+        if p["tpb"] < 32 or p["tpb"] > 1024 or p["tpb"] % 32 or p["grid"] < 0 or p["stages"] not in (0, 2):
+            bad("tpb multiple of 32 in [32,1024], grid >= 0, stages in {0,2}")
 
 
 def validate(seq):

@@ -57,6 +57,7 @@ struct DevPart {
   int64_t k1 = 0;
   const int32_t* bmtb_first_row = nullptr;
   int64_t max_block_nnz = 0;
+  int64_t smem_cap = 0, smem_rcap = 0;    // TMA CSR-stream: staged elements / row offsets per stage
   // BMT_PAD (slot-major interleaved)
   int pad = 0, vec = 1;
   int64_t n_grp = 0, grp_regular = 0;     // BMTs per group if regular, else 0

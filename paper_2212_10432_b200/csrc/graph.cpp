@@ -52,7 +52,8 @@ const std::vector<OpSpec>& specs() {
       {"BMT_NNZ_BLOCK", 2, {{"nnz", P_INT, false, 0, nullptr}}},
       {"BMT_PAD", 2, {{"scope", P_SCOPE, true, 0, "GLOBAL"}, {"vec", P_INT, true, 0, nullptr}}},
       {"SORT_BMTB", 2, {}},
-      {"SET_RESOURCE", 3, {{"tpb", P_INT, true, 256, nullptr}, {"grid", P_INT, true, 0, nullptr}}},
+      {"SET_RESOURCE", 3,
+       {{"tpb", P_INT, true, 256, nullptr}, {"grid", P_INT, true, 0, nullptr}, {"stages", P_INT, true, 2, nullptr}}},
       {"THREAD_TOTAL_RED", 3, {}},
       {"THREAD_BITMAP_RED_G", 3, {}},
       {"WARP_TOTAL_RED", 3, {}},
@@ -380,7 +381,9 @@ void check_params(const Op& o) {
     if (v != 0 && v != 1 && v != 2 && v != 4) bad("vec in {0,1,2,4}");
   } else if (o.name == "SET_RESOURCE") {
     int64_t tpb = o.geti("tpb");
-    if (tpb < 32 || tpb > 1024 || tpb % 32 || o.geti("grid") < 0) bad("tpb multiple of 32 in [32,1024], grid >= 0");
+    int64_t st = o.geti("stages");
+    if (tpb < 32 || tpb > 1024 || tpb % 32 || o.geti("grid") < 0 || (st != 0 && st != 2))
+      bad("tpb multiple of 32 in [32,1024], grid >= 0, stages in {0,2}");
   }
 }
 

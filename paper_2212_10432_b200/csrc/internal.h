@@ -86,7 +86,7 @@ struct HostPart {
   int bm_words = 0;
   bool sort_bmtb = false;
   Red red[3] = {RED_NONE, RED_NONE, RED_NONE};  // per level (BMTB, BMW, BMT)
-  int tpb = 0, grid = 0;
+  int tpb = 0, grid = 0, stages = 2;  // SET_RESOURCE
   // DIA
   int64_t r0 = 0, mb = 0;
   std::vector<int64_t> dia_off;

@@ -769,6 +769,104 @@ __global__ void __launch_bounds__(1024) k_block_total(DevPart p, const V* __rest
 }
 
 // =====================================================================================
+// FAM_BLOCK_OFFSET, TMA form: BMTB + SHMEM_OFFSET_RED with the block's values, columns and
+// CSR row offsets ("reduce_row_offsets") staged into shared memory by bulk
+// asynchronous copies (cp.async.bulk, SASS UBLKCP) that complete on an mbarrier.  Two
+// stages: while the CTA reduces block b, the copies of its next block are in flight.
+// Persistent grid; CTA c owns a contiguous range of BMTBs.
+// =====================================================================================
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+template <class V>
+__global__ void __launch_bounds__(1024) k_block_offset_tma(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  // smem per stage: val[cap] | col[cap] | rp[rcap]; then prod[cap] (double); then 2 mbarriers
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int64_t cap = p.smem_cap, rcap = p.smem_rcap;  // elements (multiples of 4, +4 slack)
+  const size_t stage_bytes = (size_t)cap * (sizeof(V) + 4) + (size_t)rcap * 4;
+  double* prod = (double*)(smem_raw + 2 * stage_bytes);
+  uint64_t* bars = (uint64_t*)(prod + cap);
+  const V* val = (const V*)p.val;
+  const int64_t per = (p.n_bmtb + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = (int64_t)blockIdx.x * per, b1 = min(b0 + per, p.n_bmtb);
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // block geometry: nonzeros [a, e), rows [r0, r1) intersecting it
+  auto geom = [&](int64_t b, int64_t& a, int64_t& e, int64_t& r0, int64_t& r1) {
+    a = p.bmtb_start ? ldm(p.bmtb_start + b) : b * p.k1;
+    e = p.bmtb_start ? ldm(p.bmtb_start + b + 1) : min(a + p.k1, p.nnz_p);
+    r0 = ldm(p.bmtb_first_row + b);
+    r1 = b + 1 < p.n_bmtb ? ldm(p.bmtb_first_row + b + 1) + 1 : p.m_p;  // conservative (+1)
+    if (r1 > p.m_p) r1 = p.m_p;
+  };
+  auto issue = [&](int64_t b, int st) {  // thread 0: copies of block b into stage st
+    int64_t a, e, r0, r1;
+    geom(b, a, e, r0, r1);
+    const int64_t aa = a & ~int64_t(3), ea = (e + 3) & ~int64_t(3);
+    const int64_t ra = r0 & ~int64_t(3), re = (r1 + 1 + 3) & ~int64_t(3);
+    unsigned char* base = smem_raw + st * stage_bytes;
+    const uint32_t bv = (uint32_t)((ea - aa) * sizeof(V)), bc = (uint32_t)((ea - aa) * 4), br = (uint32_t)((re - ra) * 4);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of this stage
+    mbar_expect_tx(&bars[st], bv + bc + br);
+    bulk_g2s(base, val + aa, bv, &bars[st]);
+    bulk_g2s(base + cap * sizeof(V), p.col + aa, bc, &bars[st]);
+    bulk_g2s(base + cap * (sizeof(V) + 4), p.row_ptr + ra, br, &bars[st]);
+  };
+  if (threadIdx.x == 0 && b0 < b1) issue(b0, 0);
+  uint32_t phase[2] = {0, 0};
+  for (int64_t b = b0; b < b1; ++b) {
+    const int st = (int)((b - b0) & 1);
+    if (threadIdx.x == 0 && b + 1 < b1) issue(b + 1, st ^ 1);
+    int64_t a, e, r0, r1;
+    geom(b, a, e, r0, r1);
+    const int64_t aa = a & ~int64_t(3), ra = r0 & ~int64_t(3);
+    const unsigned char* base = smem_raw + st * stage_bytes;
+    const V* sv = (const V*)base;
+    const int32_t* sc = (const int32_t*)(base + cap * sizeof(V));
+    const int32_t* srp = (const int32_t*)(base + cap * (sizeof(V) + 4));
+    mbar_wait(&bars[st], phase[st]);
+    phase[st] ^= 1;
+    for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x)
+      prod[i - a] = (double)sv[i - aa] * ldx(x, sc[i - aa]);
+    __syncthreads();
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+      const int64_t ra_ = srp[r - ra];
+      if (ra_ >= e) continue;
+      const int64_t re_ = srp[r + 1 - ra];
+      const int64_t fa = max(ra_, a), fe = min(re_, e);
+      if (fe <= fa) continue;
+      double s = 0.0;
+      for (int64_t i = fa; i < fe; ++i) s += prod[i - a];
+      if (fa == ra_ && fe == re_) write_excl(p, y, r, s);
+      else write_atom(p, y, r, s);
+    }
+    __syncthreads();  // stage st and prod are free for reuse
+  }
+}
+
+// =====================================================================================
 // FAM_BLOCK_OFFSET: BMTB + SHMEM_OFFSET_RED (CSR-Stream).  The CTA stages the products of
 // its nonzeros in shared memory (coalesced pass; the "adapter" of P:322 copying register
 // results to shared memory), then reduces its row fragments in parallel using the CSR-like
@@ -1097,7 +1195,8 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       k_block_total<V><<<grid_for(p, p.n_bmtb, 1), tpb, 0, s>>>(p, x, y);
       break;
     case FAM_BLOCK_OFFSET:
-      k_block_offset<V><<<grid_for(p, p.n_bmtb, 1), tpb, p.smem, s>>>(p, x, y);
+      if (p.variant == 1) k_block_offset_tma<V><<<grid_for(p, p.n_bmtb, 1), tpb, p.smem, s>>>(p, x, y);
+      else k_block_offset<V><<<grid_for(p, p.n_bmtb, 1), tpb, p.smem, s>>>(p, x, y);
       break;
     case FAM_DIA: {
       // variant 0: 16-byte row groups (higher occupancy), 1: 32-byte (sm_100 256-bit loads)
@@ -1164,6 +1263,24 @@ int launch_scale_all(int64_t m, double beta, void* y, int dtype, void* stream) {
 }
 
 int prepare_part(DevPart& p) {
+  if (p.fam == FAM_BLOCK_OFFSET && p.variant == 1) {  // TMA-staged CSR-stream
+    const size_t sv = p.dtype == 1 ? 8 : 4;
+    p.smem = 2 * ((size_t)p.smem_cap * (sv + 4) + (size_t)p.smem_rcap * 4) + (size_t)p.smem_cap * 8 + 16;
+    cudaError_t e = p.dtype == 1 ? cudaFuncSetAttribute(k_block_offset_tma<double>,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem)
+                                 : cudaFuncSetAttribute(k_block_offset_tma<float>,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    if (e != cudaSuccess) return (int)e;
+    int per_sm = 0;
+    const int tpb = p.tpb > 0 ? p.tpb : 256;
+    e = p.dtype == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_offset_tma<double>, tpb, p.smem)
+                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_offset_tma<float>, tpb, p.smem);
+    if (e != cudaSuccess) return (int)e;
+    if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
+    if (p.grid <= 0) p.grid = per_sm;  // persistent: every resident CTA slot, CTA-blocked ranges
+    else if (p.grid > per_sm) p.grid = per_sm;
+    return 0;
+  }
   if (p.fam == FAM_BLOCK_OFFSET) {
     p.smem = (size_t)p.max_block_nnz * sizeof(double);
     if (p.smem > 48 * 1024) {

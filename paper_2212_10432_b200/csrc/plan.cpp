@@ -43,12 +43,14 @@ std::vector<int32_t> to_i32(const std::vector<int64_t>& v, const char* what) {
 }  // namespace
 
 void* Plan::up(const void* h, size_t bytes, cudaStream_t s, size_t pad_to) {
-  size_t alloc = std::max<size_t>(std::max(bytes, pad_to), 16);
+  // +64 bytes of zeroed tail: aligned bulk copies (cp.async.bulk, 16-B granules) and vector
+  // loads may read up to 3 elements past the end of an array
+  size_t alloc = std::max<size_t>(std::max(bytes, pad_to), 16) + 64;
   void* d = nullptr;
   ck(cudaMalloc(&d, alloc), "cudaMalloc");
   allocs.push_back(d);
   dev_bytes += alloc;
-  if (alloc > bytes) ck(cudaMemsetAsync(d, 0, alloc, s), "cudaMemsetAsync");
+  ck(cudaMemsetAsync((char*)d + bytes, 0, alloc - bytes, s), "cudaMemsetAsync");
   if (bytes) ck(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync");
   return d;
 }
@@ -276,9 +278,24 @@ void Plan::upload(cudaStream_t s) {
           int64_t mx = 0;
           for (int64_t b = 0; b < B.count(); ++b) mx = std::max(mx, B.start[b + 1] - B.start[b]);
           d.max_block_nnz = mx;
-          if (h.fam == FAM_BLOCK_OFFSET && (int64_t)mx * 8 > max_smem)
-            fail(AS_ERR_PLAN_INFEASIBLE, "P2: SHMEM_OFFSET_RED block of " + std::to_string(mx) +
-                                             " nonzeros exceeds the shared-memory opt-in limit");
+          if (h.fam == FAM_BLOCK_OFFSET) {
+            // TMA form when two staged blocks + the product buffer fit in shared memory:
+            // per stage cap elements (aligned span + slack) and rcap row offsets
+            int64_t cap = 0, rcap = 0;
+            for (int64_t b = 0; b < B.count(); ++b) {
+              int64_t a = B.start[b], e = B.start[b + 1];
+              cap = std::max(cap, ((e + 3) & ~int64_t(3)) - (a & ~int64_t(3)));
+              int64_t r0 = B.first_row[b], r1 = b + 1 < B.count() ? std::min(B.first_row[b + 1] + 1, mp) : mp;
+              rcap = std::max(rcap, ((r1 + 1 + 3) & ~int64_t(3)) - (r0 & ~int64_t(3)));
+            }
+            d.smem_cap = cap + 4;
+            d.smem_rcap = rcap + 4;
+            int64_t need = 2 * (d.smem_cap * (sv + 4) + d.smem_rcap * 4) + d.smem_cap * 8 + 16;
+            if (need <= max_smem && h.stages == 2) d.variant = 1;
+            else if ((int64_t)mx * 8 > max_smem)
+              fail(AS_ERR_PLAN_INFEASIBLE, "P2: SHMEM_OFFSET_RED block of " + std::to_string(mx) +
+                                               " nonzeros exceeds the shared-memory opt-in limit");
+          }
           break;
         }
         default:

@@ -132,6 +132,9 @@ std::string gen_kernel(Rng& r, const Stats& st) {
       if (r.coin(0.5)) s += "BMTB_ROW_BLOCK(" + std::to_string(r.pick(std::vector<int64_t>{16, 32, 64, 128})) + "); ";
       else s += "BMTB_NNZ_BLOCK(" + std::to_string(r.pick(std::vector<int64_t>{256, 512, 1024, 2048})) + "); ";
       s += "SHMEM_OFFSET_RED; ";
+      // staging choice: TMA bulk copies (stages=2) or direct loads (stages=0)
+      tpb = "SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{256, 512})) +
+            ",grid=0,stages=" + (r.coin(0.5) ? "2" : "0") + "); ";
       break;
     }
   }
