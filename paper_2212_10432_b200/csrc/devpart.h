@@ -58,6 +58,10 @@ struct DevPart {
   const int32_t* bmtb_first_row = nullptr;
   int64_t max_block_nnz = 0;
   int64_t smem_cap = 0, smem_rcap = 0;    // TMA CSR-stream: staged elements / row offsets per stage
+  // x-window staging (k_nnz_thread_xw): ring size (power of 2), exact CTA count, rounds per
+  // CTA, and per (CTA, round) the [lo, hi] x range
+  int64_t xw_size = 0, xw_grid = 0, xw_rpc = 0;
+  const int32_t* xwin = nullptr;
   // BMT_PAD (slot-major interleaved)
   int pad = 0, vec = 1;
   int64_t n_grp = 0, grp_regular = 0;     // BMTs per group if regular, else 0
@@ -92,5 +96,7 @@ int launch_scale_all(int64_t m, double beta, void* y, int dtype, void* stream);
 int prepare_part(DevPart& p);  // per-kernel attributes (smem opt-in); returns cudaError_t
 const char* fam_kernel_name(const DevPart& p);
 int device_max_smem_optin(int device);
+int device_sm_count(int device);
+int xw_ctas_per_sm(int dtype, int pad, int vec, int tpb, size_t smem);
 
 }  // namespace as

@@ -340,9 +340,23 @@ __device__ __forceinline__ PadPos pad_pos(const DevPart& p, int64_t t) {
 
 // Serial pass over one BMT (THREAD_BITMAP_RED_G): calls seg(row, partial, head_inside) at
 // every bitmap head after element 0; returns the open (last) segment in acc/row/inside.
-template <class V, bool PAD, int VEC, int KB, class Seg>
-__device__ __forceinline__ void bmt_pass(const DevPart& p, const V* __restrict__ x, const uint32_t* bm, PadPos pp,
-                                         int64_t a, int len, int64_t& row, double& acc, bool& inside, Seg seg) {
+// x accessors: straight from global memory (L1 / L2 evict_last), or from a shared-memory
+// ring buffer holding the CTA's current x window (banded matrices, k_nnz_thread_xw).
+template <class V>
+struct XGlobal {
+  const V* __restrict__ x;
+  __device__ __forceinline__ double operator()(int64_t c) const { return ldx(x, c); }
+};
+template <class V>
+struct XRing {
+  const V* ring;
+  int64_t mask;
+  __device__ __forceinline__ double operator()(int64_t c) const { return (double)ring[c & mask]; }
+};
+
+template <class V, bool PAD, int VEC, int KB, class XA, class Seg>
+__device__ __forceinline__ void bmt_pass(const DevPart& p, XA xa, const uint32_t* bm, PadPos pp, int64_t a, int len,
+                                         int64_t& row, double& acc, bool& inside, Seg seg) {
   // Batches of KB elements: all value/column loads of a batch are issued, then all x
   // gathers, then the bitmap-segmented accumulation -> KB independent loads in flight per
   // thread instead of one element behind each head test.  pp: slot base/stride of this
@@ -382,7 +396,7 @@ __device__ __forceinline__ void bmt_pass(const DevPart& p, const V* __restrict__
     }
     double xv[KB];
 #pragma unroll
-    for (int q = 0; q < KB; ++q) xv[q] = (j0 + q < len) ? ldx(x, c[q]) : 0.0;
+    for (int q = 0; q < KB; ++q) xv[q] = (j0 + q < len) ? xa(c[q]) : 0.0;
     const uint32_t wd = ldm(bm + (j0 >> 5)) >> (j0 & 31);
 #pragma unroll
     for (int q = 0; q < KB; ++q) {
@@ -404,24 +418,56 @@ __device__ __forceinline__ void bmt_pass(const DevPart& p, const V* __restrict__
 // nonzeros serially, cutting at bitmap heads (bit j = element j starts a row, A20); rows
 // whose head and end lie in the BMT are exclusive, straddlers go to y by atomics ("_G").
 // =====================================================================================
+template <class V, bool PAD, int VEC, int KB, class XA>
+__device__ __forceinline__ void nnz_thread_bmt(const DevPart& p, XA xa, V* __restrict__ y, int64_t t) {
+  int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
+  int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
+  int64_t row = ldm(p.bmt_first_row + t);
+  double acc;
+  bool inside;
+  PadPos pp{0, 0};
+  if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
+  bmt_pass<V, PAD, VEC, KB>(p, xa, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, acc, inside,
+                            [&](int64_t r, double s, bool in) {
+                              if (in) write_excl(p, y, r, s);
+                              else write_atom(p, y, r, s);
+                            });
+  bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
+  if (inside && ends) write_excl(p, y, row, acc);
+  else write_atom(p, y, row, acc);
+}
+
 template <class V, bool PAD, int VEC, int KB>
 __global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
-  for (int64_t t = thread_units(p.n_bmt).begin, t_e = thread_units(p.n_bmt).end; t < t_e; t += blockDim.x) {
-    int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
-    int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
-    int64_t row = ldm(p.bmt_first_row + t);
-    double acc;
-    bool inside;
-    PadPos pp{0, 0};
-    if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
-    bmt_pass<V, PAD, VEC, KB>(p, x, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, acc, inside,
-                          [&](int64_t r, double s, bool in) {
-                            if (in) write_excl(p, y, r, s);
-                            else write_atom(p, y, r, s);
-                          });
-    bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
-    if (inside && ends) write_excl(p, y, row, acc);
-    else write_atom(p, y, row, acc);
+  for (int64_t t = thread_units(p.n_bmt).begin, t_e = thread_units(p.n_bmt).end; t < t_e; t += blockDim.x)
+    nnz_thread_bmt<V, PAD, VEC, KB>(p, XGlobal<V>{x}, y, t);
+}
+
+// =====================================================================================
+// k_nnz_thread, x-window form (banded matrices): persistent CTAs own contiguous BMT ranges
+// processed in rounds of blockDim BMTs; round i of CTA c needs x[lo, hi] (computed at plan
+// time, lo made non-decreasing, span < ring size).  The CTA keeps x in a shared-memory ring
+// buffer, loading only the part of each window beyond what it already holds, so the
+// gathers read shared memory instead of moving a 32-byte L1/L2 sector per nonzero.
+// =====================================================================================
+template <class V, bool PAD, int VEC>
+__global__ void __launch_bounds__(1024) k_nnz_thread_xw(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* ring = (V*)smem_raw;
+  const int64_t mask = p.xw_size - 1;
+  const int64_t per = (p.n_bmt + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = (int64_t)blockIdx.x * per, b1 = min(b0 + per, p.n_bmt);
+  const int64_t rounds = b1 > b0 ? (b1 - b0 + blockDim.x - 1) / blockDim.x : 0;
+  int64_t have_hi = -1;
+  for (int64_t i = 0; i < rounds; ++i) {
+    const int64_t w = (int64_t)blockIdx.x * p.xw_rpc + i;
+    const int64_t lo = ldm(p.xwin + 2 * w), hi = ldm(p.xwin + 2 * w + 1);
+    for (int64_t c = max(have_hi + 1, lo) + threadIdx.x; c <= hi; c += blockDim.x) ring[c & mask] = __ldg(x + c);
+    if (hi > have_hi) have_hi = hi;
+    __syncthreads();
+    const int64_t t = b0 + i * blockDim.x + threadIdx.x;
+    if (t < b1) nnz_thread_bmt<V, PAD, VEC, 8>(p, XRing<V>{ring, mask}, y, t);
+    __syncthreads();  // the next window update overwrites entries this round may read
   }
 }
 
@@ -665,7 +711,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
           else if (p.n_grp == 1) pp = PadPos{t * VEC, p.n_bmt * VEC};
           else pp = pad_pos<VEC>(p, t);
         }
-        bmt_pass<V, PAD, VEC, 8>(p, x, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, cur, in,
+        bmt_pass<V, PAD, VEC, 8>(p, XGlobal<V>{x}, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, cur, in,
                               [&](int64_t r, double s, bool inside) {
           if (!inside && first_open) {  // continuation of a row begun in an earlier lane
             cin = s;
@@ -1141,6 +1187,14 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       }
       break;
     case FAM_NNZ_THREAD: {
+      if (p.xwin) {
+        const int64_t g = p.xw_grid;
+        if (!p.pad) k_nnz_thread_xw<V, false, 1><<<g, tpb, p.smem, s>>>(p, x, y);
+        else if (p.vec == 1) k_nnz_thread_xw<V, true, 1><<<g, tpb, p.smem, s>>>(p, x, y);
+        else if (p.vec == 2) k_nnz_thread_xw<V, true, 2><<<g, tpb, p.smem, s>>>(p, x, y);
+        else k_nnz_thread_xw<V, true, 4><<<g, tpb, p.smem, s>>>(p, x, y);
+        break;
+      }
       int64_t g = grid_for(p, p.n_bmt, tpb);
       const int tt = tpb;
       // batches of 8 loads per thread (16 measured slower on c5s: 394 vs 245 us, occupancy)
@@ -1291,6 +1345,32 @@ int prepare_part(DevPart& p) {
     }
   }
   return 0;
+}
+
+// x-window kernel: opt in to `smem` bytes of dynamic shared memory and return how many
+// CTAs of `tpb` threads fit per SM (0 on failure).
+template <class V>
+static int xw_occ_t(int pad, int vec, int tpb, size_t smem) {
+  auto occ = [&](auto kern) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, tpb, smem) != cudaSuccess) return 0;
+    return n;
+  };
+  if (!pad) return occ(k_nnz_thread_xw<V, false, 1>);
+  if (vec == 1) return occ(k_nnz_thread_xw<V, true, 1>);
+  if (vec == 2) return occ(k_nnz_thread_xw<V, true, 2>);
+  return occ(k_nnz_thread_xw<V, true, 4>);
+}
+int xw_ctas_per_sm(int dtype, int pad, int vec, int tpb, size_t smem) {
+  int n = dtype == 1 ? xw_occ_t<double>(pad, vec, tpb, smem) : xw_occ_t<float>(pad, vec, tpb, smem);
+  cudaGetLastError();
+  return n;
+}
+int device_sm_count(int device) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  return v;
 }
 
 int device_max_smem_optin(int device) {

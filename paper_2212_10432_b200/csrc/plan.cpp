@@ -106,6 +106,64 @@ void Plan::upload_pad(const HostPart& h, DevPart& d, cudaStream_t s) {
   bytes_model += (double)(h.pad_col.size() * 4 + h.pad_val.size() * sv + d.n_grp * (reg ? 12 : 16));
 }
 
+// x-window staging for k_nnz_thread (banded matrices): persistent CTAs, per (CTA, round)
+// x range [lo, hi]; enabled only when every round's window fits the shared-memory ring.
+void Plan::try_xwin(const HostPart& h, DevPart& d, cudaStream_t s) {
+  const Level& T = h.lv[2];
+  const int64_t sv = dt == AS_R64F ? 8 : 4;
+  const int64_t max_smem = device_max_smem_optin(device);
+  int64_t W = 1;
+  while (W * 2 * sv <= std::min<int64_t>(max_smem, 128 * 1024)) W *= 2;
+  if (W < 4096) return;
+  const int tpb = d.tpb;
+  const int per_sm = xw_ctas_per_sm(d.dtype, d.pad, d.vec, tpb, (size_t)(W * sv));
+  if (per_sm < 1) return;
+  const int64_t grid = (int64_t)per_sm * device_sm_count(device), nb = T.count();
+  if (nb < grid * tpb) return;  // too small to fill the persistent grid
+  const int64_t per = (nb + grid - 1) / grid, rpc = (per + tpb - 1) / tpb;
+  std::vector<int64_t> win((size_t)(grid * rpc * 2), 0);
+  std::vector<uint8_t> ok((size_t)grid, 1);
+  parallel_for(
+      grid,
+      [&](int64_t c0, int64_t c1) {
+        for (int64_t c = c0; c < c1; ++c) {
+          const int64_t b0 = c * per, b1 = std::min(b0 + per, nb);
+          std::vector<int64_t> lo(rpc, INT64_MAX), hi(rpc, -1);
+          for (int64_t i = 0; i < rpc; ++i) {
+            const int64_t t0 = b0 + i * tpb, t1 = std::min(t0 + tpb, b1);
+            if (t0 >= t1) continue;
+            for (int64_t e = T.start[t0]; e < T.start[t1]; ++e) {
+              lo[i] = std::min<int64_t>(lo[i], h.col[e]);
+              hi[i] = std::max<int64_t>(hi[i], h.col[e]);
+            }
+          }
+          // lo non-decreasing (suffix minimum), every window within the ring
+          for (int64_t i = rpc - 2; i >= 0; --i) lo[i] = std::min(lo[i], lo[i + 1]);
+          int64_t mh = -1;
+          for (int64_t i = 0; i < rpc; ++i) {
+            if (hi[i] < 0) {
+              win[(c * rpc + i) * 2] = 0;
+              win[(c * rpc + i) * 2 + 1] = -1;
+              continue;
+            }
+            mh = std::max(mh, hi[i]);
+            if (mh - lo[i] >= W) ok[c] = 0;
+            win[(c * rpc + i) * 2] = lo[i];
+            win[(c * rpc + i) * 2 + 1] = hi[i];
+          }
+        }
+      },
+      1);
+  for (auto v : ok)
+    if (!v) return;
+  d.xw_size = W;
+  d.xw_grid = grid;
+  d.xw_rpc = rpc;
+  d.smem = (size_t)(W * sv);
+  d.xwin = up_i32(win, s, "xwin");
+  bytes_model += (double)(win.size() * 4);
+}
+
 Plan::~Plan() {
   if (device >= 0) {
     int cur = 0;
@@ -227,6 +285,7 @@ void Plan::upload(cudaStream_t s) {
             need_colval = false;
             d.pad_grp_bmw = (h.fam == FAM_NNZ_WARP && h.pad_scope == 1) ? 1 : 0;
           }
+          if (h.fam == FAM_NNZ_THREAD && h.stages == 2) try_xwin(h, d, s);
           if (h.fam == FAM_NNZ_WARP) {
             d.variant = h.red[1] == RED_SEG ? 1 : 2;
             d.n_bmw = W.count();
@@ -313,6 +372,11 @@ void Plan::upload(cudaStream_t s) {
       }
     }
     ck((cudaError_t)prepare_part(d), "kernel attributes");
+    // name the kernel form actually chosen (as_plan_info.kernels)
+    std::string& fn = host.parts[pi].fam_name;
+    if (d.xwin) fn += "_xwin";
+    if (d.tile) fn += "_tile";
+    if (d.fam == FAM_BLOCK_OFFSET && d.variant == 1) fn += "_tma";
     launches.push_back(d);
   }
   if (!host.prepass.empty()) {

@@ -29,6 +29,7 @@ struct Plan {
   const void* up_vals(const std::vector<double>& v, cudaStream_t s, size_t pad_elems = 0);
   void upload(cudaStream_t s);
   void upload_pad(const HostPart& h, DevPart& d, cudaStream_t s);
+  void try_xwin(const HostPart& h, DevPart& d, cudaStream_t s);
   void compute_model();
 };
 

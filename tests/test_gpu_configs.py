@@ -111,6 +111,9 @@ def test_c4_graphs(c4, graph):
 C5_GRAPHS = [
     "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
     "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED",
+    # x-window staging form (banded): 32-nonzero BMTs, CSR5-like slot-major pad, 1024 threads
+    "COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL,2); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=1024); GMEM_ATOM_RED",
+    "COMPRESS; BMT_NNZ_BLOCK(16); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=512); GMEM_ATOM_RED",
     # SELL-C-sigma: sort inside 256-row BMTBs, pad per 32-row BMW (P:279 SORT_BMTB "decrease the padding rate")
     "COMPRESS; BMTB_ROW_BLOCK(256); SORT_BMTB; BMW_ROW_BLOCK(32); BMT_ROW_BLOCK(1); BMT_PAD(BMW); THREAD_TOTAL_RED; GMEM_ATOM_RED",
 ]
@@ -119,7 +122,17 @@ C5_GRAPHS = [
 @pytest.mark.parametrize("graph", C5_GRAPHS)
 def test_c5_graphs(c5, graph):
     P = asp.Plan(_mat(c5), graph, device=0)
+    if "THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=" in graph:
+        assert P.info()["kernels"].endswith("_xwin"), P.info()["kernels"]   # banded -> x window
     run_sampled(c5, P, 1.0, 0.0, 5)
+    run_sampled(c5, P, -1.5, 0.5, 6)
+
+
+def test_c5_xwin_integer_exact():
+    c = synth.c5_band_csr(m=1 << 21, nnz=1 << 25, band=4096, int_mode=True)
+    P = asp.Plan(_mat(c), C5_GRAPHS[1], device=0)
+    assert P.info()["kernels"].endswith("_xwin")
+    run_sampled(c, P, 2.0, -1.0, 8, int_mode=True)
 
 
 @pytest.mark.parametrize("world", [2, 8])
