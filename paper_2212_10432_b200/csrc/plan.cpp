@@ -117,8 +117,11 @@ void Plan::try_xwin(const HostPart& h, DevPart& d, cudaStream_t s) {
   if (W < 4096) return;
   const int tpb = d.tpb;
   const int per_sm = xw_ctas_per_sm(d.dtype, d.pad, d.vec, tpb, (size_t)(W * sv));
-  if (per_sm < 1) return;
   const int64_t grid = (int64_t)per_sm * device_sm_count(device), nb = T.count();
+  if (std::getenv("AS_TRACE"))
+    std::fprintf(stderr, "[as_plan] x-window candidate: ring %lld, %d CTAs/SM, %lld BMTs\n", (long long)W, per_sm,
+                 (long long)nb);
+  if (per_sm < 1) return;
   if (nb < grid * tpb) return;  // too small to fill the persistent grid
   const int64_t per = (nb + grid - 1) / grid, rpc = (per + tpb - 1) / tpb;
   std::vector<int64_t> win((size_t)(grid * rpc * 2), 0);
@@ -156,6 +159,9 @@ void Plan::try_xwin(const HostPart& h, DevPart& d, cudaStream_t s) {
       1);
   for (auto v : ok)
     if (!v) return;
+  if (std::getenv("AS_TRACE"))
+    std::fprintf(stderr, "[as_plan] x-window: ring %lld, grid %lld x %d, %lld rounds/CTA\n", (long long)W,
+                 (long long)grid, tpb, (long long)rpc);
   d.xw_size = W;
   d.xw_grid = grid;
   d.xw_rpc = rpc;

@@ -130,7 +130,7 @@ def test_c5_graphs(c5, graph):
 
 def test_c5_xwin_integer_exact():
     c = synth.c5_band_csr(m=1 << 21, nnz=1 << 25, band=4096, int_mode=True)
-    P = asp.Plan(_mat(c), C5_GRAPHS[1], device=0)
+    P = asp.Plan(_mat(c), C5_GRAPHS[2], device=0)
     assert P.info()["kernels"].endswith("_xwin")
     run_sampled(c, P, 2.0, -1.0, 8, int_mode=True)
 
