@@ -97,13 +97,16 @@ def load_config(name, int_mode=False):
     if name == "c4":
         coo, _ = synth.c4_blockdense_csr()
         return coo, "blockdense-8m", [
-            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }"]
+            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
+            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMTB_ROW_BLOCK(64); BMT_ROW_BLOCK(1); BMT_PAD(BMTB); THREAD_TOTAL_RED; SET_RESOURCE(128); GMEM_ATOM_RED }",
+            "COMPRESS; BMTB_ROW_BLOCK(64); BMT_ROW_BLOCK(1); BMT_PAD(BMTB); THREAD_TOTAL_RED; SET_RESOURCE(128); GMEM_ATOM_RED"]
     if name == "c3":
         return synth.c3_rmat_csr(), "rmat-24", [
             "BIN(t=[32,2048]) { COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED"
             " | COMPRESS; BMTB_NNZ_BLOCK(2048); SHMEM_OFFSET_RED; GMEM_ATOM_RED"
             " | COMPRESS; BMTB_ROW_BLOCK(1); BMW_NNZ_BLOCK(2048); WARP_TOTAL_RED; GMEM_ATOM_RED }",
-            "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,1); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED"]
+            "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,1); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
+            "COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=256,grid=16); GMEM_ATOM_RED"]
     if name in ("c3s", "c4s", "c5s"):  # shape-preserving 1/4..1/16-scale instances (dev sweeps)
         c = {"c3s": lambda: synth.c3_rmat_csr(scale=22, nnz=1 << 26),
              "c4s": lambda: synth.c4_blockdense_csr(m=1 << 21, b=64, n_tiles=6144, nnz=50_000_000)[0],
@@ -112,7 +115,8 @@ def load_config(name, int_mode=False):
     if name == "c5":
         return synth.c5_band_csr(), "band-irreg-64m", [
             "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
-            "COMPRESS; BMTB_ROW_BLOCK(256); SORT_BMTB; BMW_ROW_BLOCK(32); BMT_ROW_BLOCK(1); BMT_PAD(BMW); THREAD_TOTAL_RED; GMEM_ATOM_RED"]
+            "COMPRESS; BMTB_ROW_BLOCK(256); SORT_BMTB; BMW_ROW_BLOCK(32); BMT_ROW_BLOCK(1); BMT_PAD(BMW); THREAD_TOTAL_RED; GMEM_ATOM_RED",
+            "COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL,2); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=512,grid=2,stages=0); GMEM_ATOM_RED"]
     raise SystemExit(f"unknown config {name}")
 
 

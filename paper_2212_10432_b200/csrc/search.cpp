@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <set>
 
 #include "internal.h"
 #include "plan.h"
@@ -219,6 +220,53 @@ std::string json_escape(const std::string& s) {
   return o;
 }
 
+// Fine-grained neighbour of a graph: one numeric parameter moved to an adjacent grid value
+// (the paper's fine parameter grid, P:369 step 3, explored by local search instead of an
+// XGBoost surrogate).  Returns "" when the graph has no mutable parameter.
+void collect_params(Seq& g, std::vector<std::pair<Op*, size_t>>& out) {
+  for (auto& op : g) {
+    for (size_t j = 0; j < op.params.size(); ++j) {
+      const std::string& k = op.params[j].first;
+      if (k == "cuts" || k == "t" || k == "scope") continue;
+      out.push_back({&op, j});
+    }
+    for (auto& b : op.br) collect_params(b, out);
+  }
+}
+
+std::string mutate_graph(const Seq& g0, Rng& r) {
+  Seq g = g0;
+  std::vector<std::pair<Op*, size_t>> ps;
+  collect_params(g, ps);
+  if (ps.empty()) return "";
+  auto [op, j] = ps[(size_t)r.uni((int64_t)ps.size())];
+  Value& v = op->params[j].second;
+  const std::string& k = op->params[j].first;
+  auto step = [&](const std::vector<int64_t>& grid) {
+    size_t at = 0;
+    for (size_t i = 0; i < grid.size(); ++i)
+      if (grid[i] == v.i) at = i;
+    if (grid.size() < 2) return;
+    size_t nx = r.coin(0.5) ? (at + 1) % grid.size() : (at + grid.size() - 1) % grid.size();
+    v.i = grid[nx];
+  };
+  if (k == "tpb") step({64, 128, 256, 512, 1024});
+  else if (k == "grid") step({0, 1, 2, 4, 8, 16});
+  else if (k == "stages") v.i = v.i ? 0 : 2;
+  else if (k == "vec") step({0, 1, 2, 4});
+  else if (k == "max") step({4, 8, 16, 32});
+  else if (k == "b") step({16, 32, 64, 128});
+  else if (k == "theta") v.f = v.f >= 0.85 ? 0.5 : v.f + 0.2;
+  else if (v.k == Value::INT) v.i = std::max<int64_t>(1, r.coin(0.5) ? v.i * 2 : v.i / 2);  // block sizes, g
+  std::string s = print_graph(g);
+  try {
+    parse_graph(s);  // keep only dependency-respecting neighbours
+  } catch (const Error&) {
+    return "";
+  }
+  return s;
+}
+
 }  // namespace
 
 std::string random_graph(const Matrix& A, uint64_t seed) {
@@ -329,17 +377,16 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
     return t < bt * 0.99 || (t <= bt * 1.01 && (bytes < bb || (bytes == bb && c < bc)));  // A29 ties
   };
   int tried = 0;
-  Rng seq(cfg->seed);
-  for (int i = 0; i < maxc + cfg->n_seed_graphs; ++i) {
-    double el = std::chrono::duration<double>(clk::now() - t_start).count();
-    if (cfg->budget_seconds > 0 && el > cfg->budget_seconds && tried > 0) break;
-    if (i >= cfg->n_seed_graphs && tried >= maxc) break;
-    std::string text = i < cfg->n_seed_graphs ? std::string(cfg->seed_graphs[i]) : random_graph(M, seq.next());
+  std::set<std::string> seen;
+  // evaluate one candidate text: time it, keep the best plan (full-size runs); returns the
+  // median time or -1 (infeasible / rejected)
+  auto evaluate = [&](int i, const std::string& text, const char* tag) -> std::pair<double, std::string> {
     std::string canon;
     double t_med = -1;
     try {
       Plan* P = run(M, text, canon, t_med);
       ++tried;
+      seen.insert(canon);
       ranked.push_back({t_med, P->info.bytes_model, canon});
       if (!sampled && (!best_plan || better(t_med, P->info.bytes_model, canon, best_t, best_bytes, best_canon))) {
         delete best_plan;
@@ -350,12 +397,42 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       } else {
         delete P;
       }
-      logline(i, canon, sampled ? "sample" : "ok", t_med);
+      logline(i, canon, tag, t_med);
     } catch (const Error& e) {
       if (e.st == AS_ERR_CUDA) cudaGetLastError();
       set_last_error(e.msg);
+      if (!canon.empty()) seen.insert(canon);
       logline(i, canon.empty() ? text : canon,
               e.st == AS_ERR_PLAN_INFEASIBLE ? "infeasible" : e.st == AS_ERR_CUDA ? "cuda_error" : "rejected", -1);
+    }
+    return {t_med, canon};
+  };
+  auto elapsed = [&] { return std::chrono::duration<double>(clk::now() - t_start).count(); };
+  // step 1-2: random structures x coarse parameter grid; 60 % of the budget
+  Rng seq(cfg->seed);
+  for (int i = 0; i < maxc + cfg->n_seed_graphs; ++i) {
+    if (cfg->budget_seconds > 0 && elapsed() > 0.6 * cfg->budget_seconds && tried > 0) break;
+    if (i >= cfg->n_seed_graphs && tried >= maxc) break;
+    std::string text = i < cfg->n_seed_graphs ? std::string(cfg->seed_graphs[i]) : random_graph(M, seq.next());
+    evaluate(i, text, sampled ? "sample" : "ok");
+  }
+  // fine stage: simulated annealing over one-parameter neighbours of the incumbent, starting
+  // from the best coarse candidate ("terminated early by simulated annealing")
+  if (!ranked.empty()) {
+    auto it = std::min_element(ranked.begin(), ranked.end(), [](const Cand& a, const Cand& b) { return a.t < b.t; });
+    std::string cur = it->canon;
+    double tcur = it->t, temp = 0.05 * tcur;
+    Rng mr(cfg->seed ^ 0x5DEECE66Dull);
+    for (int step = 0; step < maxc; ++step) {
+      if (cfg->budget_seconds > 0 && elapsed() > cfg->budget_seconds) break;
+      std::string nb = mutate_graph(parse_graph(cur), mr);
+      if (nb.empty() || seen.count(nb)) continue;
+      auto [t, canon] = evaluate(1000 + step, nb, sampled ? "sample_refine" : "refine");
+      if (t > 0 && (t < tcur || mr.coin(std::exp(-(t - tcur) / std::max(temp, 1e-9))))) {
+        cur = canon;
+        tcur = t;
+      }
+      temp *= 0.85;
     }
   }
   if (sampled) {  // final: the seed graphs (expert designs) + the best 3 of the sample, full matrix
