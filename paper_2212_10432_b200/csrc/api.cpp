@@ -89,7 +89,8 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
     info.nnz_real = A.nnz();
     info.n_parts = (int64_t)P->host.parts.size();
     info.prepass_rows = (int64_t)P->host.prepass.size();
-    info.n_launches = (int64_t)P->host.launch_order.size() + (P->host.prepass.empty() ? 0 : 1);
+    info.n_launches = (int64_t)P->host.launch_order.size() + (P->host.prepass.empty() ? 0 : 1) +
+                      (P->n_heavy ? 1 : 0);  // heavy-row epilogue (the scratch memset is a copy op)
     int64_t slots = 0;
     for (auto& p : P->host.parts) {
       if (p.kind == "csr") slots += p.pad ? (int64_t)p.pad_val.size() : (int64_t)p.val.size();
@@ -104,6 +105,7 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
       if (!k.empty()) k += ";";
       k += P->host.parts[pi].fam_name;
     }
+    if (P->n_heavy) k += ";k_heavy_epilogue";
     std::strncpy(info.kernels, k.c_str(), sizeof(info.kernels) - 1);
     P->host_kept = device < 0 || (flags & AS_PLAN_KEEP_HOST);
     if (!P->host_kept) P->host = HostPlan();
@@ -297,12 +299,15 @@ as_status_t as_spmv(as_plan_t h, const void* alpha, const void* x, const void* b
     if (cur != P.device) cudaSetDevice(P.device);
     int err = 0;
     if (P.n_prepass) err = launch_prepass(P.d_prepass, P.n_prepass, b, y, P.dt == AS_R64F ? 1 : 0, stream);
+    if (P.n_heavy && !err)
+      err = (int)cudaMemsetAsync(P.d_heavy_acc, 0, (size_t)P.n_heavy * 8, (cudaStream_t)stream);
     for (size_t i = 0; i < P.launches.size() && !err; ++i) {
       DevPart d = P.launches[i];
       d.alpha = a;
       d.beta = b;
       err = launch_part(d, x, y, stream);
     }
+    if (P.n_heavy && !err) err = launch_heavy_epilogue(P.d_heavy_rows, P.d_heavy_acc, P.n_heavy, y, stream);
     if (cur != P.device) cudaSetDevice(cur);
     if (err) fail(AS_ERR_CUDA, std::string("launch: ") + cudaGetErrorString((cudaError_t)err));
   });

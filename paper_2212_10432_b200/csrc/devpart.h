@@ -82,6 +82,11 @@ struct DevPart {
   const int32_t* tile_row_ptr = nullptr;
   const int32_t* tile_col = nullptr;
   const void* tile_val = nullptr;
+  // fp32 plans: rows whose chain of fp32 partial additions would exceed the A25 bound add
+  // into an fp64 scratch instead (sorted global row ids, scratch slot = index)
+  const int32_t* heavy_rows = nullptr;
+  int64_t n_heavy = 0;
+  double* heavy_acc = nullptr;
   // launch
   int tpb = 256, grid = 0;
   size_t smem = 0;
@@ -93,6 +98,7 @@ struct DevPart {
 int launch_part(const DevPart& p, const void* x, void* y, void* stream);      // returns cudaError_t
 int launch_prepass(const int32_t* rows, int64_t n, double beta, void* y, int dtype, void* stream);
 int launch_scale_all(int64_t m, double beta, void* y, int dtype, void* stream);
+int launch_heavy_epilogue(const int32_t* rows, const double* acc, int64_t n, void* y, void* stream);  // fp32 y
 int prepare_part(DevPart& p);  // per-kernel attributes (smem opt-in); returns cudaError_t
 const char* fam_kernel_name(const DevPart& p);
 int device_max_smem_optin(int device);

@@ -97,9 +97,31 @@ __device__ __forceinline__ int64_t ldm(const int64_t* p) { return __ldg(p); }
 __device__ __forceinline__ int64_t out_row(const DevPart& p, int64_t r) {
   return p.origin ? (int64_t)ldm(p.origin + r) : p.origin_base + r;
 }
+// fp32 plans: scratch slot of a heavy row (A25), or -1
+__device__ __forceinline__ int64_t heavy_slot(const DevPart& p, int64_t g) {
+  int64_t lo = 0, hi = p.n_heavy - 1;
+  while (lo <= hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int64_t v = __ldg(p.heavy_rows + mid);
+    if (v == g) return mid;
+    if (v < g) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  return -1;
+}
+
 template <class V>
 __device__ __forceinline__ void write_excl(const DevPart& p, V* y, int64_t r, double acc) {
   int64_t g = out_row(p, r);
+  if constexpr (sizeof(V) == 4) {
+    if (p.n_heavy && p.mode == 1) {
+      const int64_t sl = heavy_slot(p, g);
+      if (sl >= 0) {
+        atomicAdd(p.heavy_acc + sl, p.alpha * acc);
+        return;
+      }
+    }
+  }
   if (p.mode == 0) {
     double v = p.alpha * acc;
     if (p.beta != 0.0) v += p.beta * (double)y[g];
@@ -110,7 +132,17 @@ __device__ __forceinline__ void write_excl(const DevPart& p, V* y, int64_t r, do
 }
 template <class V>
 __device__ __forceinline__ void write_atom(const DevPart& p, V* y, int64_t r, double acc) {
-  atomicAdd(y + out_row(p, r), (V)(p.alpha * acc));
+  const int64_t g = out_row(p, r);
+  if constexpr (sizeof(V) == 4) {
+    if (p.n_heavy) {
+      const int64_t sl = heavy_slot(p, g);
+      if (sl >= 0) {
+        atomicAdd(p.heavy_acc + sl, p.alpha * acc);  // fp64 accumulation (A2, A25)
+        return;
+      }
+    }
+  }
+  atomicAdd(y + g, (V)(p.alpha * acc));
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -1145,6 +1177,15 @@ __global__ void k_prepass(const int32_t* __restrict__ rows, int64_t n, double be
     y[r] = beta == 0.0 ? (V)0 : (V)(beta * (double)y[r]);
   }
 }
+// heavy rows of fp32 plans: y[r] += (float)acc (one rounding of the fp64 sum)
+__global__ void k_heavy_epilogue(const int32_t* __restrict__ rows, const double* __restrict__ acc, int64_t n,
+                                 float* __restrict__ y) {
+  for (int64_t i = gtid(); i < n; i += gthreads()) {
+    const int64_t r = rows[i];
+    y[r] = (float)((double)y[r] + acc[i]);
+  }
+}
+
 template <class V>
 __global__ void k_scale_all(int64_t m, double beta, V* __restrict__ y) {
   for (int64_t i = gtid(); i < m; i += gthreads()) y[i] = beta == 0.0 ? (V)0 : (V)(beta * (double)y[i]);
@@ -1305,6 +1346,13 @@ int launch_prepass(const int32_t* rows, int64_t n, double beta, void* y, int dty
   int64_t g = std::min<int64_t>((n + 255) / 256, 148 * 16);
   if (dtype == 1) k_prepass<double><<<g, 256, 0, (cudaStream_t)stream>>>(rows, n, beta, (double*)y);
   else k_prepass<float><<<g, 256, 0, (cudaStream_t)stream>>>(rows, n, beta, (float*)y);
+  return (int)cudaGetLastError();
+}
+
+int launch_heavy_epilogue(const int32_t* rows, const double* acc, int64_t n, void* y, void* stream) {
+  if (n <= 0) return 0;
+  int64_t g = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_heavy_epilogue<<<g, 256, 0, (cudaStream_t)stream>>>(rows, acc, n, (float*)y);
   return (int)cudaGetLastError();
 }
 

@@ -170,6 +170,51 @@ void Plan::try_xwin(const HostPart& h, DevPart& d, cudaStream_t s) {
   bytes_model += (double)(win.size() * 4);
 }
 
+// A25 for fp32 plans: a row whose value is assembled from more than 167 fp32 additions
+// (1e-5 / 2^-24; atomic partials of the units it spans plus ADDs from other parts) could
+// exceed the fp32 tolerance; such rows accumulate in an fp64 scratch instead and are added
+// to y once by an epilogue (k_heavy_epilogue).
+void Plan::mark_heavy_rows(cudaStream_t s) {
+  const int64_t kBound = 167;
+  std::vector<int32_t> cnt((size_t)m, 0);
+  for (int64_t pi : host.launch_order) {
+    const HostPart& h = host.parts[pi];
+    for (int64_t r : h.excl) cnt[r] += 1;
+    if (h.atom.empty()) continue;
+    int top = -1;
+    for (int l = 2; l >= 0; --l)
+      if (h.red[l] != RED_NONE) top = l;
+    const int64_t mp = (int64_t)h.origin.size();
+    int64_t u = 0;
+    for (int64_t r = 0; r < mp; ++r) {
+      const int64_t a = h.row_ptr[r], e = h.row_ptr[r + 1];
+      int64_t span;
+      if (top < 0) {
+        span = e - a;
+      } else {
+        const std::vector<int64_t>& st = h.lv[top].start;
+        while (st[u + 1] <= a) ++u;
+        int64_t v = u;
+        while (st[v + 1] < e) ++v;
+        span = v - u + 1;
+      }
+      if (span > 1) cnt[h.origin[r]] += (int32_t)std::min<int64_t>(span, INT32_MAX / 4);
+    }
+  }
+  std::vector<int64_t> heavy;
+  for (int64_t r = 0; r < m; ++r)
+    if (cnt[r] > kBound) heavy.push_back(r);
+  if (heavy.empty()) return;
+  d_heavy_rows = up_i32(heavy, s, "heavy_rows");
+  n_heavy = (int64_t)heavy.size();
+  d_heavy_acc = (double*)up(nullptr, 0, s, (size_t)n_heavy * 8);
+  for (auto& d : launches) {
+    d.heavy_rows = d_heavy_rows;
+    d.n_heavy = n_heavy;
+    d.heavy_acc = d_heavy_acc;
+  }
+}
+
 Plan::~Plan() {
   if (device >= 0) {
     int cur = 0;
@@ -389,6 +434,7 @@ void Plan::upload(cudaStream_t s) {
     d_prepass = up_i32(host.prepass, s, "prepass");
     n_prepass = (int64_t)host.prepass.size();
   }
+  if (dt == AS_R32F) mark_heavy_rows(s);
   ck(cudaStreamSynchronize(s), "upload");
 }
 

@@ -30,6 +30,10 @@ struct Plan {
   void upload(cudaStream_t s);
   void upload_pad(const HostPart& h, DevPart& d, cudaStream_t s);
   void try_xwin(const HostPart& h, DevPart& d, cudaStream_t s);
+  void mark_heavy_rows(cudaStream_t s);
+  const int32_t* d_heavy_rows = nullptr;  // fp32 A25 heavy rows (sorted) + fp64 scratch
+  double* d_heavy_acc = nullptr;
+  int64_t n_heavy = 0;
   void compute_model();
 };
 

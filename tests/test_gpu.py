@@ -83,6 +83,32 @@ def test_random_graphs(seed):
         assert e.status == "AS_ERR_PLAN_INFEASIBLE", (text, e)
 
 
+@pytest.mark.parametrize("graph", [
+    "COMPRESS; BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; GMEM_ATOM_RED",
+    "COMPRESS; BMW_NNZ_BLOCK(64); BMT_NNZ_BLOCK(2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
+    "COMPRESS; BMTB_NNZ_BLOCK(32); SHMEM_OFFSET_RED; GMEM_ATOM_RED",
+    "COL_DIV(cuts=[5000,10000,20000]) { COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
+])
+def test_fp32_heavy_rows(graph):
+    """A25: an fp32 hub row split over thousands of writer units must stay within 1e-5 of
+    sum|a x|: its partials go to the fp64 heavy-row accumulator."""
+    g = np.random.default_rng(5)
+    m, n = 2000, 60000
+    rows = [np.full(n, 7)]                       # one dense hub row of 60,000 nonzeros
+    cols = [np.arange(n)]
+    for r in range(m):
+        if r != 7:
+            c = np.sort(g.choice(n, 5, replace=False))
+            rows.append(np.full(5, r))
+            cols.append(c)
+    row = np.concatenate(rows).astype(np.int64)
+    col = np.concatenate(cols).astype(np.int64)
+    order = np.lexsort((col, row))
+    coo = synth.Coo(m, n, row[order], col[order], g.uniform(-1, 1, row.shape[0]).astype(np.float32))
+    P, ratio = run_check(coo, graph, 1.0, 0.5, seed=2)
+    assert "k_heavy_epilogue" in P.info()["kernels"]
+
+
 def test_beta_zero_ignores_nan():
     coo = synth.random_matrix(50, 40, 0.2, 1)
     for g in FAMILY_GRAPHS[:4]:

@@ -24,9 +24,14 @@ def _mat(c):
     return asp.Matrix.from_csr(c.m, c.n, c.row_ptr, c.col, c.val)
 
 
-def _sample_rows(m, seed=0):
-    return np.unique(np.concatenate([np.arange(0, min(m, 4096)), np.arange(max(0, m - 4096), m),
-                                     np.random.default_rng(seed).integers(0, m, 20000)]))
+def _sample_rows(m, seed=0, row_ptr=None):
+    """first/last 4096 rows, 20,000 random rows, and the 256 longest rows (hub rows carry
+    the longest accumulation / atomic chains)."""
+    parts = [np.arange(0, min(m, 4096)), np.arange(max(0, m - 4096), m),
+             np.random.default_rng(seed).integers(0, m, 20000)]
+    if row_ptr is not None:
+        parts.append(np.argsort(-np.diff(row_ptr), kind="stable")[:256])
+    return np.unique(np.concatenate(parts))
 
 
 def run_sampled(c, P, alpha, beta, seed, int_mode=False):
@@ -35,7 +40,7 @@ def run_sampled(c, P, alpha, beta, seed, int_mode=False):
     P.spmv(alpha, dx, beta, dy)
     torch.cuda.synchronize()
     y = dy.cpu().numpy()
-    rows = _sample_rows(c.m, seed)
+    rows = _sample_rows(c.m, seed, c.row_ptr)
     rp, col, val = c.rows(rows)
     yref, bound = S.spmv_csr(rp, col, val.astype(np.float64), x.astype(np.float64), alpha, beta,
                              y0[rows].astype(np.float64), nthreads=os.cpu_count() or 1)
@@ -72,6 +77,10 @@ C3_GRAPHS = [
     "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,1); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
     "COMPRESS; BMT_NNZ_BLOCK(16); BMT_PAD(GLOBAL,1); THREAD_BITMAP_RED_G; GMEM_ATOM_RED",
     "SORT; COMPRESS; BMTB_ROW_BLOCK(1); SHMEM_TOTAL_RED; GMEM_ATOM_RED",
+    # hub rows span thousands of BMTs: fp32 atomic chains beyond the A25 bound go through
+    # the fp64 heavy-row accumulator
+    "COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=256,grid=16); GMEM_ATOM_RED",
+    "COMPRESS; BMW_NNZ_BLOCK(2048); BMT_NNZ_BLOCK(2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
 ]
 
 
