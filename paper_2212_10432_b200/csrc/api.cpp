@@ -298,7 +298,14 @@ as_status_t as_spmv(as_plan_t h, const void* alpha, const void* x, const void* b
     cudaGetDevice(&cur);
     if (cur != P.device) cudaSetDevice(P.device);
     int err = 0;
-    if (P.n_prepass) err = launch_prepass(P.d_prepass, P.n_prepass, b, y, P.dt == AS_R64F ? 1 : 0, stream);
+    if (P.n_prepass) {
+      // beta == 0: y is write-only, so zeroing all of y is as correct as zeroing the listed
+      // rows; a plain fill beats the indexed pre-pass once the list covers most rows
+      if (b == 0.0 && (double)P.m * sv <= 1.5 * (double)P.n_prepass * (4 + sv))
+        err = (int)cudaMemsetAsync(y, 0, (size_t)P.m * sv, (cudaStream_t)stream);
+      else
+        err = launch_prepass(P.d_prepass, P.n_prepass, b, y, P.dt == AS_R64F ? 1 : 0, stream);
+    }
     if (P.n_heavy && !err)
       err = (int)cudaMemsetAsync(P.d_heavy_acc, 0, (size_t)P.n_heavy * 8, (cudaStream_t)stream);
     for (size_t i = 0; i < P.launches.size() && !err; ++i) {

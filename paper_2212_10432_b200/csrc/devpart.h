@@ -85,6 +85,7 @@ struct DevPart {
   // fp32 plans: rows whose chain of fp32 partial additions would exceed the A25 bound add
   // into an fp64 scratch instead (sorted global row ids, scratch slot = index)
   const int32_t* heavy_rows = nullptr;
+  const uint32_t* heavy_bits = nullptr;   // 1 bit per global row: is heavy
   int64_t n_heavy = 0;
   double* heavy_acc = nullptr;
   // launch

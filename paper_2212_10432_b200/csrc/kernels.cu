@@ -97,8 +97,10 @@ __device__ __forceinline__ int64_t ldm(const int64_t* p) { return __ldg(p); }
 __device__ __forceinline__ int64_t out_row(const DevPart& p, int64_t r) {
   return p.origin ? (int64_t)ldm(p.origin + r) : p.origin_base + r;
 }
-// fp32 plans: scratch slot of a heavy row (A25), or -1
+// fp32 plans: scratch slot of a heavy row (A25), or -1.  A 1-bit-per-row filter (L1/L2
+// resident) answers the common case; only heavy rows pay the binary search.
 __device__ __forceinline__ int64_t heavy_slot(const DevPart& p, int64_t g) {
+  if (!((__ldg(p.heavy_bits + (g >> 5)) >> (g & 31)) & 1u)) return -1;
   int64_t lo = 0, hi = p.n_heavy - 1;
   while (lo <= hi) {
     const int64_t mid = (lo + hi) >> 1;

@@ -208,7 +208,12 @@ void Plan::mark_heavy_rows(cudaStream_t s) {
   d_heavy_rows = up_i32(heavy, s, "heavy_rows");
   n_heavy = (int64_t)heavy.size();
   d_heavy_acc = (double*)up(nullptr, 0, s, (size_t)n_heavy * 8);
+  std::vector<uint32_t> bits((size_t)(m / 32 + 1), 0u);
+  for (int64_t r : heavy) bits[(size_t)(r >> 5)] |= 1u << (r & 31);
+  const uint32_t* d_bits = (const uint32_t*)up(bits.data(), bits.size() * 4, s);
+  cudaStreamSynchronize(s);
   for (auto& d : launches) {
+    d.heavy_bits = d_bits;
     d.heavy_rows = d_heavy_rows;
     d.n_heavy = n_heavy;
     d.heavy_acc = d_heavy_acc;
