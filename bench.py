@@ -8,7 +8,8 @@ inputs resident in HBM.  L2 is flushed (memset of 2 x L2 bytes) before every tim
 outside the timed events.
 
 Multi-GPU (torchrun, one rank per GPU): ROW_DIV bands with nnz-balanced cuts (reading A35),
-each rank plans/searches its own band; y all-gather over NCCL only with --allgather.
+each rank plans/searches its own band; the y -> x exchange (all-gather over NCCL, or the
+halo of banded matrices) runs only with --exchange allgather|halo.
 `--impl reference` times the oracle (long-double CPU SpMV) on the host instead.
 """
 from __future__ import annotations
@@ -194,7 +195,8 @@ def main():
     ap.add_argument("--search-candidates", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--allgather", action="store_true")
+    ap.add_argument("--exchange", default="none", choices=["none", "allgather", "halo"],
+                    help="y -> next x exchange after the SpMV (N > 1), timed separately")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no search/baseline/e2e)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile else args.warmup
@@ -275,19 +277,23 @@ def main():
             step()
             e1.record(stream)
         torch.cuda.synchronize()
-        if args.allgather and dist:
-            # y all-gather (uneven bands): NCCL broadcasts of each rank's slice
-            y_full = torch.zeros(coo.m, dtype=dy.dtype, device="cuda")
+        gather_ms = None
+        if args.exchange != "none" and dist:
+            # y -> next x: all-gather (uneven bands, NCCL broadcasts) or halo (P2P of the
+            # band's column span only, NEXT-1), timed separately from the SpMV
+            from paper_2212_10432_b200 import dist as D
+            x_next = torch.zeros(coo.m, dtype=dy.dtype, device="cuda")
+            moves = D.halo_plan(D.gather_spans(A.col_span()), cuts) if args.exchange == "halo" else None
+            dist.barrier()
             g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             g0.record(stream)
-            y_full[r0:r1] = dy
-            for r in range(world):
-                dist.broadcast(y_full[int(cuts[r]):int(cuts[r + 1])], src=r)
+            if args.exchange == "halo":
+                D.halo_exchange(dy, x_next, cuts, moves)
+            else:
+                D.allgather_rows(dy, x_next, cuts)
             g1.record(stream)
             torch.cuda.synchronize()
             gather_ms = g0.elapsed_time(g1)
-        else:
-            gather_ms = None
     ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     t_ms = statistics.mean(ms)
     if dist:
@@ -363,7 +369,7 @@ def main():
         "e2e": e2e,
     }
     if gather_ms is not None:
-        line["allgather_ms"] = gather_ms
+        line["exchange"] = {"kind": args.exchange, "ms": gather_ms}
     if not args.no_cpu_baseline and not args.profile and world == 1:
         line["cpu_baseline"] = cpu_baseline(coo, wl)
     print(json.dumps(line))

@@ -163,6 +163,10 @@ as_status_t as_random_graph(as_matrix_t, uint64_t seed, char* buf, size_t* len);
 /* ---------------------------------------------------------------- e: multi-GPU helpers
  * nnz-balanced ROW_DIV cuts over `world` ranks (reading A35): cuts[world+1]. */
 as_status_t as_dist_row_cuts(as_matrix_t, int world, int64_t* cuts);
+/* Column span [*lo, *hi] referenced by the matrix (a ROW_DIV band): the x rows a rank needs
+ * from its peers when y becomes the next x (halo exchange).  An empty
+ * matrix gives lo = 0, hi = -1. */
+as_status_t as_matrix_col_span(as_matrix_t, int64_t* lo, int64_t* hi);
 
 #ifdef __cplusplus
 }

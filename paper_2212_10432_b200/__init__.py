@@ -82,12 +82,13 @@ _sig("as_spmv_host", [_vp, _vp, _vp, _vp, _vp, _vp])
 _sig("as_search", [_vp, _P(AsSearchCfg), _i32, _vp, _P(_vp), ctypes.c_char_p, _P(_sz)])
 _sig("as_random_graph", [_vp, ctypes.c_uint64, ctypes.c_char_p, _P(_sz)])
 _sig("as_dist_row_cuts", [_vp, _i32, _vp])
+_sig("as_matrix_col_span", [_vp, _vp, _vp])
 
 EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create_csr", "as_matrix_create_mtx",
             "as_matrix_stats", "as_matrix_row_slice", "as_matrix_export_csr", "as_matrix_destroy", "as_graph_parse",
             "as_graph_print", "as_graph_destroy", "as_plan", "as_plan_ex", "as_plan_info", "as_plan_export",
             "as_plan_keys", "as_plan_destroy", "as_spmv", "as_spmv_host", "as_search", "as_random_graph",
-            "as_dist_row_cuts"]
+            "as_dist_row_cuts", "as_matrix_col_span"]
 
 
 class AsError(RuntimeError):
@@ -181,6 +182,11 @@ class Matrix:
         val = np.zeros(s["nnz"], self.dtype)
         _ck(_lib.as_matrix_export_csr(self._h, rp.ctypes.data, col.ctypes.data, val.ctypes.data))
         return rp, col, val
+
+    def col_span(self):
+        lo, hi = ctypes.c_int64(), ctypes.c_int64()
+        _ck(_lib.as_matrix_col_span(self._h, ctypes.byref(lo), ctypes.byref(hi)))
+        return lo.value, hi.value
 
     def row_cuts(self, world: int) -> np.ndarray:
         cuts = np.zeros(world + 1, np.int64)

@@ -366,6 +366,19 @@ as_status_t as_random_graph(as_matrix_t M, uint64_t seed, char* buf, size_t* len
   return copy_string(s, buf, len);
 }
 
+as_status_t as_matrix_col_span(as_matrix_t M, int64_t* lo, int64_t* hi) {
+  return guard([&] {
+    if (!M || !lo || !hi) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    int64_t a = INT64_MAX, b = -1;
+    for (int32_t c : M->A.col) {
+      a = std::min<int64_t>(a, c);
+      b = std::max<int64_t>(b, c);
+    }
+    *lo = b < 0 ? 0 : a;
+    *hi = b;
+  });
+}
+
 as_status_t as_dist_row_cuts(as_matrix_t M, int world, int64_t* cuts) {
   return guard([&] {
     if (!M || !cuts) fail(AS_ERR_INVALID_ARG, "NULL argument");
