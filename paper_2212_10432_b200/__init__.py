@@ -19,6 +19,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libalphasparse.so")
+if os.environ.get("AS_LIB_AB"):  # developer A/B timing of another in-tree build (tools/sweep.py)
+    LIB_PATH = os.path.join(_HERE, "..", os.environ["AS_LIB_AB"])
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
 _lib = ctypes.CDLL(LIB_PATH)

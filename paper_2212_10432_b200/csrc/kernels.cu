@@ -388,6 +388,56 @@ struct XRing {
   __device__ __forceinline__ double operator()(int64_t c) const { return (double)ring[c & mask]; }
 };
 
+// One batch of KB elements starting at j0.  FULL: j0 + KB <= len, so no bounds predicates
+// (the common case: every batch but the BMT's last).
+template <class V, bool PAD, int VEC, int KB, bool FULL, class XA, class Seg>
+__device__ __forceinline__ void bmt_batch(XA xa, const uint32_t* bm, const V* pv, const int32_t* pc, int64_t stride,
+                                          int j0, int len, int64_t& row, double& acc, bool& inside, Seg& seg) {
+  double v[KB];
+  int32_t c[KB];
+  if constexpr (PAD) {
+#pragma unroll
+    for (int q = 0; q < KB; q += VEC) {
+      if (FULL || j0 + q < len) {
+        PadLoad<V, VEC>::ld(pv + ((j0 + q) / VEC) * stride, pc + ((j0 + q) / VEC) * stride, v + q, c + q);
+      } else {
+#pragma unroll
+        for (int r = 0; r < VEC; ++r) {
+          v[q + r] = 0.0;
+          c[q + r] = 0;
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      if (FULL || j0 + q < len) {
+        v[q] = (double)ld_seq(pv + j0 + q);
+        c[q] = ld_seq(pc + j0 + q);
+      } else {
+        v[q] = 0.0;
+        c[q] = 0;
+      }
+    }
+  }
+  double xv[KB];
+#pragma unroll
+  for (int q = 0; q < KB; ++q) xv[q] = (FULL || j0 + q < len) ? xa(c[q]) : 0.0;
+  // head bits of this batch; element 0 of the BMT never cuts (its head state is `inside`)
+  const uint32_t wd = (ldm(bm + (j0 >> 5)) >> (j0 & 31)) & ~(uint32_t)(j0 == 0);
+#pragma unroll
+  for (int q = 0; q < KB; ++q) {
+    if (!FULL && j0 + q >= len) break;
+    if ((wd >> q) & 1u) {
+      seg(row, acc, inside);
+      ++row;
+      acc = 0.0;
+      inside = true;
+    }
+    acc += v[q] * xv[q];
+  }
+}
+
 template <class V, bool PAD, int VEC, int KB, class XA, class Seg>
 __device__ __forceinline__ void bmt_pass(const DevPart& p, XA xa, const uint32_t* bm, PadPos pp, int64_t a, int len,
                                          int64_t& row, double& acc, bool& inside, Seg seg) {
@@ -400,51 +450,11 @@ __device__ __forceinline__ void bmt_pass(const DevPart& p, XA xa, const uint32_t
   acc = 0.0;
   const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;
   const int32_t* pc = PAD ? p.pad_col + pp.base : p.col + a;
-  for (int j0 = 0; j0 < len; j0 += KB) {
-    double v[KB];
-    int32_t c[KB];
-    if constexpr (PAD) {
-#pragma unroll
-      for (int q = 0; q < KB; q += VEC) {
-        if (j0 + q < len) {
-          PadLoad<V, VEC>::ld(pv + ((j0 + q) / VEC) * pp.stride, pc + ((j0 + q) / VEC) * pp.stride, v + q, c + q);
-        } else {
-#pragma unroll
-          for (int r = 0; r < VEC; ++r) {
-            v[q + r] = 0.0;
-            c[q + r] = 0;
-          }
-        }
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < KB; ++q) {
-        if (j0 + q < len) {
-          v[q] = (double)ld_seq(pv + j0 + q);
-          c[q] = ld_seq(pc + j0 + q);
-        } else {
-          v[q] = 0.0;
-          c[q] = 0;
-        }
-      }
-    }
-    double xv[KB];
-#pragma unroll
-    for (int q = 0; q < KB; ++q) xv[q] = (j0 + q < len) ? xa(c[q]) : 0.0;
-    const uint32_t wd = ldm(bm + (j0 >> 5)) >> (j0 & 31);
-#pragma unroll
-    for (int q = 0; q < KB; ++q) {
-      const int64_t j = j0 + q;
-      if (j >= len) break;
-      if (j && ((wd >> q) & 1u)) {
-        seg(row, acc, inside);
-        ++row;
-        acc = 0.0;
-        inside = true;
-      }
-      acc += v[q] * xv[q];
-    }
-  }
+  const int full = len & ~(KB - 1);
+  int j0 = 0;
+  for (; j0 < full; j0 += KB)
+    bmt_batch<V, PAD, VEC, KB, true>(xa, bm, pv, pc, pp.stride, j0, len, row, acc, inside, seg);
+  if (j0 < len) bmt_batch<V, PAD, VEC, KB, false>(xa, bm, pv, pc, pp.stride, j0, len, row, acc, inside, seg);
 }
 
 // =====================================================================================
@@ -486,7 +496,7 @@ __global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restr
 // =====================================================================================
 template <class V, bool PAD, int VEC>
 __global__ void __launch_bounds__(1024) k_nnz_thread_xw(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   V* ring = (V*)smem_raw;
   const int64_t mask = p.xw_size - 1;
   const int64_t per = (p.n_bmt + gridDim.x - 1) / gridDim.x;
@@ -954,7 +964,7 @@ __global__ void __launch_bounds__(1024) k_block_offset_tma(DevPart p, const V* _
 // =====================================================================================
 template <class V>
 __global__ void __launch_bounds__(1024) k_block_offset(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   double* prod = (double*)smem_raw;  // max_block_nnz products
   const V* val = (const V*)p.val;
   for (int64_t b = blockIdx.x; b < p.n_bmtb; b += gridDim.x) {
@@ -1240,8 +1250,9 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       }
       int64_t g = grid_for(p, p.n_bmt, tpb);
       const int tt = tpb;
-      // batches of 8 loads per thread (16 measured slower on c5s: 394 vs 245 us, occupancy)
-#define AS_NT(PADV, VECV) k_nnz_thread<V, PADV, VECV, 8><<<g, tt, 0, s>>>(p, x, y);
+      // batches of KB loads per thread: 8 for fp64, 4 for fp32 (A/B on c5s fp64: KB 4 633 vs
+      // KB 8 646 GF/s; c3s fp32: 408 vs 394; KB 16 or 80 registers slower everywhere)
+#define AS_NT(PADV, VECV) k_nnz_thread<V, PADV, VECV, (sizeof(V) == 4 && VECV <= 4 ? 4 : 8)><<<g, tt, 0, s>>>(p, x, y);
       if (!p.pad) {
         AS_NT(false, 1)
       } else if (p.vec == 1) {
