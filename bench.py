@@ -9,7 +9,7 @@ outside the timed events.
 
 Multi-GPU (torchrun, one rank per GPU): ROW_DIV bands with nnz-balanced cuts (reading A35),
 each rank plans/searches its own band; the y -> x exchange (all-gather over NCCL, or the
-halo of banded matrices) runs only with --exchange allgather|halo.
+halo of banded matrices) runs only with --exchange allgather|halo|nccl|peer.
 `--impl reference` times the oracle (long-double CPU SpMV) on the host instead.
 """
 from __future__ import annotations
@@ -195,8 +195,10 @@ def main():
     ap.add_argument("--search-candidates", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--exchange", default="none", choices=["none", "allgather", "halo"],
-                    help="y -> next x exchange after the SpMV (N > 1), timed separately")
+    ap.add_argument("--exchange", default="none", choices=["none", "allgather", "halo", "nccl", "peer"],
+                    help="y -> next x exchange after the SpMV (N > 1), timed separately: allgather/halo "
+                         "over torch.distributed; nccl/peer = as_spmv_dist (C-ABI: SpMV + AllGatherV, or "
+                         "SpMV + peer-memory push), timed as whole steps")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no search/baseline/e2e)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile else args.warmup
@@ -278,7 +280,31 @@ def main():
             e1.record(stream)
         torch.cuda.synchronize()
         gather_ms = None
-        if args.exchange != "none" and dist:
+        if args.exchange in ("nccl", "peer") and dist:
+            # as_spmv_dist: band SpMV into y_full + the exchange inside the library
+            from paper_2212_10432_b200 import dist as D
+            d = D.init_dist(rank, world, local, cuts, nccl=args.exchange == "nccl")
+            y_full = torch.zeros(coo.m, dtype=dy.dtype, device="cuda")
+            if args.exchange == "peer":
+                D.register_peers(d, y_full)
+            for _ in range(3):
+                d.spmv(P, 1.0, dx, 0.0, y_full, args.exchange, stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+            gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for g0, g1 in gev:
+                if not args.no_flush:
+                    flush_l2()
+                g0.record(stream)
+                d.spmv(P, 1.0, dx, 0.0, y_full, args.exchange, stream)
+                g1.record(stream)
+            torch.cuda.synchronize()
+            d.check()
+            gather_ms = statistics.mean(g0.elapsed_time(g1) for g0, g1 in gev)
+            dist.barrier()
+            d.close()
+        elif args.exchange != "none" and dist:
             # y -> next x: all-gather (uneven bands, NCCL broadcasts) or halo (P2P of the
             # band's column span only, NEXT-1), timed separately from the SpMV
             from paper_2212_10432_b200 import dist as D
@@ -294,6 +320,10 @@ def main():
             g1.record(stream)
             torch.cuda.synchronize()
             gather_ms = g0.elapsed_time(g1)
+    if gather_ms is not None:
+        gm = torch.tensor([gather_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(gm, op=dist.ReduceOp.MAX)
+        gather_ms = float(gm.item())
     ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     t_ms = statistics.mean(ms)
     if dist:
@@ -369,7 +399,9 @@ def main():
         "e2e": e2e,
     }
     if gather_ms is not None:
-        line["exchange"] = {"kind": args.exchange, "ms": gather_ms}
+        line["exchange"] = {"kind": args.exchange, "ms": gather_ms,
+                            "timed": "spmv + exchange per step (as_spmv_dist)" if args.exchange in ("nccl", "peer")
+                            else "exchange only"}
     if not args.no_cpu_baseline and not args.profile and world == 1:
         line["cpu_baseline"] = cpu_baseline(coo, wl)
     print(json.dumps(line))

@@ -43,7 +43,8 @@ typedef enum {
   AS_ERR_CUDA = 9,
   AS_ERR_NO_FEASIBLE = 10,     /* as_search: no candidate could be planned */
   AS_ERR_DTYPE = 11,
-  AS_ERR_NOT_FOUND = 12        /* as_plan_export: key not present in this plan */
+  AS_ERR_NOT_FOUND = 12,       /* as_plan_export: key not present in this plan */
+  AS_ERR_NCCL = 13             /* NCCL missing or an NCCL call failed (as_dist_*) */
 } as_status_t;
 
 typedef enum { AS_R32F = 0, AS_R64F = 1 } as_dtype_t;
@@ -160,6 +161,17 @@ as_status_t as_search(as_matrix_t, const as_search_cfg_t*, int device, void* str
 /* One random legal graph text for this matrix (the search's generator), for tests. */
 as_status_t as_random_graph(as_matrix_t, uint64_t seed, char* buf, size_t* len);
 
+/* ---------------------------------------------------------------- device memory
+ * Route every device allocation of the library (plan arrays, as_spmv_host / as_search
+ * scratch, dist flags) through caller hooks, e.g. torch's caching allocator:
+ * alloc(bytes, stream, ctx) returns device memory of the current device or NULL (->
+ * AS_ERR_OOM); release(ptr, stream, ctx) frees it.  Both NULL restores cudaMalloc/cudaFree.
+ * Process-wide; set it before creating plans (a plan frees through the hooks that were
+ * active when it was created only if they are still installed: do not swap hooks while
+ * plans are alive). */
+as_status_t as_set_allocator(void* (*alloc)(size_t bytes, void* stream, void* ctx),
+                             void (*release)(void* ptr, void* stream, void* ctx), void* ctx);
+
 /* ---------------------------------------------------------------- e: multi-GPU helpers
  * nnz-balanced ROW_DIV cuts over `world` ranks (reading A35): cuts[world+1]. */
 as_status_t as_dist_row_cuts(as_matrix_t, int world, int64_t* cuts);
@@ -167,6 +179,49 @@ as_status_t as_dist_row_cuts(as_matrix_t, int world, int64_t* cuts);
  * from its peers when y becomes the next x (halo exchange).  An empty
  * matrix gives lo = 0, hi = -1. */
 as_status_t as_matrix_col_span(as_matrix_t, int64_t* lo, int64_t* hi);
+
+/* ---------------------------------------------------------------- e: multi-GPU SpMV
+ * ROW_DIV across ranks ("divide the matrix in the row direction", P:46
+ * ROW_DIV example): one process per GPU; rank r owns rows [cuts[r], cuts[r+1]) of y (the
+ * nnz-balanced cuts of as_dist_row_cuts), holds a plan of its band
+ * (as_matrix_row_slice(A, cuts[r], cuts[r+1]), global column indices) and the full x.
+ * The SpMV itself needs no communication; the exchange makes the new y whole on every rank
+ * (it is the next x of an iterative solver, north_star):
+ *   AS_EXCH_NONE  only the band y_full[cuts[r]:cuts[r+1]] is written;
+ *   AS_EXCH_NCCL  AllGatherV of the bands: one ncclBroadcast per rank inside an NCCL group
+ *                 (needs a communicator: as_dist_init with an id);
+ *   AS_EXCH_PEER  the band is pushed by one kernel straight into every peer's y_full over
+ *                 peer memory (NVLink P2P stores through CUDA IPC mappings, no NCCL), then
+ *                 each rank's stream waits for its peers' release flags (one epoch per
+ *                 call).  y_full must be registered on every rank first
+ *                 (as_dist_ipc_handle + as_dist_open_peers).  The wait times out after
+ *                 AS_DIST_WAIT_TIMEOUT_NS and reports AS_ERR_CUDA at as_dist_check.
+ * Every rank must make the same sequence of as_spmv_dist calls.  x_full and y_full must
+ * not alias (iterate with two buffers).  NCCL is loaded at run time (dlopen
+ * libnccl.so.2), so the library itself has no link-time NCCL dependency. */
+typedef struct as_dist_s* as_dist_t;
+#define AS_DIST_ID_BYTES 128      /* ncclUniqueId */
+#define AS_DIST_HANDLE_BYTES 256  /* one rank's IPC registration blob */
+#define AS_DIST_MAX_WORLD 64
+#define AS_DIST_WAIT_TIMEOUT_NS 20000000000ull
+enum { AS_EXCH_NONE = 0, AS_EXCH_NCCL = 1, AS_EXCH_PEER = 2 };
+/* ncclGetUniqueId into id[AS_DIST_ID_BYTES] (rank 0; the caller broadcasts the bytes). */
+as_status_t as_dist_unique_id(void* id);
+/* Communicator of `world` ranks on `device`.  id NULL: peer-memory mode only (no NCCL). */
+as_status_t as_dist_init(int rank, int world, const void* id, int device, as_dist_t* out);
+/* The world+1 row cuts of y (as_dist_row_cuts); required before as_spmv_dist. */
+as_status_t as_dist_set_cuts(as_dist_t, const int64_t* cuts);
+/* IPC registration of this rank's y buffer `y_full` (device memory from cudaMalloc or a
+ * caching allocator built on it): writes handle[AS_DIST_HANDLE_BYTES] to be all-gathered
+ * by the caller (any transport), in rank order, then passed to as_dist_open_peers. */
+as_status_t as_dist_ipc_handle(as_dist_t, void* y_full, void* handle);
+as_status_t as_dist_open_peers(as_dist_t, void* y_full, const void* handles /* world x HANDLE_BYTES */);
+as_status_t as_spmv_dist(as_dist_t, as_plan_t local, const void* alpha, const void* x_full,
+                         const void* beta, void* y_full, int exchange, void* stream);
+/* Device-side status of the peer exchange (AS_ERR_CUDA after a wait timeout); synchronizes
+ * the dist's device. */
+as_status_t as_dist_check(as_dist_t);
+void as_dist_destroy(as_dist_t);
 
 #ifdef __cplusplus
 }

@@ -29,7 +29,10 @@ AS_R32F, AS_R64F = 0, 1
 AS_PLAN_KEEP_HOST = 1
 STATUS = {0: "AS_OK", 1: "AS_ERR_INVALID_ARG", 2: "AS_ERR_MALFORMED", 3: "AS_ERR_INDEX_OUT_OF_RANGE",
           4: "AS_ERR_DUPLICATE", 5: "AS_ERR_GRAPH_PARSE", 6: "AS_ERR_GRAPH_ILLEGAL", 7: "AS_ERR_PLAN_INFEASIBLE",
-          8: "AS_ERR_OOM", 9: "AS_ERR_CUDA", 10: "AS_ERR_NO_FEASIBLE", 11: "AS_ERR_DTYPE", 12: "AS_ERR_NOT_FOUND"}
+          8: "AS_ERR_OOM", 9: "AS_ERR_CUDA", 10: "AS_ERR_NO_FEASIBLE", 11: "AS_ERR_DTYPE", 12: "AS_ERR_NOT_FOUND",
+          13: "AS_ERR_NCCL"}
+AS_DIST_ID_BYTES, AS_DIST_HANDLE_BYTES = 128, 256
+EXCHANGE = {"none": 0, "nccl": 1, "peer": 2}
 
 _vp, _i64, _i32, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
 _P = ctypes.POINTER
@@ -85,12 +88,25 @@ _sig("as_search", [_vp, _P(AsSearchCfg), _i32, _vp, _P(_vp), ctypes.c_char_p, _P
 _sig("as_random_graph", [_vp, ctypes.c_uint64, ctypes.c_char_p, _P(_sz)])
 _sig("as_dist_row_cuts", [_vp, _i32, _vp])
 _sig("as_matrix_col_span", [_vp, _vp, _vp])
+_ALLOC_T = ctypes.CFUNCTYPE(_vp, _sz, _vp, _vp)
+_FREE_T = ctypes.CFUNCTYPE(None, _vp, _vp, _vp)
+_sig("as_set_allocator", [_ALLOC_T, _FREE_T, _vp])
+_sig("as_dist_unique_id", [_vp])
+_sig("as_dist_init", [_i32, _i32, _vp, _i32, _P(_vp)])
+_sig("as_dist_set_cuts", [_vp, _vp])
+_sig("as_dist_ipc_handle", [_vp, _vp, _vp])
+_sig("as_dist_open_peers", [_vp, _vp, _vp])
+_sig("as_spmv_dist", [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp])
+_sig("as_dist_check", [_vp])
+_sig("as_dist_destroy", [_vp], None)
 
 EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create_csr", "as_matrix_create_mtx",
             "as_matrix_stats", "as_matrix_row_slice", "as_matrix_export_csr", "as_matrix_destroy", "as_graph_parse",
             "as_graph_print", "as_graph_destroy", "as_plan", "as_plan_ex", "as_plan_info", "as_plan_export",
             "as_plan_keys", "as_plan_destroy", "as_spmv", "as_spmv_host", "as_search", "as_random_graph",
-            "as_dist_row_cuts", "as_matrix_col_span"]
+            "as_dist_row_cuts", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
+            "as_dist_set_cuts", "as_dist_ipc_handle", "as_dist_open_peers", "as_spmv_dist", "as_dist_check",
+            "as_dist_destroy"]
 
 
 class AsError(RuntimeError):
@@ -317,3 +333,88 @@ def search(matrix: Matrix, device: int = 0, stream=None, seed: int = 1, max_cand
 
 def version() -> str:
     return _lib.as_version().decode()
+
+
+_hooks = None  # keeps the ctypes callbacks alive while installed
+
+
+def set_allocator(alloc=None, release=None):
+    """as_set_allocator with Python callables alloc(nbytes, stream) -> int pointer (0 = out of
+    memory) and release(ptr, stream); no arguments restores cudaMalloc/cudaFree."""
+    global _hooks
+    if alloc is None and release is None:
+        _ck(_lib.as_set_allocator(_ALLOC_T(), _FREE_T(), None))
+        _hooks = None
+        return
+
+    def _a(nbytes, stream, ctx):
+        try:
+            return alloc(nbytes, stream or 0) or None
+        except Exception:
+            return None
+
+    def _r(ptr, stream, ctx):
+        release(ptr, stream or 0)
+
+    hooks = (_ALLOC_T(_a), _FREE_T(_r))
+    _ck(_lib.as_set_allocator(hooks[0], hooks[1], None))
+    _hooks = hooks
+
+
+def use_torch_allocator():
+    """Route the library's device allocations through torch's caching allocator."""
+    import torch
+    set_allocator(lambda n, s: torch.cuda.caching_allocator_alloc(n, torch.cuda.current_device(), s),
+                  lambda p, s: torch.cuda.caching_allocator_delete(p))
+
+
+class Dist:
+    """e: ROW_DIV multi-GPU SpMV of one rank (as_dist_*): band plan -> y_full, then the
+    exchange ("none" | "nccl" AllGatherV | "peer" push over peer memory)."""
+
+    def __init__(self, rank: int, world: int, device: int, nccl_id: bytes | None = None):
+        h = _vp()
+        idb = ctypes.create_string_buffer(nccl_id, AS_DIST_ID_BYTES) if nccl_id is not None else None
+        _ck(_lib.as_dist_init(rank, world, idb, device, ctypes.byref(h)))
+        self._h = h
+        self.rank, self.world, self.device = rank, world, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        b = ctypes.create_string_buffer(AS_DIST_ID_BYTES)
+        _ck(_lib.as_dist_unique_id(b))
+        return b.raw
+
+    def set_cuts(self, cuts):
+        c = np.ascontiguousarray(cuts, np.int64)
+        if c.shape[0] != self.world + 1:
+            raise AsError(1, "cuts must have world+1 entries")
+        _ck(_lib.as_dist_set_cuts(self._h, c.ctypes.data))
+
+    def ipc_handle(self, y_full) -> bytes:
+        b = ctypes.create_string_buffer(AS_DIST_HANDLE_BYTES)
+        _ck(_lib.as_dist_ipc_handle(self._h, _ptr(y_full), b))
+        return b.raw
+
+    def open_peers(self, y_full, handles):
+        blob = b"".join(handles)
+        if len(blob) != AS_DIST_HANDLE_BYTES * self.world:
+            raise AsError(1, "one handle per rank expected")
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        _ck(_lib.as_dist_open_peers(self._h, _ptr(y_full), buf))
+
+    def spmv(self, plan: Plan, alpha, x_full, beta, y_full, exchange: str = "none", stream=None):
+        a, b = plan._scalars(alpha, beta)
+        _ck(_lib.as_spmv_dist(self._h, plan._h, ctypes.byref(a), _ptr(x_full), ctypes.byref(b), _ptr(y_full),
+                              EXCHANGE[exchange], _stream_handle(stream)))
+
+    def check(self):
+        _ck(_lib.as_dist_check(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib:
+            _lib.as_dist_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()

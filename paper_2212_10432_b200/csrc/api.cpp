@@ -17,24 +17,34 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
 
 namespace {
 thread_local std::string g_last_error;
+struct AllocHooks {
+  void* (*alloc)(size_t, void*, void*) = nullptr;
+  void (*release)(void*, void*, void*) = nullptr;
+  void* ctx = nullptr;
+} g_hooks;
 }
 void set_last_error(const std::string& m) { g_last_error = m; }
 
-template <class F>
-as_status_t guard(F f) {
-  try {
-    f();
-    return AS_OK;
-  } catch (const Error& e) {
-    set_last_error(e.msg);
-    return e.st;
-  } catch (const std::bad_alloc&) {
-    set_last_error("host out of memory");
-    return AS_ERR_OOM;
-  } catch (const std::exception& e) {
-    set_last_error(e.what());
-    return AS_ERR_INVALID_ARG;
+void* dev_alloc(size_t bytes, void* stream) {
+  void* d = nullptr;
+  if (g_hooks.alloc) {
+    d = g_hooks.alloc(bytes, stream, g_hooks.ctx);
+    if (!d) fail(AS_ERR_OOM, "allocator hook returned NULL for " + std::to_string(bytes) + " bytes");
+    return d;
   }
+  cudaError_t e = cudaMalloc(&d, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? AS_ERR_OOM : AS_ERR_CUDA,
+         "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  }
+  return d;
+}
+
+void dev_free(void* p, void* stream) {
+  if (!p) return;
+  if (g_hooks.release) g_hooks.release(p, stream, g_hooks.ctx);
+  else cudaFree(p);
 }
 
 as_status_t copy_string(const std::string& s, char* buf, size_t* len) {
@@ -72,6 +82,7 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
     P->canon = canon;
     P->host = build_plan(A, g);
     P->device = device;
+    P->stream = stream;
     if (device >= 0) {
       int cur = 0;
       check_cuda(cudaGetDevice(&cur), "cudaGetDevice");
@@ -123,6 +134,15 @@ using namespace as;
 extern "C" {
 
 const char* as_last_error(void) { return g_last_error.c_str(); }
+
+as_status_t as_set_allocator(void* (*alloc)(size_t, void*, void*), void (*release)(void*, void*, void*), void* ctx) {
+  return guard([&] {
+    if (!alloc != !release) fail(AS_ERR_INVALID_ARG, "alloc and release must both be set or both be NULL");
+    g_hooks.alloc = alloc;
+    g_hooks.release = release;
+    g_hooks.ctx = alloc ? ctx : nullptr;
+  });
+}
 const char* as_version(void) { return "alphasparse-b200 0.1 (sm_100a)"; }
 
 as_status_t as_matrix_create(int64_t m, int64_t n, int64_t nnz, const int64_t* row, const int64_t* col,
@@ -330,8 +350,8 @@ as_status_t as_spmv_host(as_plan_t h, const void* alpha, const void* x_host, con
     int cur = -1;
     cudaGetDevice(&cur);
     cudaSetDevice(P.device);
-    if (!P.d_x) check_cuda(cudaMalloc(&P.d_x, std::max<size_t>(16, P.n * sv)), "cudaMalloc x");
-    if (!P.d_y) check_cuda(cudaMalloc(&P.d_y, std::max<size_t>(16, P.m * sv)), "cudaMalloc y");
+    if (!P.d_x) P.d_x = dev_alloc(std::max<size_t>(16, P.n * sv), P.stream);
+    if (!P.d_y) P.d_y = dev_alloc(std::max<size_t>(16, P.m * sv), P.stream);
     cudaStream_t s = (cudaStream_t)stream;
     double b = P.dt == AS_R64F ? *(const double*)beta : (double)*(const float*)beta;
     check_cuda(cudaMemcpyAsync(P.d_x, x_host, P.n * sv, cudaMemcpyHostToDevice, s), "H2D x");

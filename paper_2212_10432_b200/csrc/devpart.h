@@ -106,4 +106,16 @@ int device_max_smem_optin(int device);
 int device_sm_count(int device);
 int xw_ctas_per_sm(int dtype, int pad, int vec, int tpb, size_t smem);
 
+// dist_kernels.cu: peer-memory exchange of as_spmv_dist (AS_EXCH_PEER)
+constexpr int kMaxPeers = 64;  // AS_DIST_MAX_WORLD
+struct PeerPush {
+  void* dst[kMaxPeers];                 // peer y_full + band offset (IPC mappings)
+  unsigned long long* flag[kMaxPeers];  // peer flag arrays (IPC mappings)
+  int n = 0;
+};
+int launch_push(const void* src, int64_t bytes, const PeerPush& pp, unsigned* ctr, unsigned* target,
+                unsigned long long epoch, int rank, void* stream);
+int launch_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch,
+                unsigned long long timeout_ns, int* status, void* stream);
+
 }  // namespace as

@@ -1,0 +1,97 @@
+// Peer-memory exchange of the ROW_DIV multi-GPU path (as_spmv_dist, AS_EXCH_PEER).
+//
+// After the band SpMV, ONE kernel streams this rank's y band into every peer's y_full over
+// NVLink (P2P stores into CUDA IPC mappings of the peers' buffers) and, once every CTA's
+// stores are fenced at system scope, the last CTA publishes the call's epoch into each
+// peer's flag array with a release store.  Each rank's stream then runs a one-CTA wait
+// kernel that acquires its peers' flags for that epoch (bounded by a timeout so a missing
+// peer cannot hang the GPU).  No NCCL on this path: one pass over the band instead of the
+// AllGatherV's rounds.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "devpart.h"
+
+namespace as {
+namespace {
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <class E>
+__global__ void __launch_bounds__(512) k_push(const E* __restrict__ src, int64_t cnt, PeerPush pp, unsigned* ctr,
+                                              unsigned target, unsigned long long epoch, int rank) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
+    const E v = src[i];
+#pragma unroll 4
+    for (int p = 0; p < pp.n; ++p) ((E*)pp.dst[p])[i] = v;
+  }
+  __threadfence_system();  // this thread's peer stores before the CTA's arrival
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(ctr, 1u);
+    if (prev + 1 == target) {  // last CTA of this call: every CTA's stores are fenced
+      __threadfence_system();
+      for (int p = 0; p < pp.n; ++p) st_release_sys(pp.flag[p] + rank, epoch);
+    }
+  }
+}
+
+__global__ void k_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch,
+                       unsigned long long timeout_ns, int* status) {
+  const int r = threadIdx.x;
+  if (r < world && r != rank) {
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(flags + r) < epoch) {
+      if (globaltimer() - t0 > timeout_ns) {
+        atomicExch(status, 1);
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+}
+
+}  // namespace
+
+int launch_push(const void* src, int64_t bytes, const PeerPush& pp, unsigned* ctr, unsigned* target,
+                unsigned long long epoch, int rank, void* stream) {
+  // widest element all addresses and the byte count are aligned to
+  uintptr_t a = (uintptr_t)src | (uintptr_t)bytes;
+  for (int p = 0; p < pp.n; ++p) a |= (uintptr_t)pp.dst[p];
+  const int esz = (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : 4;
+  const int64_t cnt = bytes / esz;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t g = std::max<int64_t>(1, std::min<int64_t>((cnt + 511) / 512, (int64_t)sms * 2));
+  *target += (unsigned)g;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (esz == 16) k_push<uint4><<<g, 512, 0, s>>>((const uint4*)src, cnt, pp, ctr, *target, epoch, rank);
+  else if (esz == 8) k_push<uint64_t><<<g, 512, 0, s>>>((const uint64_t*)src, cnt, pp, ctr, *target, epoch, rank);
+  else k_push<uint32_t><<<g, 512, 0, s>>>((const uint32_t*)src, cnt, pp, ctr, *target, epoch, rank);
+  return (int)cudaGetLastError();
+}
+
+int launch_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch,
+                unsigned long long timeout_ns, int* status, void* stream) {
+  const int t = (world + 31) / 32 * 32;
+  k_wait<<<1, t, 0, (cudaStream_t)stream>>>(flags, world, rank, epoch, timeout_ns, status);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace as

@@ -7,6 +7,8 @@
 #include <utility>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "../../include/as.h"
 #include "devpart.h"
 
@@ -20,6 +22,31 @@ struct Error : std::exception {
 };
 [[noreturn]] inline void fail(as_status_t s, const std::string& m) { throw Error(s, m); }
 void set_last_error(const std::string& m);
+void check_cuda(cudaError_t e, const char* what);
+
+// Runs f, converting exceptions to statuses (every C entry point).
+template <class F>
+inline as_status_t guard(F f) {
+  try {
+    f();
+    return AS_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host out of memory");
+    return AS_ERR_OOM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return AS_ERR_INVALID_ARG;
+  }
+}
+
+// Device memory of plans and scratch: cudaMalloc/cudaFree on the current device, or the
+// caller's hooks (as_set_allocator, e.g. torch's caching allocator).  dev_alloc throws
+// AS_ERR_OOM on failure.
+void* dev_alloc(size_t bytes, void* stream);
+void dev_free(void* p, void* stream);
 
 // ------------------------------------------------------------------ graph IR
 struct Value {

@@ -46,8 +46,7 @@ void* Plan::up(const void* h, size_t bytes, cudaStream_t s, size_t pad_to) {
   // +64 bytes of zeroed tail: aligned bulk copies (cp.async.bulk, 16-B granules) and vector
   // loads may read up to 3 elements past the end of an array
   size_t alloc = std::max<size_t>(std::max(bytes, pad_to), 16) + 64;
-  void* d = nullptr;
-  ck(cudaMalloc(&d, alloc), "cudaMalloc");
+  void* d = dev_alloc(alloc, s);
   allocs.push_back(d);
   dev_bytes += alloc;
   ck(cudaMemsetAsync((char*)d + bytes, 0, alloc - bytes, s), "cudaMemsetAsync");
@@ -225,9 +224,9 @@ Plan::~Plan() {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(device);
-    for (void* p : allocs) cudaFree(p);
-    if (d_x) cudaFree(d_x);
-    if (d_y) cudaFree(d_y);
+    for (void* p : allocs) dev_free(p, stream);
+    if (d_x) dev_free(d_x, stream);
+    if (d_y) dev_free(d_y, stream);
     cudaSetDevice(cur);
   }
 }

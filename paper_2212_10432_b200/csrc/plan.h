@@ -8,6 +8,7 @@ namespace as {
 
 struct Plan {
   int device = -1;
+  void* stream = nullptr;        // creation stream (allocator hooks free on it)
   as_dtype_t dt = AS_R64F;
   int64_t m = 0, n = 0, nnz_real = 0;
   HostPlan host;                 // logical metadata (kept for host-only plans / AS_PLAN_KEEP_HOST)

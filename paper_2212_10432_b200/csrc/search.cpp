@@ -295,8 +295,8 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       z ^= z << 17;
       v = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
     }
-    check_cuda(cudaMalloc(&dx, std::max<size_t>(16, A.n * sv)), "cudaMalloc x");
-    check_cuda(cudaMalloc(&dy, std::max<size_t>(16, A.m * sv)), "cudaMalloc y");
+    dx = dev_alloc(std::max<size_t>(16, A.n * sv), stream);
+    dy = dev_alloc(std::max<size_t>(16, A.m * sv), stream);
     if (sv == 8) {
       check_cuda(cudaMemcpy(dx, xd.data(), A.n * 8, cudaMemcpyHostToDevice), "H2D x");
     } else {
@@ -307,7 +307,7 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       int l2 = 0;
       cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
       flush_bytes = (size_t)std::max(l2, 1 << 20) * 2;
-      check_cuda(cudaMalloc(&flush, flush_bytes), "cudaMalloc flush");
+      flush = dev_alloc(flush_bytes, stream);
     }
   }
   cudaEvent_t e0, e1;
@@ -476,9 +476,9 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
   if (log) std::fclose(log);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  cudaFree(dx);
-  cudaFree(dy);
-  if (flush) cudaFree(flush);
+  dev_free(dx, stream);
+  dev_free(dy, stream);
+  dev_free(flush, stream);
   cudaSetDevice(cur);
   if (!best_plan) {
     set_last_error("as_search: no candidate could be planned");

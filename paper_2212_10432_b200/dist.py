@@ -7,7 +7,13 @@ The SpMV itself needs no communication when x is replicated; an exchange runs on
 next iterate needs y as its x (north_star).  All-gather: every rank receives all of y
 ((m - rows_r)*sv bytes).  Halo: rank r receives only the part of y inside its band's column
 span [lo_r, hi_r] that other ranks own (C5, band +-4096: 2*4096 rows per rank instead of
-the whole vector)."""
+the whole vector).
+
+The C-ABI path (as_dist_*, class Dist) runs the band SpMV and the exchange inside the library:
+"nccl" = AllGatherV as grouped ncclBroadcasts, "peer" = one push kernel storing the band
+into every peer's y_full over peer memory + release/acquire flags.  init_dist and
+register_peers below only carry the 128-byte NCCL id and the 256-byte IPC blobs over the
+torch process group."""
 from __future__ import annotations
 
 
@@ -77,3 +83,24 @@ def halo_exchange(y_local, x_full, cuts, moves, group=None):
         for req in dist.batch_isend_irecv(ops):
             req.wait()
     return x_full
+
+
+def init_dist(rank: int, world: int, device: int, cuts, nccl: bool = True, group=None):
+    """Dist of this rank: rank 0's ncclUniqueId is broadcast over the process group (nccl=False:
+    peer-memory mode only); the row cuts are installed."""
+    import torch.distributed as dist
+    from . import Dist
+    obj = [Dist.unique_id() if (nccl and rank == 0) else None]
+    if nccl and world > 1:
+        dist.broadcast_object_list(obj, src=0, group=group)
+    d = Dist(rank, world, device, obj[0] if nccl else None)
+    d.set_cuts(cuts)
+    return d
+
+
+def register_peers(d, y_full, group=None):
+    """All-gather the IPC blobs of every rank's y_full and map the peers' buffers (collective)."""
+    import torch.distributed as dist
+    handles = [None] * d.world
+    dist.all_gather_object(handles, d.ipc_handle(y_full), group=group)
+    d.open_peers(y_full, handles)

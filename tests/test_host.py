@@ -257,3 +257,39 @@ def test_fp32_plan_values():
     P = asp.Plan(_mat(coo), "COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED", device=-1)
     assert P.export("p0.val").dtype == np.float32
     assert compare_export(P, coo, "COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED", np.float32)
+
+
+def test_dist_host_validation():
+    """as_dist_* host logic without a GPU: rank/world ranges, cut validation, NCCL id needs a
+    device, spmv before cuts; as_set_allocator rejects half-installed hooks."""
+    with pytest.raises(asp.AsError) as e:
+        asp.Dist(2, 2, -1)
+    assert e.value.status == "AS_ERR_INVALID_ARG"
+    with pytest.raises(asp.AsError):
+        asp.Dist(0, asp.AS_DIST_HANDLE_BYTES, -1)  # world > AS_DIST_MAX_WORLD
+    d = asp.Dist(1, 3, -1)
+    d.set_cuts([0, 4, 4, 9])                      # an empty band is legal (A35)
+    for bad in ([1, 4, 6, 9], [0, 5, 4, 9]):
+        with pytest.raises(asp.AsError) as e:
+            d.set_cuts(bad)
+        assert e.value.status == "AS_ERR_INVALID_ARG"
+    with pytest.raises(asp.AsError) as e:
+        asp.Dist(0, 2, -1, b"\0" * asp.AS_DIST_ID_BYTES)
+    assert e.value.status == "AS_ERR_INVALID_ARG"
+    with pytest.raises(asp.AsError):
+        d.ipc_handle(1 << 20)                     # host-only dist
+    d.close()
+    import ctypes
+    with pytest.raises(asp.AsError):
+        asp._ck(asp._lib.as_set_allocator(asp._ALLOC_T(lambda n, s, c: None), asp._FREE_T(), None))
+    asp.set_allocator()                           # restore defaults: OK
+
+
+def test_dist_unique_id():
+    """ncclGetUniqueId through the runtime-loaded NCCL (no device needed)."""
+    try:
+        a = asp.Dist.unique_id()
+    except asp.AsError as e:
+        assert e.status == "AS_ERR_NCCL"
+        pytest.skip("NCCL not loadable here")
+    assert len(a) == asp.AS_DIST_ID_BYTES and a != asp.Dist.unique_id()
