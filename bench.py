@@ -183,6 +183,11 @@ def cpu_baseline(coo, wl, budget_s=10.0):
             "sample": f"{n} full passes over {wl} ({coo.nnz} nnz), long double, {cores} threads, {t_tot:.1f} s"}
 
 
+def cdev():
+    """Device of control-plane tensors: cuda under nccl, cpu under gloo."""
+    return "cpu" if os.environ.get("AS_BENCH_BACKEND") == "gloo" else "cuda"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -200,6 +205,9 @@ def main():
                          "over torch.distributed; nccl/peer = as_spmv_dist (C-ABI: SpMV + AllGatherV, or "
                          "SpMV + peer-memory push), timed as whole steps")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no search/baseline/e2e)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1 on c2: weak = the Laplacian grows to 2048 x 2048N and each rank owns one "
+                         "2048 x 2048 ROW_DIV band (per-GPU work fixed); strong = C2 itself cut into N bands")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile else args.warmup
 
@@ -207,8 +215,16 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
-    coo, wl, seeds = load_config(args.config)
-    coo = to_csr(coo)
+    weak = world > 1 and args.config == "c2" and args.scaling == "weak"
+    if weak:
+        # weak scaling of the ROW_DIV path: global grid 2048 x 2048*world, rank r generates
+        # only its band (grid rows [2048r, 2048(r+1)), global columns)
+        g = 2048
+        coo = synth.c2_lap2d_band(g, g * world, g * rank, g * (rank + 1))
+        wl, seeds = f"lap2d-{g}x{g * world}", C2_SEEDS
+    else:
+        coo, wl, seeds = load_config(args.config)
+        coo = to_csr(coo)
     if args.impl == "reference":
         if rank == 0:
             reference_arm(args, coo, wl)
@@ -217,16 +233,29 @@ def main():
     import torch
     import paper_2212_10432_b200 as asp
 
+    if os.environ.get("AS_BENCH_BACKEND") == "gloo":
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # AS_BENCH_BACKEND=gloo: control plane over gloo so that N ranks can share one GPU
+        # (single-GPU validation of the N > 1 code path; the exchange kinds need nccl)
+        if os.environ.get("AS_BENCH_BACKEND") == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    A_full = asp.Matrix.from_csr(coo.m, coo.n, coo.row_ptr, coo.col, coo.val)
-    cuts = A_full.row_cuts(world)
+    if weak:
+        A = asp.Matrix.from_csr(coo.m, coo.n, coo.row_ptr, coo.col, coo.val)
+        cuts = np.arange(world + 1, dtype=np.int64) * coo.m
+        m_global = coo.m * world
+    else:
+        A_full = asp.Matrix.from_csr(coo.m, coo.n, coo.row_ptr, coo.col, coo.val)
+        cuts = A_full.row_cuts(world)
+        m_global = coo.m
     r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
-    A = A_full if world == 1 else A_full.row_slice(r0, r1)
+    A = A if weak else (A_full if world == 1 else A_full.row_slice(r0, r1))
     nnz_local = A.nnz
     stream = torch.cuda.current_stream()
 
@@ -284,7 +313,7 @@ def main():
             # as_spmv_dist: band SpMV into y_full + the exchange inside the library
             from paper_2212_10432_b200 import dist as D
             d = D.init_dist(rank, world, local, cuts, nccl=args.exchange == "nccl")
-            y_full = torch.zeros(coo.m, dtype=dy.dtype, device="cuda")
+            y_full = torch.zeros(m_global, dtype=dy.dtype, device="cuda")
             if args.exchange == "peer":
                 D.register_peers(d, y_full)
             for _ in range(3):
@@ -308,7 +337,7 @@ def main():
             # y -> next x: all-gather (uneven bands, NCCL broadcasts) or halo (P2P of the
             # band's column span only, NEXT-1), timed separately from the SpMV
             from paper_2212_10432_b200 import dist as D
-            x_next = torch.zeros(coo.m, dtype=dy.dtype, device="cuda")
+            x_next = torch.zeros(m_global, dtype=dy.dtype, device="cuda")
             moves = D.halo_plan(D.gather_spans(A.col_span()), cuts) if args.exchange == "halo" else None
             dist.barrier()
             g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -321,16 +350,16 @@ def main():
             torch.cuda.synchronize()
             gather_ms = g0.elapsed_time(g1)
     if gather_ms is not None:
-        gm = torch.tensor([gather_ms], device="cuda", dtype=torch.float64)
+        gm = torch.tensor([gather_ms], device=cdev(), dtype=torch.float64)
         dist.all_reduce(gm, op=dist.ReduceOp.MAX)
         gather_ms = float(gm.item())
     ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     t_ms = statistics.mean(ms)
     if dist:
-        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
+        tt = torch.tensor([t_ms], device=cdev(), dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
-        tot = torch.tensor([float(nnz_local)], device="cuda", dtype=torch.float64)
+        tot = torch.tensor([float(nnz_local)], device=cdev(), dtype=torch.float64)
         dist.all_reduce(tot)
         nnz_total = int(tot.item())
     else:
@@ -360,7 +389,7 @@ def main():
             e2e_ms.append(e0.elapsed_time(e1))
         tm = statistics.mean(e2e_ms)
         if dist:
-            tt = torch.tensor([tm], device="cuda", dtype=torch.float64)
+            tt = torch.tensor([tm], device=cdev(), dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             tm = float(tt.item())
         sv = dx.element_size()
@@ -382,9 +411,10 @@ def main():
             pass
     line = {
         "metric": METRIC, "value": gflops, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
+        "scaling": "weak" if (weak or world == 1) and args.config == "c2" and args.scaling == "weak" else "strong",
         "vs_baseline": None, "dtype": "f64" if dt == np.float64 else "f32", "data": "synthetic",
-        "config": {"workload": wl, "rows": coo.m, "nnz": coo.nnz, "graph": graph, "searched": searched,
+        "config": {"workload": wl, "rows": m_global, "nnz": nnz_total, "graph": graph, "searched": searched,
                    "alpha": 1.0, "beta": 0.0, "l2": "flushed before every step" if not args.no_flush else "not flushed",
                    "parallelism": f"row_div{world}", "plan_and_search_s": round(plan_s, 2),
                    "kernels": info["kernels"], "bytes_model": info["bytes_model"], "bytes_floor": info["bytes_floor"]},

@@ -163,6 +163,26 @@ def c2_lap2d(grid: int = 2048, dtype=np.float64) -> Coo:
     return Coo(m, m, row[order], col[order], val[order].astype(dtype), f"lap2d-{grid}")
 
 
+def c2_lap2d_band(grid: int, ny: int, gy0: int, gy1: int, dtype=np.float64) -> "Csr":
+    """Rows of the 5-point stencil on a grid x ny grid (row i = gx + grid*gy) whose grid row
+    gy lies in [gy0, gy1), with GLOBAL column indices (n = grid*ny).  The ROW_DIV band of
+    rank r in the weak-scaled C2 (ny = grid*P, band = grid rows [grid*r, grid*(r+1))).
+    c2_lap2d_band(g, g, 0, g) has exactly the rows of c2_lap2d(g)."""
+    r0, r1 = gy0 * grid, gy1 * grid
+    i = np.arange(r0, r1, dtype=np.int64)
+    gx, gy = i % grid, i // grid
+    # per row, the 5 candidate columns in ascending order with their presence mask
+    cand = np.stack([i - grid, i - 1, i, i + 1, i + grid], axis=1)
+    ok = np.stack([gy > 0, gx > 0, np.ones_like(gx, bool), gx < grid - 1, gy < ny - 1], axis=1)
+    vals = np.array([-1.0, -1.0, 4.0, -1.0, -1.0])
+    rl = ok.sum(axis=1)
+    rp = np.zeros(r1 - r0 + 1, np.int64)
+    np.cumsum(rl, out=rp[1:])
+    col = cand[ok].astype(np.int32)
+    val = np.broadcast_to(vals, cand.shape)[ok].astype(dtype)
+    return Csr(r1 - r0, grid * ny, rp, col, val, f"lap2d-{grid}x{ny}-band{gy0}")
+
+
 # ----------------------------------------------------------------------------------
 # C3 rmat
 # ----------------------------------------------------------------------------------
