@@ -183,6 +183,9 @@ def cpu_baseline(coo, wl, budget_s=10.0):
             "sample": f"{n} full passes over {wl} ({coo.nnz} nnz), long double, {cores} threads, {t_tot:.1f} s"}
 
 
+E2E_BANDS = 8  # ROW_DIV bands of the pipelined e2e plan
+
+
 def cdev():
     """Device of control-plane tensors: cuda under nccl, cpu under gloo."""
     return "cpu" if os.environ.get("AS_BENCH_BACKEND") == "gloo" else "cuda"
@@ -369,32 +372,48 @@ def main():
     achieved_gbs = info["bytes_model"] / (t_ms * 1e-3) / 1e9
     launches = int(info["n_launches"])
 
-    # e2e through the C-ABI with host buffers (pinned), copies inside the timed region
+    # e2e through the C-ABI with host buffers (pinned), copies inside the timed region.  Two
+    # plans: the searched one (copies, kernels, copies back to back) and the same graph under
+    # ROW_DIV into E2E_BANDS bands, which as_spmv_host pipelines (chunked H2D of x and D2H of
+    # y on copy streams overlapping the band kernels); the faster is reported.
     e2e = None
     if not args.profile:
         xh = torch.from_numpy(x).pin_memory()
         yh = torch.zeros(m_local, dtype=dy.dtype).pin_memory()
         xn, yn = xh.numpy(), yh.numpy()
-        for _ in range(2):
-            P.spmv_host(1.0, xn, 0.0, yn, stream)
-        e2e_ms = []
-        for _ in range(max(3, args.steps // 3)):
-            if not args.no_flush:
-                flush_l2()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            P.spmv_host(1.0, xn, 0.0, yn, stream)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            e2e_ms.append(e0.elapsed_time(e1))
-        tm = statistics.mean(e2e_ms)
+        cands = [(graph, P)]
+        if "ROW_DIV" not in graph and m_local >= 8 * E2E_BANDS:
+            cut = ",".join(str(m_local * i // E2E_BANDS) for i in range(1, E2E_BANDS))
+            g_pipe = f"ROW_DIV(cuts=[{cut}]) {{ {graph} }}"
+            try:
+                cands.append((g_pipe, asp.Plan(A, g_pipe, device=local)))
+            except asp.AsError:
+                pass
+        res = []
+        for g_e, P_e in cands:
+            for _ in range(2):
+                P_e.spmv_host(1.0, xn, 0.0, yn, stream)
+            e2e_ms = []
+            for _ in range(max(3, args.steps // 3)):
+                if not args.no_flush:
+                    flush_l2()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                P_e.spmv_host(1.0, xn, 0.0, yn, stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                e2e_ms.append(e0.elapsed_time(e1))
+            res.append((statistics.mean(e2e_ms), g_e, int(P_e.info()["n_launches"])))
+        tm, g_e, l_e = min(res)
         if dist:
             tt = torch.tensor([tm], device=cdev(), dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             tm = float(tt.item())
         sv = dx.element_size()
         e2e = {"value": 2.0 * nnz_total / (tm * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": tm,
-               "h2d_bytes_per_step": int(coo.n * sv), "d2h_bytes_per_step": int(m_local * sv)}
+               "h2d_bytes_per_step": int(coo.n * sv), "d2h_bytes_per_step": int(m_local * sv),
+               "graph": g_e, "launches_per_step": l_e,
+               "candidates_ms": {("pipelined" if i else "searched"): r[0] for i, r in enumerate(res)}}
 
     if rank != 0:
         if dist:

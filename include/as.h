@@ -134,8 +134,14 @@ void as_plan_destroy(as_plan_t);
  * device faults surface as AS_ERR_CUDA at a later call. */
 as_status_t as_spmv(as_plan_t, const void* alpha, const void* x, const void* beta, void* y,
                     void* stream);
-/* Same with HOST x[n] / y[m] (pinned or pageable): copies x (and y when beta != 0) to the
- * plan's device scratch, runs as_spmv, copies y back; synchronous. */
+/* Same with HOST x[n] / y[m] (pinned for overlap; pageable works): copies x (and y when
+ * beta != 0) to the plan's device scratch, runs as_spmv, copies y back; synchronous.
+ * Plans with several launches (e.g. ROW_DIV bands) are pipelined: x goes up in
+ * column chunks on a plan-owned copy stream, launch i waits only for the chunk holding the
+ * last column it reads, and each y row range no later launch writes goes down on a second
+ * copy stream once its last writer is done (PCIe is full duplex).  Not pipelined: a single
+ * launch, fp32 plans with heavy rows, or AS_HOST_NOPIPE set in the environment.  The
+ * result is identical either way (same kernels, same order on the device). */
 as_status_t as_spmv_host(as_plan_t, const void* alpha, const void* x_host, const void* beta,
                          void* y_host, void* stream);
 

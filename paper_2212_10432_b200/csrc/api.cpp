@@ -127,6 +127,34 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
   }
 }
 
+// The launch sequence of one as_spmv call: beta pre-pass, fp32 heavy-row scratch reset, the
+// parts in writer-rule order, the heavy-row epilogue.  before(i) runs on the host before
+// launch i is enqueued, after(i) after it (as_spmv_host hooks its copy pipeline there).
+template <class Before, class After>
+int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s, Before before, After after) {
+  const size_t sv = P.dt == AS_R64F ? 8 : 4;
+  int err = 0;
+  if (P.n_prepass) {
+    // beta == 0: y is write-only, so zeroing all of y is as correct as zeroing the listed
+    // rows; a plain fill beats the indexed pre-pass once the list covers most rows
+    if (b == 0.0 && (double)P.m * sv <= 1.5 * (double)P.n_prepass * (4 + sv))
+      err = (int)cudaMemsetAsync(y, 0, (size_t)P.m * sv, s);
+    else
+      err = launch_prepass(P.d_prepass, P.n_prepass, b, y, P.dt == AS_R64F ? 1 : 0, s);
+  }
+  if (P.n_heavy && !err) err = (int)cudaMemsetAsync(P.d_heavy_acc, 0, (size_t)P.n_heavy * 8, s);
+  for (size_t i = 0; i < P.launches.size() && !err; ++i) {
+    before(i);
+    DevPart d = P.launches[i];
+    d.alpha = a;
+    d.beta = b;
+    err = launch_part(d, x, y, s);
+    if (!err) after(i);
+  }
+  if (P.n_heavy && !err) err = launch_heavy_epilogue(P.d_heavy_rows, P.d_heavy_acc, P.n_heavy, y, s);
+  return err;
+}
+
 }  // namespace as
 
 using namespace as;
@@ -300,6 +328,7 @@ as_status_t as_plan_keys(as_plan_t P, char* buf, size_t* len) {
 
 void as_plan_destroy(as_plan_t P) { delete P; }
 
+
 as_status_t as_spmv(as_plan_t h, const void* alpha, const void* x, const void* beta, void* y, void* stream) {
   return guard([&] {
     if (!h || !alpha || !beta) fail(AS_ERR_INVALID_ARG, "NULL argument");
@@ -317,35 +346,25 @@ as_status_t as_spmv(as_plan_t h, const void* alpha, const void* x, const void* b
     int cur = -1;
     cudaGetDevice(&cur);
     if (cur != P.device) cudaSetDevice(P.device);
-    int err = 0;
-    if (P.n_prepass) {
-      // beta == 0: y is write-only, so zeroing all of y is as correct as zeroing the listed
-      // rows; a plain fill beats the indexed pre-pass once the list covers most rows
-      if (b == 0.0 && (double)P.m * sv <= 1.5 * (double)P.n_prepass * (4 + sv))
-        err = (int)cudaMemsetAsync(y, 0, (size_t)P.m * sv, (cudaStream_t)stream);
-      else
-        err = launch_prepass(P.d_prepass, P.n_prepass, b, y, P.dt == AS_R64F ? 1 : 0, stream);
-    }
-    if (P.n_heavy && !err)
-      err = (int)cudaMemsetAsync(P.d_heavy_acc, 0, (size_t)P.n_heavy * 8, (cudaStream_t)stream);
-    for (size_t i = 0; i < P.launches.size() && !err; ++i) {
-      DevPart d = P.launches[i];
-      d.alpha = a;
-      d.beta = b;
-      err = launch_part(d, x, y, stream);
-    }
-    if (P.n_heavy && !err) err = launch_heavy_epilogue(P.d_heavy_rows, P.d_heavy_acc, P.n_heavy, y, stream);
+    int err = run_plan(P, x, y, a, b, (cudaStream_t)stream, [](size_t) {}, [](size_t) {});
     if (cur != P.device) cudaSetDevice(cur);
     if (err) fail(AS_ERR_CUDA, std::string("launch: ") + cudaGetErrorString((cudaError_t)err));
   });
 }
 
+// Host-buffer SpMV.  With several launches whose spans allow it (e.g. a ROW_DIV graph), the
+// copies are pipelined against the kernels: x goes up in chunks on a copy stream (chunk
+// boundaries = the running maximum of the launches' last column), launch i waits only for
+// the chunk holding its last column, and every y row range no later launch writes goes down
+// on a second copy stream as soon as the launch that finishes it is done -- PCIe is full
+// duplex, so H2D of x, the kernels and D2H of y overlap instead of running back to back.
 as_status_t as_spmv_host(as_plan_t h, const void* alpha, const void* x_host, const void* beta, void* y_host,
                          void* stream) {
   return guard([&] {
     if (!h || !alpha || !beta) fail(AS_ERR_INVALID_ARG, "NULL argument");
     Plan& P = *h->P;
     if (P.device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan");
+    if ((P.n > 0 && !x_host) || (P.m > 0 && !y_host)) fail(AS_ERR_INVALID_ARG, "NULL x or y");
     const size_t sv = P.dt == AS_R64F ? 8 : 4;
     int cur = -1;
     cudaGetDevice(&cur);
@@ -353,14 +372,95 @@ as_status_t as_spmv_host(as_plan_t h, const void* alpha, const void* x_host, con
     if (!P.d_x) P.d_x = dev_alloc(std::max<size_t>(16, P.n * sv), P.stream);
     if (!P.d_y) P.d_y = dev_alloc(std::max<size_t>(16, P.m * sv), P.stream);
     cudaStream_t s = (cudaStream_t)stream;
+    double a = P.dt == AS_R64F ? *(const double*)alpha : (double)*(const float*)alpha;
     double b = P.dt == AS_R64F ? *(const double*)beta : (double)*(const float*)beta;
-    check_cuda(cudaMemcpyAsync(P.d_x, x_host, P.n * sv, cudaMemcpyHostToDevice, s), "H2D x");
-    if (b != 0.0) check_cuda(cudaMemcpyAsync(P.d_y, y_host, P.m * sv, cudaMemcpyHostToDevice, s), "H2D y");
-    cudaSetDevice(cur);
-    as_status_t st = as_spmv(h, alpha, P.d_x, beta, P.d_y, stream);
-    if (st != AS_OK) fail(st, g_last_error);
-    cudaSetDevice(P.device);
-    check_cuda(cudaMemcpyAsync(y_host, P.d_y, P.m * sv, cudaMemcpyDeviceToHost, s), "D2H y");
+    cudaError_t prior = cudaGetLastError();
+    if (prior != cudaSuccess) fail(AS_ERR_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(prior));
+    const size_t L = P.launches.size();
+    const bool pipe = L >= 2 && !P.n_heavy && P.spans.size() == L && !std::getenv("AS_HOST_NOPIPE");
+    char* dx = (char*)P.d_x;
+    char* dy = (char*)P.d_y;
+    int err = 0;
+    if (!pipe) {
+      check_cuda(cudaMemcpyAsync(dx, x_host, P.n * sv, cudaMemcpyHostToDevice, s), "H2D x");
+      if (b != 0.0) check_cuda(cudaMemcpyAsync(dy, y_host, P.m * sv, cudaMemcpyHostToDevice, s), "H2D y");
+      err = run_plan(P, dx, dy, a, b, s, [](size_t) {}, [](size_t) {});
+      if (!err) err = (int)cudaMemcpyAsync(y_host, dy, P.m * sv, cudaMemcpyDeviceToHost, s);
+    } else {
+      if (!P.s_h2d) {
+        check_cuda(cudaStreamCreateWithFlags(&P.s_h2d, cudaStreamNonBlocking), "copy stream");
+        check_cuda(cudaStreamCreateWithFlags(&P.s_d2h, cudaStreamNonBlocking), "copy stream");
+      }
+      size_t ev = 0;
+      auto fork = [&](cudaStream_t from, cudaStream_t to) {  // `to` waits for work so far on `from`
+        cudaEvent_t e = P.host_event(ev++);
+        check_cuda(cudaEventRecord(e, from), "event");
+        check_cuda(cudaStreamWaitEvent(to, e, 0), "wait");
+        return e;
+      };
+      // the copy streams start after everything already queued on s (earlier users of d_x/d_y)
+      fork(s, P.s_h2d);
+      fork(s, P.s_d2h);
+      if (b != 0.0) {
+        check_cuda(cudaMemcpyAsync(dy, y_host, P.m * sv, cudaMemcpyHostToDevice, P.s_h2d), "H2D y");
+        fork(P.s_h2d, s);
+      }
+      // x prefix each launch needs (running max of chi + 1) and the chunk events
+      std::vector<int64_t> need(L);
+      int64_t run = 0;
+      for (size_t i = 0; i < L; ++i) {
+        run = std::max(run, std::min<int64_t>(P.spans[i].chi + 1, P.n));
+        need[i] = run;
+      }
+      int64_t sent = 0;
+      std::vector<std::pair<int64_t, cudaEvent_t>> chunks;  // (end column, event)
+      for (size_t i = 0; i < L; ++i) {
+        int64_t e = i + 1 == L ? P.n : need[i];
+        if (e > sent) {
+          check_cuda(cudaMemcpyAsync(dx + sent * sv, (const char*)x_host + sent * sv, (e - sent) * sv,
+                                     cudaMemcpyHostToDevice, P.s_h2d), "H2D x chunk");
+          cudaEvent_t ce = P.host_event(ev++);
+          check_cuda(cudaEventRecord(ce, P.s_h2d), "event");
+          chunks.push_back({e, ce});
+          sent = e;
+        }
+      }
+      // rows final after launch i: below the lowest row any later launch writes
+      std::vector<int64_t> fin(L);
+      int64_t lo = P.m;
+      for (size_t i = L; i-- > 0;) {
+        fin[i] = lo;
+        if (P.spans[i].rlo <= P.spans[i].rhi) lo = std::min(lo, P.spans[i].rlo);
+      }
+      int64_t done = 0;
+      size_t ci = 0;
+      err = run_plan(
+          P, dx, dy, a, b, s,
+          [&](size_t i) {
+            while (ci < chunks.size() && chunks[ci].first < need[i]) ++ci;
+            if (need[i] > 0 && ci < chunks.size()) check_cuda(cudaStreamWaitEvent(s, chunks[ci].second, 0), "wait");
+          },
+          [&](size_t i) {
+            int64_t f = i + 1 == L ? P.m : fin[i];
+            if (f > done && (f - done) * (int64_t)sv >= (1 << 20)) {  // >= 1 MB per D2H chunk
+              fork(s, P.s_d2h);
+              check_cuda(cudaMemcpyAsync((char*)y_host + done * sv, dy + done * sv, (f - done) * sv,
+                                         cudaMemcpyDeviceToHost, P.s_d2h), "D2H y chunk");
+              done = f;
+            }
+          });
+      if (!err && done < P.m) {
+        fork(s, P.s_d2h);
+        check_cuda(cudaMemcpyAsync((char*)y_host + done * sv, dy + done * sv, (P.m - done) * sv,
+                                   cudaMemcpyDeviceToHost, P.s_d2h), "D2H y tail");
+      }
+      fork(P.s_d2h, s);
+      fork(P.s_h2d, s);
+    }
+    if (err) {
+      cudaSetDevice(cur);
+      fail(AS_ERR_CUDA, std::string("launch: ") + cudaGetErrorString((cudaError_t)err));
+    }
     check_cuda(cudaStreamSynchronize(s), "sync");
     cudaSetDevice(cur);
   });

@@ -487,6 +487,113 @@ __global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restr
     nnz_thread_bmt<V, PAD, VEC, KB>(p, XGlobal<V>{x}, y, t);
 }
 
+// -------------------------------------------------------------------------------------
+// k_nnz_thread, predicated-emit form (plans without fp32 heavy rows).  The per-element
+// head test of the form above branches around a writer call, and the 32 lanes of a warp
+// hit their heads at different elements, so ncu saw 12 of 32 threads active on average
+// (C5: 1.35 warp instructions per nonzero).  Here the loop body is branch-free: rows that
+// close inside the BMT (the only ones a head can close, apart from the BMT's first
+// segment) are written by one predicated store; the straddling first segment is kept in
+// a register and, with the open last segment, written after the loop (atomically when
+// it straddles, A22) -- the same writes as THREAD_BITMAP_RED_G above, in the same order
+// per row.
+//   EM 0: STORE mode, beta == 0, affine origin_rows (y[base + r] = alpha * s)
+//   EM 1: any mode / beta / origin_rows
+// -------------------------------------------------------------------------------------
+template <class V, int EM>
+__device__ __forceinline__ void emit_excl(const DevPart& p, V* y, bool pred, int64_t r, double s) {
+  if constexpr (EM == 0) {
+    if (pred) y[p.origin_base + r] = (V)(p.alpha * s);
+  } else {
+    if (pred) {
+      const int64_t g = out_row(p, r);
+      double v = p.alpha * s;
+      if (p.mode == 1) v += (double)y[g];
+      else if (p.beta != 0.0) v += p.beta * (double)y[g];
+      y[g] = (V)v;
+    }
+  }
+}
+
+template <class V, bool PAD, int VEC, int KB, int EM, bool FULL, class XA>
+__device__ __forceinline__ void bmt_batch_pe(const DevPart& p, V* y, XA xa, const uint32_t* bm, const V* pv,
+                                             const int32_t* pc, int64_t stride, int j0, int len, int64_t& row,
+                                             double& acc, bool& inside, double& first) {
+  double v[KB];
+  int32_t c[KB];
+  if constexpr (PAD) {
+#pragma unroll
+    for (int q = 0; q < KB; q += VEC) {
+      if (FULL || j0 + q < len) {
+        PadLoad<V, VEC>::ld(pv + ((j0 + q) / VEC) * stride, pc + ((j0 + q) / VEC) * stride, v + q, c + q);
+      } else {
+#pragma unroll
+        for (int r = 0; r < VEC; ++r) {
+          v[q + r] = 0.0;
+          c[q + r] = 0;
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      if (FULL || j0 + q < len) {
+        v[q] = (double)ld_seq(pv + j0 + q);
+        c[q] = ld_seq(pc + j0 + q);
+      } else {
+        v[q] = 0.0;
+        c[q] = 0;
+      }
+    }
+  }
+  double xv[KB];
+#pragma unroll
+  for (int q = 0; q < KB; ++q) xv[q] = (FULL || j0 + q < len) ? xa(c[q]) : 0.0;
+  const uint32_t wd = (ldm(bm + (j0 >> 5)) >> (j0 & 31)) & ~(uint32_t)(j0 == 0);
+#pragma unroll
+  for (int q = 0; q < KB; ++q) {
+    const bool h = (FULL || j0 + q < len) && ((wd >> q) & 1u);
+    emit_excl<V, EM>(p, y, h && inside, row, acc);
+    first = (h && !inside) ? acc : first;
+    row += h ? 1 : 0;
+    inside = inside || h;
+    acc = (h ? 0.0 : acc) + v[q] * xv[q];
+  }
+}
+
+template <class V, bool PAD, int VEC, int KB, int EM>
+__global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  static_assert(32 % KB == 0 && KB % VEC == 0, "KB divides 32 and is a multiple of VEC");
+  const XGlobal<V> xa{x};
+  for (int64_t t = thread_units(p.n_bmt).begin, t_e = thread_units(p.n_bmt).end; t < t_e; t += blockDim.x) {
+    const int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
+    const int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
+    const int len = (int)(e - a);
+    const int64_t row0 = ldm(p.bmt_first_row + t);
+    const uint32_t* bm = p.bitmap + t * p.bm_words;
+    PadPos pp{0, 0};
+    if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
+    const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;
+    const int32_t* pc = PAD ? p.pad_col + pp.base : p.col + a;
+    const bool start_inside = ldm(bm) & 1u;
+    bool inside = start_inside;
+    int64_t row = row0;
+    double acc = 0.0, first = 0.0;
+    const int full = len & ~(KB - 1);
+    int j0 = 0;
+    for (; j0 < full; j0 += KB)
+      bmt_batch_pe<V, PAD, VEC, KB, EM, true>(p, y, xa, bm, pv, pc, pp.stride, j0, len, row, acc, inside, first);
+    if (j0 < len)
+      bmt_batch_pe<V, PAD, VEC, KB, EM, false>(p, y, xa, bm, pv, pc, pp.stride, j0, len, row, acc, inside, first);
+    // first segment closed inside the BMT but begun before it: straddler
+    if (!start_inside && inside) write_atom(p, y, row0, first);
+    // open last segment: exclusive iff it began at a head here and the next BMT starts a row
+    const bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
+    if (inside && ends) write_excl(p, y, row, acc);
+    else write_atom(p, y, row, acc);
+  }
+}
+
 // =====================================================================================
 // k_nnz_thread, x-window form (banded matrices): persistent CTAs own contiguous BMT ranges
 // processed in rounds of blockDim BMTs; round i of CTA c needs x[lo, hi] (computed at plan
@@ -1252,7 +1359,17 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       const int tt = tpb;
       // batches of KB loads per thread: 8 for fp64, 4 for fp32 (A/B on c5s fp64: KB 4 633 vs
       // KB 8 646 GF/s; c3s fp32: 408 vs 394; KB 16 or 80 registers slower everywhere)
-#define AS_NT(PADV, VECV) k_nnz_thread<V, PADV, VECV, (sizeof(V) == 4 && VECV <= 4 ? 4 : 8)><<<g, tt, 0, s>>>(p, x, y);
+      // predicated-emit form unless fp32 heavy rows need the scratch path (or the legacy
+      // form is forced for A/B timing: variant 9)
+      const bool pe = p.variant != 9 && !(sizeof(V) == 4 && p.n_heavy);
+      const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin;
+#define AS_NT(PADV, VECV)                                                                                 \
+  {                                                                                                       \
+    constexpr int KBV = sizeof(V) == 4 && VECV <= 4 ? 4 : 8;                                              \
+    if (!pe) k_nnz_thread<V, PADV, VECV, KBV><<<g, tt, 0, s>>>(p, x, y);                                  \
+    else if (em0) k_nnz_thread_pe<V, PADV, VECV, KBV, 0><<<g, tt, 0, s>>>(p, x, y);                       \
+    else k_nnz_thread_pe<V, PADV, VECV, KBV, 1><<<g, tt, 0, s>>>(p, x, y);                                \
+  }
       if (!p.pad) {
         AS_NT(false, 1)
       } else if (p.vec == 1) {

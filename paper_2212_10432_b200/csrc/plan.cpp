@@ -227,8 +227,52 @@ Plan::~Plan() {
     for (void* p : allocs) dev_free(p, stream);
     if (d_x) dev_free(d_x, stream);
     if (d_y) dev_free(d_y, stream);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
     cudaSetDevice(cur);
   }
+}
+
+cudaEvent_t Plan::host_event(size_t i) {
+  while (evs.size() <= i) {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    evs.push_back(e);
+  }
+  return evs[i];
+}
+
+// Superset of the x columns a part reads and of the global y rows it writes.
+static Plan::Span part_span(const HostPart& h, int64_t n) {
+  Plan::Span sp{INT64_MAX, -1, INT64_MAX, -1};
+  auto rows = [&](int64_t a, int64_t b) {  // [a, b]
+    sp.rlo = std::min(sp.rlo, a);
+    sp.rhi = std::max(sp.rhi, b);
+  };
+  auto cols = [&](int64_t a, int64_t b) {
+    sp.clo = std::min(sp.clo, std::max<int64_t>(a, 0));
+    sp.chi = std::max(sp.chi, std::min<int64_t>(b, n - 1));
+  };
+  if (h.kind == "dia") {
+    if (h.mb > 0 && !h.dia_off.empty()) {
+      rows(h.r0, h.r0 + h.mb - 1);
+      auto mm = std::minmax_element(h.dia_off.begin(), h.dia_off.end());
+      cols(h.r0 + *mm.first, h.r0 + h.mb - 1 + *mm.second);
+    }
+  } else if (h.kind == "dense") {
+    if (h.mb > 0 && !h.tile_col.empty()) {
+      rows(h.r0, h.r0 + h.mb - 1);
+      auto mm = std::minmax_element(h.tile_col.begin(), h.tile_col.end());
+      cols(*mm.first * h.b, *mm.second * h.b + h.b - 1);
+    }
+  } else {
+    for (int32_t c : h.col) cols(c, c);
+    for (int64_t r : h.origin) rows(r, r);
+    for (int64_t r : h.excl) rows(r, r);
+    for (int64_t r : h.atom) rows(r, r);
+  }
+  return sp;
 }
 
 void Plan::upload(cudaStream_t s) {
@@ -426,6 +470,7 @@ void Plan::upload(cudaStream_t s) {
         bytes_model += (double)(nnz * (4 + sv));
       }
     }
+    if (d.fam == FAM_NNZ_THREAD && std::getenv("AS_NT_LEGACY")) d.variant = 9;  // A/B knob: branching form
     ck((cudaError_t)prepare_part(d), "kernel attributes");
     // name the kernel form actually chosen (as_plan_info.kernels)
     std::string& fn = host.parts[pi].fam_name;
@@ -433,6 +478,7 @@ void Plan::upload(cudaStream_t s) {
     if (d.tile) fn += "_tile";
     if (d.fam == FAM_BLOCK_OFFSET && d.variant == 1) fn += "_tma";
     launches.push_back(d);
+    spans.push_back(part_span(h, host.n));
   }
   if (!host.prepass.empty()) {
     d_prepass = up_i32(host.prepass, s, "prepass");

@@ -22,6 +22,15 @@ struct Plan {
   as_plan_info_t info{};
   void* d_x = nullptr;           // scratch for as_spmv_host
   void* d_y = nullptr;
+  // per launch: x columns read [clo, chi] and global y rows written [rlo, rhi] (supersets;
+  // empty = clo > chi).  as_spmv_host pipelines chunked copies against launches with them.
+  struct Span {
+    int64_t clo, chi, rlo, rhi;
+  };
+  std::vector<Span> spans;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // as_spmv_host copy streams (lazy)
+  std::vector<cudaEvent_t> evs;                    // as_spmv_host events (lazy)
+  cudaEvent_t host_event(size_t i);
   std::string canon;
 
   ~Plan();

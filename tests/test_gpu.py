@@ -153,6 +153,46 @@ def test_spmv_host_path():
     assert S.check(y, yref, bound, np.float64)[0]
 
 
+LAP_CUTS = "cuts=[262144,524288,786432]"
+PIPE_GRAPHS = [
+    f"ROW_DIV({LAP_CUTS}) {{ DIA_DECOM(theta=0.5) {{ DIA }} }}",
+    f"ROW_DIV({LAP_CUTS}) {{ COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }}",
+    "COL_DIV(cuts=[500000]) { COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
+    "DIA_DECOM(theta=0.9995) { DIA | COMPRESS; BMW_ROW_BLOCK(1); WARP_TOTAL_RED; GMEM_ATOM_RED }",
+]
+
+
+@pytest.mark.parametrize("graph", PIPE_GRAPHS)
+@pytest.mark.parametrize("beta", [0.0, -2.0])
+def test_spmv_host_pipelined(graph, beta):
+    """as_spmv_host with several launches: chunked H2D of x / D2H of y on copy streams,
+    overlapped with the kernels (integer-exact inputs -> bit-identical to the oracle)."""
+    coo = synth.c2_lap2d(1024)
+    x, y0 = synth.vectors(coo.n, coo.m, 4, np.float64, True)
+    P = asp.Plan(_mat(coo), graph, device=0)
+    assert P.info()["n_launches"] >= 2
+    yref, _ = S.spmv_coo(coo.m, coo.row, coo.col, coo.val, x, 3.0, beta, y0)
+    xh = torch.from_numpy(x).pin_memory().numpy()
+    for _ in range(2):  # twice: the plan's copy streams and events are reused
+        yh = torch.from_numpy(y0.copy()).pin_memory().numpy()
+        P.spmv_host(3.0, xh, beta, yh)
+        assert np.array_equal(yh, yref), np.nonzero(yh != yref)[0][:10]
+
+
+def test_spmv_host_pipelined_bin():
+    """BIN: launch order is not monotone in rows or columns."""
+    coo = synth.random_powerlaw(20_000, 20_000, 7, 400, int_mode=True)
+    x, y0 = synth.vectors(coo.n, coo.m, 5, np.float64, True)
+    g = ("BIN(t=[4,64]) { COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED | "
+         "COMPRESS; BMW_ROW_BLOCK(1); WARP_TOTAL_RED; GMEM_ATOM_RED | "
+         "COMPRESS; BMTB_ROW_BLOCK(1); SHMEM_TOTAL_RED; GMEM_ATOM_RED }")
+    P = asp.Plan(_mat(coo), g, device=0)
+    yref, _ = S.spmv_coo(coo.m, coo.row, coo.col, coo.val, x, 1.0, 1.0, y0)
+    yh = y0.copy()
+    P.spmv_host(1.0, x, 1.0, yh)
+    assert np.array_equal(yh, yref)
+
+
 # ------------------------------------------------------------------ BASELINE configs
 C1_GRAPH = "COMPRESS; BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; SET_RESOURCE(128); GMEM_ATOM_RED"
 

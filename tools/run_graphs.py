@@ -21,7 +21,11 @@ CONFIGS = {
 
 
 def main():
-    c = CONFIGS[sys.argv[1]]()
+    if sys.argv[1] in CONFIGS:
+        c = CONFIGS[sys.argv[1]]()
+    else:  # full-size BASELINE configs (c1..c5)
+        import bench
+        c = bench.to_csr(bench.load_config(sys.argv[1])[0])
     A = asp.Matrix.from_csr(c.m, c.n, c.row_ptr, c.col, c.val)
     tdt = torch.float64 if c.val.dtype.itemsize == 8 else torch.float32
     x = torch.rand(c.n, dtype=tdt, device="cuda")
