@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restr
 }
 
 // -------------------------------------------------------------------------------------
-// k_nnz_thread, predicated-emit form (plans without fp32 heavy rows).  The per-element
+// k_nnz_thread, predicated-emit form (all plans but fp32 ADD-mode parts with heavy rows).  The per-element
 // head test of the form above branches around a writer call, and the 32 lanes of a warp
 // hit their heads at different elements, so ncu saw 12 of 32 threads active on average
 // (C5: 1.35 warp instructions per nonzero).  Here the loop body is branch-free: rows that
@@ -517,7 +517,7 @@ __device__ __forceinline__ void emit_excl(const DevPart& p, V* y, bool pred, int
 
 template <class V, bool PAD, int VEC, int KB, int EM, bool FULL, class XA>
 __device__ __forceinline__ void bmt_batch_pe(const DevPart& p, V* y, XA xa, const uint32_t* bm, const V* pv,
-                                             const int32_t* pc, int64_t stride, int j0, int len, int64_t& row,
+                                             const int32_t* pc, int64_t stride, int j0, int len, int32_t& row,
                                              double& acc, bool& inside, double& first) {
   double v[KB];
   int32_t c[KB];
@@ -525,7 +525,7 @@ __device__ __forceinline__ void bmt_batch_pe(const DevPart& p, V* y, XA xa, cons
 #pragma unroll
     for (int q = 0; q < KB; q += VEC) {
       if (FULL || j0 + q < len) {
-        PadLoad<V, VEC>::ld(pv + ((j0 + q) / VEC) * stride, pc + ((j0 + q) / VEC) * stride, v + q, c + q);
+        PadLoad<V, VEC>::ld(pv + (q / VEC) * stride, pc + (q / VEC) * stride, v + q, c + q);
       } else {
 #pragma unroll
         for (int r = 0; r < VEC; ++r) {
@@ -538,8 +538,8 @@ __device__ __forceinline__ void bmt_batch_pe(const DevPart& p, V* y, XA xa, cons
 #pragma unroll
     for (int q = 0; q < KB; ++q) {
       if (FULL || j0 + q < len) {
-        v[q] = (double)ld_seq(pv + j0 + q);
-        c[q] = ld_seq(pc + j0 + q);
+        v[q] = (double)ld_seq(pv + q);
+        c[q] = ld_seq(pc + q);
       } else {
         v[q] = 0.0;
         c[q] = 0;
@@ -573,15 +573,17 @@ __global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __re
     const uint32_t* bm = p.bitmap + t * p.bm_words;
     PadPos pp{0, 0};
     if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
-    const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;
+    const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;      // batch base
     const int32_t* pc = PAD ? p.pad_col + pp.base : p.col + a;
     const bool start_inside = ldm(bm) & 1u;
     bool inside = start_inside;
-    int64_t row = row0;
+    int32_t row = (int32_t)row0;  // device row indices are int32 (A36)
     double acc = 0.0, first = 0.0;
     const int full = len & ~(KB - 1);
     int j0 = 0;
-    for (; j0 < full; j0 += KB)
+    // pv / pc advance to the batch's first element (slot-major: KB/VEC chunk rows per batch)
+    const int64_t adv = PAD ? (KB / VEC) * pp.stride : KB;
+    for (; j0 < full; j0 += KB, pv += adv, pc += adv)
       bmt_batch_pe<V, PAD, VEC, KB, EM, true>(p, y, xa, bm, pv, pc, pp.stride, j0, len, row, acc, inside, first);
     if (j0 < len)
       bmt_batch_pe<V, PAD, VEC, KB, EM, false>(p, y, xa, bm, pv, pc, pp.stride, j0, len, row, acc, inside, first);
@@ -1359,9 +1361,10 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       const int tt = tpb;
       // batches of KB loads per thread: 8 for fp64, 4 for fp32 (A/B on c5s fp64: KB 4 633 vs
       // KB 8 646 GF/s; c3s fp32: 408 vs 394; KB 16 or 80 registers slower everywhere)
-      // predicated-emit form unless fp32 heavy rows need the scratch path (or the legacy
-      // form is forced for A/B timing: variant 9)
-      const bool pe = p.variant != 9 && !(sizeof(V) == 4 && p.n_heavy);
+      // predicated-emit form unless exclusive rows may need the fp32 heavy-row scratch
+      // (write_excl consults it in ADD mode only), or the legacy form is forced for A/B
+      // timing (variant 9)
+      const bool pe = p.variant != 9 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
       const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin;
 #define AS_NT(PADV, VECV)                                                                                 \
   {                                                                                                       \

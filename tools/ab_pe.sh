@@ -9,8 +9,8 @@ G3=("COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL,0); THREAD_BITMAP_RED_G; SET_RE
 CFG5=${1:-c5s}; CFG3=${2:-c3s}
 for leg in 1 ""; do
   tag=${leg:+legacy}; tag=${tag:-pe}
-  AS_NT_LEGACY=$leg python tools/sweep.py --config $CFG5 --reps 20 --graphs "${G5[@]}" > gpurun_out/ab_pe_${CFG5}_$tag.jsonl 2>> gpurun_out/ab_pe.err
-  AS_NT_LEGACY=$leg python tools/sweep.py --config $CFG3 --reps 20 --graphs "${G3[@]}" > gpurun_out/ab_pe_${CFG3}_$tag.jsonl 2>> gpurun_out/ab_pe.err
+  env ${leg:+AS_NT_LEGACY=1} python tools/sweep.py --config $CFG5 --reps 20 --graphs "${G5[@]}" > gpurun_out/ab_pe_${CFG5}_$tag.jsonl 2>> gpurun_out/ab_pe.err
+  env ${leg:+AS_NT_LEGACY=1} python tools/sweep.py --config $CFG3 --reps 20 --graphs "${G3[@]}" > gpurun_out/ab_pe_${CFG3}_$tag.jsonl 2>> gpurun_out/ab_pe.err
 done
 for f in gpurun_out/ab_pe_*.jsonl; do echo "== $f"; python -c "
 import json,sys
