@@ -68,6 +68,8 @@ typedef struct {
   int64_t nnz_real, stored_slots, pads, n_parts, n_launches, prepass_rows;
   double bytes_model, bytes_model_beta, bytes_floor;
   char kernels[512]; /* ';'-separated kernel names in launch order */
+  int single_writer;  /* every row's final value comes from exactly one STORE: as_spmv_dist
+                         with AS_EXCH_PEER fuses the peer stores into the SpMV epilogue */
 } as_plan_info_t;
 
 const char* as_last_error(void);
@@ -202,6 +204,11 @@ as_status_t as_matrix_col_span(as_matrix_t, int64_t* lo, int64_t* hi);
  *                 call).  y_full must be registered on every rank first
  *                 (as_dist_ipc_handle + as_dist_open_peers).  The wait times out after
  *                 AS_DIST_WAIT_TIMEOUT_NS and reports AS_ERR_CUDA at as_dist_check.
+ *                 Fused form: when the band plan is single-writer (as_plan_info_t.
+ *                 single_writer) and world <= 8, the SpMV kernels themselves store every
+ *                 final y value into the peers' y_full (the exchange overlaps the SpMV tile
+ *                 by tile) and the push kernel only publishes the flags; AS_DIST_NO_FUSE in
+ *                 the environment forces the separate push.
  * Every rank must make the same sequence of as_spmv_dist calls.  x_full and y_full must
  * not alias (iterate with two buffers).  NCCL is loaded at run time (dlopen
  * libnccl.so.2), so the library itself has no link-time NCCL dependency. */

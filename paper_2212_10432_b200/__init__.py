@@ -48,7 +48,7 @@ class AsPlanInfo(ctypes.Structure):
     _fields_ = [("nnz_real", _i64), ("stored_slots", _i64), ("pads", _i64), ("n_parts", _i64),
                 ("n_launches", _i64), ("prepass_rows", _i64), ("bytes_model", ctypes.c_double),
                 ("bytes_model_beta", ctypes.c_double), ("bytes_floor", ctypes.c_double),
-                ("kernels", ctypes.c_char * 512)]
+                ("kernels", ctypes.c_char * 512), ("single_writer", ctypes.c_int)]
 
 
 class AsSearchCfg(ctypes.Structure):

@@ -131,7 +131,8 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
 // parts in writer-rule order, the heavy-row epilogue.  before(i) runs on the host before
 // launch i is enqueued, after(i) after it (as_spmv_host hooks its copy pipeline there).
 template <class Before, class After>
-int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s, Before before, After after) {
+int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s, Before before, After after,
+             void* const* peer_y = nullptr, int n_peers = 0) {
   const size_t sv = P.dt == AS_R64F ? 8 : 4;
   int err = 0;
   if (P.n_prepass) {
@@ -148,11 +149,19 @@ int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s
     DevPart d = P.launches[i];
     d.alpha = a;
     d.beta = b;
+    d.n_peer = n_peers;
+    for (int q = 0; q < n_peers; ++q) d.peer_y[q] = peer_y[q];
     err = launch_part(d, x, y, s);
     if (!err) after(i);
   }
   if (P.n_heavy && !err) err = launch_heavy_epilogue(P.d_heavy_rows, P.d_heavy_acc, P.n_heavy, y, s);
   return err;
+}
+
+int run_plan_peers(Plan& P, const void* x, void* y, double alpha, double beta, void* stream, void* const* peer_y,
+                   int n_peers) {
+  if (n_peers > kMaxFusedPeers || (n_peers > 0 && !P.single_writer)) return (int)cudaErrorInvalidValue;
+  return run_plan(P, x, y, alpha, beta, (cudaStream_t)stream, [](size_t) {}, [](size_t) {}, peer_y, n_peers);
 }
 
 }  // namespace as
@@ -298,6 +307,7 @@ as_status_t as_plan_info(as_plan_t P, as_plan_info_t* out) {
   return guard([&] {
     if (!P || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
     *out = P->P->info;
+    out->single_writer = P->P->single_writer ? 1 : 0;
   });
 }
 

@@ -20,6 +20,7 @@ enum Fam {
 };
 
 constexpr int kMaxDiags = 64;
+constexpr int kMaxFusedPeers = 7;  // as_spmv_dist fused peer stores: up to 8 ranks
 
 struct DevPart {
   int fam = FAM_NONE;
@@ -88,6 +89,11 @@ struct DevPart {
   const uint32_t* heavy_bits = nullptr;   // 1 bit per global row: is heavy
   int64_t n_heavy = 0;
   double* heavy_acc = nullptr;
+  // as_spmv_dist, AS_EXCH_PEER on single-writer plans: every STORE of a final y value is
+  // also written to the same offset of each peer's y_full band (P2P stores over NVLink into
+  // CUDA IPC mappings), fusing the exchange into the SpMV epilogue
+  void* peer_y[kMaxFusedPeers] = {nullptr};
+  int n_peer = 0;
   // launch
   int tpb = 256, grid = 0;
   size_t smem = 0;

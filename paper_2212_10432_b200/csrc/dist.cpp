@@ -252,7 +252,25 @@ as_status_t as_spmv_dist(as_dist_t D, as_plan_t local, const void* alpha, const 
       fail(AS_ERR_INVALID_ARG, "exchange must be AS_EXCH_NONE, AS_EXCH_NCCL or AS_EXCH_PEER");
     }
     char* band = (char*)y_full + r0 * sv;
-    if (P.m > 0) {
+    // fused exchange: single-writer band plans store every final y value into the peers'
+    // y_full directly from the SpMV epilogue; the push kernel then only signals (0 bytes)
+    const bool fused = exchange == AS_EXCH_PEER && P.single_writer && D->world - 1 <= kMaxFusedPeers &&
+                       !std::getenv("AS_DIST_NO_FUSE");
+    if (fused && P.m > 0) {
+      void* pys[kMaxFusedPeers];
+      int np = 0;
+      for (int q = 0; q < D->world; ++q)
+        if (q != r) pys[np++] = (*peers)[q] + r0 * sv;
+      const double a = P.dt == AS_R64F ? *(const double*)alpha : (double)*(const float*)alpha;
+      const double b = P.dt == AS_R64F ? *(const double*)beta : (double)*(const float*)beta;
+      int cur0 = 0;
+      cudaGetDevice(&cur0);
+      cudaSetDevice(D->device);
+      cudaError_t prior = cudaGetLastError();
+      int e = prior != cudaSuccess ? (int)prior : run_plan_peers(P, x_full, band, a, b, stream, pys, np);
+      cudaSetDevice(cur0);
+      if (e) fail(AS_ERR_CUDA, std::string("fused band SpMV: ") + cudaGetErrorString((cudaError_t)e));
+    } else if (P.m > 0) {
       as_status_t st = as_spmv(local, alpha, x_full, beta, band, stream);
       if (st != AS_OK) fail(st, as_last_error());
     }
@@ -283,7 +301,7 @@ as_status_t as_spmv_dist(as_dist_t D, as_plan_t local, const void* alpha, const 
       ++pp.n;
     }
     ++D->epoch;
-    err = launch_push(band, (r1 - r0) * (int64_t)sv, pp, D->ctr, &D->target, D->epoch, r, stream);
+    err = launch_push(band, fused ? 0 : (r1 - r0) * (int64_t)sv, pp, D->ctr, &D->target, D->epoch, r, stream);
     if (!err) err = launch_wait(D->flags, D->world, r, D->epoch, AS_DIST_WAIT_TIMEOUT_NS, D->status, stream);
     cudaSetDevice(cur);
     if (err) fail(AS_ERR_CUDA, std::string("peer exchange: ") + cudaGetErrorString((cudaError_t)err));

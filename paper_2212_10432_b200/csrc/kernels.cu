@@ -112,6 +112,13 @@ __device__ __forceinline__ int64_t heavy_slot(const DevPart& p, int64_t g) {
   return -1;
 }
 
+// fused exchange (as_spmv_dist): the final value of row g also goes to every peer's band
+template <class V>
+__device__ __forceinline__ void peer_store(const DevPart& p, int64_t g, V v) {
+#pragma unroll 1
+  for (int i = 0; i < p.n_peer; ++i) ((V*)p.peer_y[i])[g] = v;
+}
+
 template <class V>
 __device__ __forceinline__ void write_excl(const DevPart& p, V* y, int64_t r, double acc) {
   int64_t g = out_row(p, r);
@@ -128,6 +135,7 @@ __device__ __forceinline__ void write_excl(const DevPart& p, V* y, int64_t r, do
     double v = p.alpha * acc;
     if (p.beta != 0.0) v += p.beta * (double)y[g];
     y[g] = (V)v;
+    if (p.n_peer) peer_store(p, g, (V)v);
   } else {
     y[g] = (V)((double)y[g] + p.alpha * acc);
   }
@@ -503,7 +511,10 @@ __global__ void __launch_bounds__(1024) k_nnz_thread(DevPart p, const V* __restr
 template <class V, int EM>
 __device__ __forceinline__ void emit_excl(const DevPart& p, V* y, bool pred, int64_t r, double s) {
   if constexpr (EM == 0) {
-    if (pred) y[p.origin_base + r] = (V)(p.alpha * s);
+    if (pred) {
+      y[p.origin_base + r] = (V)(p.alpha * s);
+      if (p.n_peer) peer_store(p, p.origin_base + r, (V)(p.alpha * s));
+    }
   } else {
     if (pred) {
       const int64_t g = out_row(p, r);
@@ -511,6 +522,7 @@ __device__ __forceinline__ void emit_excl(const DevPart& p, V* y, bool pred, int
       if (p.mode == 1) v += (double)y[g];
       else if (p.beta != 0.0) v += p.beta * (double)y[g];
       y[g] = (V)v;
+      if (p.mode == 0 && p.n_peer) peer_store(p, g, (V)v);
     }
   }
 }

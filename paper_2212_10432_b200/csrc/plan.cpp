@@ -485,6 +485,9 @@ void Plan::upload(cudaStream_t s) {
     n_prepass = (int64_t)host.prepass.size();
   }
   if (dt == AS_R32F) mark_heavy_rows(s);
+  single_writer = host.prepass.empty() && n_heavy == 0;
+  for (int64_t pi : host.launch_order)
+    if (host.parts[pi].mode != 0 || !host.parts[pi].atom.empty()) single_writer = false;
   ck(cudaStreamSynchronize(s), "upload");
 }
 

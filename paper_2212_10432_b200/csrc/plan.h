@@ -28,6 +28,9 @@ struct Plan {
     int64_t clo, chi, rlo, rhi;
   };
   std::vector<Span> spans;
+  // every row's final value is produced by exactly one STORE (no pre-pass, no ADD parts,
+  // no atomic rows, no fp32 heavy-row epilogue): as_spmv_dist may fuse peer stores
+  bool single_writer = false;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // as_spmv_host copy streams (lazy)
   std::vector<cudaEvent_t> evs;                    // as_spmv_host events (lazy)
   cudaEvent_t host_event(size_t i);
@@ -46,6 +49,11 @@ struct Plan {
   int64_t n_heavy = 0;
   void compute_model();
 };
+
+// Enqueue one SpMV of the plan on `stream` (pre-pass, parts, epilogue); with n_peers > 0
+// every part's final STOREs also go to peer_y[i] (+ the row offset).  Returns cudaError_t.
+int run_plan_peers(Plan& P, const void* x, void* y, double alpha, double beta, void* stream, void* const* peer_y,
+                   int n_peers);
 
 }  // namespace as
 

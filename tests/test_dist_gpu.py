@@ -66,10 +66,21 @@ def test_dist_world1(exchange):
     d.close()
 
 
-def _peer_worker(rank, world, port, iters, q):
+PEER_GRAPHS = {
+    # straddling rows (atomics): separate push kernel after the SpMV
+    "push": "COMPRESS; BMT_NNZ_BLOCK(16); BMT_PAD(GLOBAL,2); THREAD_BITMAP_RED_G; GMEM_ATOM_RED",
+    # single-writer (one STORE per row): peer stores fused into the SpMV epilogue
+    "fused": "COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED",
+    "fused_warp": "COMPRESS; BMW_ROW_BLOCK(1); WARP_TOTAL_RED; GMEM_ATOM_RED",
+}
+
+
+def _peer_worker(rank, world, port, iters, q, graph="push", no_fuse=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if no_fuse:
+        os.environ["AS_DIST_NO_FUSE"] = "1"
     import torch
     import torch.distributed as dist
     import paper_2212_10432_b200 as asp
@@ -80,8 +91,8 @@ def _peer_worker(rank, world, port, iters, q):
         c, x = _band_case()
         A = asp.Matrix.from_csr(c.m, c.n, c.row_ptr, c.col, c.val)
         r0, r1, Ab, cuts = D.band(A, rank, world)
-        P = asp.Plan(Ab, "COMPRESS; BMT_NNZ_BLOCK(16); BMT_PAD(GLOBAL,2); THREAD_BITMAP_RED_G; GMEM_ATOM_RED",
-                     device=0)
+        P = asp.Plan(Ab, PEER_GRAPHS[graph], device=0)
+        assert P.info()["single_writer"] == (graph != "push"), P.info()
         d = D.init_dist(rank, world, 0, cuts, nccl=False)
         Y = [torch.from_numpy(x).cuda(), torch.full((c.m,), float("nan"), dtype=torch.float64, device="cuda")]
         for y in Y:
@@ -97,14 +108,18 @@ def _peer_worker(rank, world, port, iters, q):
         q.put((rank, None, repr(e)))
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_dist_peer_push_multiprocess(world):
+@pytest.mark.parametrize("world,graph,no_fuse", [(2, "push", False), (3, "push", False), (2, "fused", False),
+                                                (3, "fused", False), (3, "fused_warp", False),
+                                                (2, "fused", True)])
+def test_dist_peer_push_multiprocess(world, graph, no_fuse):
+    """x_{k+1} = A x_k over peer memory: separate push kernel, or (single-writer plans) peer
+    stores fused into the SpMV epilogue; bit-identical to the oracle on every rank."""
     import torch.multiprocessing as mp
     iters = 3
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, iters, q)) for r in range(world)]
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, iters, q, graph, no_fuse)) for r in range(world)]
     for p in procs:
         p.start()
     try:
