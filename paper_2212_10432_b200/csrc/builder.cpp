@@ -240,46 +240,74 @@ struct Builder {
     double theta = op.getf("theta");
     int64_t mb = (int64_t)st.rows.size();
     int64_t r0 = mb ? st.rows[0] : 0, r1 = r0 + mb;
-    std::unordered_map<int64_t, int64_t> cnt;  // key I * nbc + J
-    int64_t nbc = (A.n + b - 1) / b + 1;
-    for (int64_t r = r0; r < r1; ++r)
-      for (int64_t e = A.row_ptr[r]; e < A.row_ptr[r + 1]; ++e)
-        if (live(st, e)) cnt[(r / b) * nbc + A.col[e] / b]++;
-    std::vector<int64_t> tiles;
-    for (auto& kv : cnt)
-      if ((double)kv.second >= theta * (double)(b * b)) tiles.push_back(kv.first);
-    std::sort(tiles.begin(), tiles.end());
-    int64_t T = (int64_t)tiles.size();
+    // per tile row I (b rows): the column tiles J of its live nonzeros, sorted; a tile is
+    // selected when it holds >= theta*b^2 of them.  Tile rows are independent -> parallel.
+    const int64_t I0 = mb ? r0 / b : 0, nI = mb ? (r1 - 1) / b - I0 + 1 : 0;
+    const double need = theta * (double)(b * b);
+    std::vector<std::vector<int64_t>> sel((size_t)nI);
+    parallel_for(
+        nI,
+        [&](int64_t ia, int64_t ie) {
+          std::vector<int64_t> js;
+          for (int64_t ii = ia; ii < ie; ++ii) {
+            const int64_t I = I0 + ii;
+            js.clear();
+            for (int64_t r = std::max(I * b, r0); r < std::min(I * b + b, r1); ++r)
+              for (int64_t e = A.row_ptr[r]; e < A.row_ptr[r + 1]; ++e)
+                if (live(st, e)) js.push_back(A.col[e] / b);
+            std::sort(js.begin(), js.end());
+            for (size_t u = 0; u < js.size();) {
+              size_t v = u;
+              while (v < js.size() && js[v] == js[u]) ++v;
+              if ((double)(v - u) >= need) sel[(size_t)ii].push_back(js[u]);
+              u = v;
+            }
+          }
+        },
+        256);
     HostPart P;
     P.kind = "dense";
     P.b = b;
     P.r0 = r0;
     P.mb = mb;
-    P.tile_val.assign((size_t)(T * b * b), 0.0);
-    std::unordered_map<int64_t, int64_t> tindex;
-    for (int64_t t = 0; t < T; ++t) {
-      tindex[tiles[t]] = t;
-      int64_t I = tiles[t] / nbc, J = tiles[t] % nbc;
-      if (P.tile_row_id.empty() || P.tile_row_id.back() != I) {
-        P.tile_row_id.push_back(I);
-        P.tile_row_ptr.push_back(t);
-      }
-      P.tile_col.push_back(J);
+    std::vector<int64_t> tile_of_row((size_t)nI + 1, 0);  // first tile index of tile row ii
+    for (int64_t ii = 0; ii < nI; ++ii) {
+      tile_of_row[(size_t)ii + 1] = tile_of_row[(size_t)ii] + (int64_t)sel[(size_t)ii].size();
+      if (sel[(size_t)ii].empty()) continue;
+      P.tile_row_id.push_back(I0 + ii);
+      P.tile_row_ptr.push_back(tile_of_row[(size_t)ii]);
+      for (int64_t J : sel[(size_t)ii]) P.tile_col.push_back(J);
     }
+    const int64_t T = tile_of_row[(size_t)nI];
     P.tile_row_ptr.push_back(T);
+    P.tile_val.assign((size_t)(T * b * b), 0.0);
     auto mk = std::make_shared<std::vector<uint8_t>>(A.nnz());
     auto& M = *mk;
-    for (int64_t e = 0; e < A.nnz(); ++e) M[e] = live(st, e);
+    parallel_for(A.nnz(), [&](int64_t a0, int64_t e0) {
+      for (int64_t e = a0; e < e0; ++e) M[e] = live(st, e);
+    });
     if (T) {
-      for (int64_t r = r0; r < r1; ++r)
-        for (int64_t e = A.row_ptr[r]; e < A.row_ptr[r + 1]; ++e) {
-          if (!M[e]) continue;
-          auto it = tindex.find((r / b) * nbc + A.col[e] / b);
-          if (it == tindex.end()) continue;
-          int64_t i = r - (r / b) * b, j = A.col[e] - (A.col[e] / b) * b;
-          P.tile_val[(size_t)(it->second * b * b + j * b + i)] = A.val[e];
-          M[e] = 0;
-        }
+      parallel_for(
+          nI,
+          [&](int64_t ia, int64_t ie) {
+            for (int64_t ii = ia; ii < ie; ++ii) {
+              const std::vector<int64_t>& js = sel[(size_t)ii];
+              if (js.empty()) continue;
+              const int64_t I = I0 + ii;
+              for (int64_t r = std::max(I * b, r0); r < std::min(I * b + b, r1); ++r)
+                for (int64_t e = A.row_ptr[r]; e < A.row_ptr[r + 1]; ++e) {
+                  if (!M[e]) continue;
+                  const int64_t J = A.col[e] / b;
+                  auto it = std::lower_bound(js.begin(), js.end(), J);
+                  if (it == js.end() || *it != J) continue;
+                  const int64_t t = tile_of_row[(size_t)ii] + (it - js.begin());
+                  const int64_t i = r - I * b, j = A.col[e] - J * b;
+                  P.tile_val[(size_t)(t * b * b + j * b + i)] = A.val[e];
+                  M[e] = 0;
+                }
+            }
+          },
+          256);
       for (int64_t I : P.tile_row_id)
         for (int64_t r = I * b; r < I * b + b; ++r)
           if (r >= r0 && r < r1) P.excl.push_back(r);

@@ -112,6 +112,13 @@ __device__ __forceinline__ int64_t heavy_slot(const DevPart& p, int64_t g) {
   return -1;
 }
 
+// L2 prefetch of [ptr, ptr + bytes): 16-byte aligned start and size (rounded inward)
+__device__ __forceinline__ void bulk_prefetch(const void* ptr, int64_t bytes) {
+  const uintptr_t a = ((uintptr_t)ptr + 15) & ~(uintptr_t)15;
+  const uintptr_t e = ((uintptr_t)ptr + bytes) & ~(uintptr_t)15;
+  if (e > a) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
+
 // fused exchange (as_spmv_dist): the final value of row g also goes to every peer's band
 template <class V>
 __device__ __forceinline__ void peer_store(const DevPart& p, int64_t g, V v) {
@@ -577,7 +584,34 @@ template <class V, bool PAD, int VEC, int KB, int EM>
 __global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   static_assert(32 % KB == 0 && KB % VEC == 0, "KB divides 32 and is a multiple of VEC");
   const XGlobal<V> xa{x};
-  for (int64_t t = thread_units(p.n_bmt).begin, t_e = thread_units(p.n_bmt).end; t < t_e; t += blockDim.x) {
+  const Units u = thread_units(p.n_bmt);
+  for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x) {
+    // L2 bulk prefetch (cp.async.bulk.prefetch) of the CTA's round p.pf rounds ahead: the
+    // HBM stream of values/columns runs ahead of the latency-bound per-thread batches
+    // without registers or shared memory.  Rounds are contiguous in the CSR order and in
+    // each chunk row of the global slot-major layout.
+    if (p.pf && threadIdx.x < 64) {
+      const int64_t r0 = t - threadIdx.x + (int64_t)p.pf * blockDim.x;
+      const int64_t r1 = min(r0 + (int64_t)blockDim.x, t_e);
+      if (r0 < r1) {
+        if constexpr (PAD) {
+          if (p.n_grp == 1) {
+            const int nch = (int)((p.k + VEC - 1) / VEC);
+            const int c = threadIdx.x >> 1;
+            if (c < nch) {
+              const int64_t slot = (int64_t)c * p.n_bmt * VEC + r0 * VEC;
+              const int64_t cnt = (r1 - r0) * VEC;
+              if (threadIdx.x & 1) bulk_prefetch(p.pad_col + slot, cnt * 4);
+              else bulk_prefetch((const V*)p.pad_val + slot, cnt * (int64_t)sizeof(V));
+            }
+          }
+        } else if (!p.bmt_start && threadIdx.x < 2) {
+          const int64_t e0 = r0 * p.k, e1 = min(r1 * p.k, p.nnz_p);
+          if (threadIdx.x & 1) bulk_prefetch(p.col + e0, (e1 - e0) * 4);
+          else bulk_prefetch((const V*)p.val + e0, (e1 - e0) * (int64_t)sizeof(V));
+        }
+      }
+    }
     const int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
     const int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
     const int len = (int)(e - a);

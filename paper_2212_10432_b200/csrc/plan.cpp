@@ -471,6 +471,8 @@ void Plan::upload(cudaStream_t s) {
       }
     }
     if (d.fam == FAM_NNZ_THREAD && std::getenv("AS_NT_LEGACY")) d.variant = 9;  // A/B knob: branching form
+    if (d.fam == FAM_NNZ_THREAD)  // L2 bulk prefetch distance in CTA rounds (A/B knob AS_NT_PF)
+      d.pf = std::getenv("AS_NT_PF") ? std::atoi(std::getenv("AS_NT_PF")) : 0;
     ck((cudaError_t)prepare_part(d), "kernel attributes");
     // name the kernel form actually chosen (as_plan_info.kernels)
     std::string& fn = host.parts[pi].fam_name;
