@@ -166,6 +166,18 @@ typedef struct {
 } as_search_cfg_t;
 as_status_t as_search(as_matrix_t, const as_search_cfg_t*, int device, void* stream,
                       as_plan_t* best, char* best_graph, size_t* len);
+/* The search's cost model (NEXT-3; the paper's learned performance model of P:369 step 3,
+ * P:371-377).  as_graph_features: fixed-length feature vector of a graph -- per operator
+ * the occurrence count over all branches (24: ROW_DIV ... SHMEM_OFFSET_RED, SET_RESOURCE),
+ * per numeric parameter class the mean log2(1 + value) (15: BMT/BMW/BMTB block sizes,
+ * tpb, grid, stages, vec, DIA theta/max, DENSE b/theta, SORT_SUB g), then the number of
+ * leaves.  out == NULL -> *n = length.  as_surrogate_fit_predict: fits the gradient-boosted
+ * regression-tree ensemble the search uses (60 rounds, depth 3, shrinkage 0.2, squared
+ * loss) on X[n x d] (row-major) -> y[n] and writes its predictions for Xq[nq x d] to
+ * out[nq].  Deterministic; host only. */
+as_status_t as_graph_features(as_graph_t, double* out, size_t* n);
+as_status_t as_surrogate_fit_predict(const double* X, const double* y, size_t n, size_t d,
+                                     const double* Xq, size_t nq, double* out);
 /* One random legal graph text for this matrix (the search's generator), for tests. */
 as_status_t as_random_graph(as_matrix_t, uint64_t seed, char* buf, size_t* len);
 

@@ -86,6 +86,8 @@ _sig("as_spmv", [_vp, _vp, _vp, _vp, _vp, _vp])
 _sig("as_spmv_host", [_vp, _vp, _vp, _vp, _vp, _vp])
 _sig("as_search", [_vp, _P(AsSearchCfg), _i32, _vp, _P(_vp), ctypes.c_char_p, _P(_sz)])
 _sig("as_random_graph", [_vp, ctypes.c_uint64, ctypes.c_char_p, _P(_sz)])
+_sig("as_graph_features", [_vp, _vp, _P(_sz)])
+_sig("as_surrogate_fit_predict", [_vp, _vp, _sz, _sz, _vp, _sz, _vp])
 _sig("as_dist_row_cuts", [_vp, _i32, _vp])
 _sig("as_matrix_col_span", [_vp, _vp, _vp])
 _ALLOC_T = ctypes.CFUNCTYPE(_vp, _sz, _vp, _vp)
@@ -106,7 +108,7 @@ EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create
             "as_plan_keys", "as_plan_destroy", "as_spmv", "as_spmv_host", "as_search", "as_random_graph",
             "as_dist_row_cuts", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
             "as_dist_set_cuts", "as_dist_ipc_handle", "as_dist_open_peers", "as_spmv_dist", "as_dist_check",
-            "as_dist_destroy"]
+            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict"]
 
 
 class AsError(RuntimeError):
@@ -231,6 +233,14 @@ class Graph:
     def __str__(self):
         return _string(_lib.as_graph_print, self._h)
 
+    def features(self) -> np.ndarray:
+        """Feature vector of the search's cost model (as_graph_features)."""
+        n = _sz(0)
+        _ck(_lib.as_graph_features(self._h, None, ctypes.byref(n)))
+        out = np.zeros(n.value, np.float64)
+        _ck(_lib.as_graph_features(self._h, out.ctypes.data, ctypes.byref(n)))
+        return out
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib:
             _lib.as_graph_destroy(self._h)
@@ -329,6 +339,17 @@ def search(matrix: Matrix, device: int = 0, stream=None, seed: int = 1, max_cand
         text = buf.value.decode()
     p = Plan(matrix, None, device, _handle=h.value)
     return p, text
+
+
+def surrogate_fit_predict(X, y, Xq) -> np.ndarray:
+    """The search's gradient-boosted tree cost model: fit on (X, y), predict Xq."""
+    X = np.ascontiguousarray(X, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    Xq = np.ascontiguousarray(Xq, np.float64)
+    out = np.zeros(Xq.shape[0], np.float64)
+    _ck(_lib.as_surrogate_fit_predict(X.ctypes.data, y.ctypes.data, X.shape[0], X.shape[1], Xq.ctypes.data,
+                                      Xq.shape[0], out.ctypes.data))
+    return out
 
 
 def version() -> str:

@@ -73,6 +73,12 @@ Seq parse_graph(const std::string& text);  // parse + expand replicated branches
 std::string print_graph(const Seq& g);
 bool is_branching(const std::string& name);
 
+// search cost model (surrogate.cpp, NEXT-3)
+size_t graph_feature_count();
+std::vector<double> graph_features(const Seq& g);
+void surrogate_fit_predict(const double* X, const double* y, size_t n, size_t d, const double* Xq, size_t nq,
+                           double* out, int rounds, int max_depth, double lr);
+
 // ------------------------------------------------------------------ matrix (host, canonical CSR)
 struct Matrix {
   int64_t m = 0, n = 0;

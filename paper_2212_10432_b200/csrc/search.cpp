@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <cstdlib>
 #include <set>
 
 #include "internal.h"
@@ -408,13 +409,72 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
     return {t_med, canon};
   };
   auto elapsed = [&] { return std::chrono::duration<double>(clk::now() - t_start).count(); };
-  // step 1-2: random structures x coarse parameter grid; 60 % of the budget
+  // step 1-2: random structures x coarse parameter grid; 45 % of the budget (60 %
+  // without the cost-model stage)
+  const bool use_model = !std::getenv("AS_SEARCH_NO_SURROGATE");
+  const double coarse_frac = use_model ? 0.45 : 0.6;
   Rng seq(cfg->seed);
   for (int i = 0; i < maxc + cfg->n_seed_graphs; ++i) {
-    if (cfg->budget_seconds > 0 && elapsed() > 0.6 * cfg->budget_seconds && tried > 0) break;
+    if (cfg->budget_seconds > 0 && elapsed() > coarse_frac * cfg->budget_seconds && tried > 0) break;
     if (i >= cfg->n_seed_graphs && tried >= maxc) break;
     std::string text = i < cfg->n_seed_graphs ? std::string(cfg->seed_graphs[i]) : random_graph(M, seq.next());
     evaluate(i, text, sampled ? "sample" : "ok");
+  }
+  // cost-model stage (NEXT-3, P:369 step 3): fit the gradient-boosted tree model on the
+  // candidates timed so far (log time), rank a pool of unseen random graphs and
+  // one-parameter neighbours of the best four, and run them in predicted order, refitting
+  // after every 4 new timings; up to 80 % of the budget
+  if (use_model) {
+    Rng pr(cfg->seed ^ 0xA24BAED4963EE407ull);
+    const size_t d = graph_feature_count();
+    int ran = 0;
+    const int cap = std::max(4, maxc / 2);
+    while (cfg->budget_seconds <= 0 || elapsed() < 0.8 * cfg->budget_seconds) {
+      std::vector<Cand> okc;
+      for (auto& c : ranked)
+        if (c.t > 0) okc.push_back(c);
+      if (okc.size() < 8 || ran >= cap) break;
+      std::vector<double> X, y;
+      for (auto& c : okc) {
+        std::vector<double> f = graph_features(parse_graph(c.canon));
+        X.insert(X.end(), f.begin(), f.end());
+        y.push_back(std::log(c.t));
+      }
+      std::sort(okc.begin(), okc.end(), [](const Cand& a, const Cand& b) { return a.t < b.t; });
+      std::vector<std::string> pool;
+      std::set<std::string> inpool;
+      auto add = [&](const std::string& text) {
+        if (text.empty()) return;
+        std::string c;
+        try {
+          c = print_graph(parse_graph(text));
+        } catch (const Error&) {
+          return;
+        }
+        if (seen.count(c) || inpool.count(c)) return;
+        inpool.insert(c);
+        pool.push_back(c);
+      };
+      for (int k = 0; k < 192; ++k) add(random_graph(M, pr.next()));
+      for (size_t b = 0; b < std::min<size_t>(4, okc.size()); ++b)
+        for (int k = 0; k < 24; ++k) add(mutate_graph(parse_graph(okc[b].canon), pr));
+      if (pool.empty()) break;
+      std::vector<double> Xq;
+      for (auto& c : pool) {
+        std::vector<double> f = graph_features(parse_graph(c));
+        Xq.insert(Xq.end(), f.begin(), f.end());
+      }
+      std::vector<double> pred(pool.size());
+      surrogate_fit_predict(X.data(), y.data(), y.size(), d, Xq.data(), pool.size(), pred.data(), 60, 3, 0.2);
+      std::vector<size_t> order(pool.size());
+      for (size_t k = 0; k < order.size(); ++k) order[k] = k;
+      std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return pred[a] < pred[b]; });
+      for (size_t k = 0; k < std::min<size_t>(4, order.size()) && ran < cap; ++k) {
+        if (cfg->budget_seconds > 0 && elapsed() > 0.8 * cfg->budget_seconds) break;
+        evaluate(2000 + ran, pool[order[k]], sampled ? "sample_model" : "model");
+        ++ran;
+      }
+    }
   }
   // fine stage: simulated annealing over one-parameter neighbours of the incumbent, starting
   // from the best coarse candidate ("terminated early by simulated annealing")
