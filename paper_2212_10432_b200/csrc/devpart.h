@@ -94,7 +94,6 @@ struct DevPart {
   // CUDA IPC mappings), fusing the exchange into the SpMV epilogue
   void* peer_y[kMaxFusedPeers] = {nullptr};
   int n_peer = 0;
-  int pf = 0;  // k_nnz_thread_pe: L2 bulk prefetch this many CTA rounds ahead (0 = off)
   // launch
   int tpb = 256, grid = 0;
   size_t smem = 0;

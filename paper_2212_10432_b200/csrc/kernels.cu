@@ -112,13 +112,6 @@ __device__ __forceinline__ int64_t heavy_slot(const DevPart& p, int64_t g) {
   return -1;
 }
 
-// L2 prefetch of [ptr, ptr + bytes): 16-byte aligned start and size (rounded inward)
-__device__ __forceinline__ void bulk_prefetch(const void* ptr, int64_t bytes) {
-  const uintptr_t a = ((uintptr_t)ptr + 15) & ~(uintptr_t)15;
-  const uintptr_t e = ((uintptr_t)ptr + bytes) & ~(uintptr_t)15;
-  if (e > a) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
-}
-
 // fused exchange (as_spmv_dist): the final value of row g also goes to every peer's band
 template <class V>
 __device__ __forceinline__ void peer_store(const DevPart& p, int64_t g, V v) {
@@ -580,65 +573,55 @@ __device__ __forceinline__ void bmt_batch_pe(const DevPart& p, V* y, XA xa, cons
   }
 }
 
+// One BMT in predicated-emit form: rows closed inside the BMT are stored in the loop; the
+// caller gets the straddling first segment (`first`, valid when !s0 && inside), the open last
+// segment (`acc`, of row `row`), and whether the BMT starts at a row head (s0) / holds a
+// head anywhere (inside).
+struct ScanPE {
+  double first, acc;
+  int32_t row;
+  bool s0, inside;
+};
+template <class V, bool PAD, int VEC, int KB, int EM, class XA>
+__device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int64_t t, PadPos pp) {
+  static_assert(32 % KB == 0 && KB % VEC == 0, "KB divides 32 and is a multiple of VEC");
+  const int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
+  const int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
+  const int len = (int)(e - a);
+  const uint32_t* bm = p.bitmap + t * p.bm_words;
+  const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;  // batch base
+  const int32_t* pc = PAD ? p.pad_col + pp.base : p.col + a;
+  ScanPE o;
+  o.s0 = ldm(bm) & 1u;
+  o.inside = o.s0;
+  o.row = (int32_t)ldm(p.bmt_first_row + t);  // device row indices are int32 (A36)
+  o.acc = 0.0;
+  o.first = 0.0;
+  const int full = len & ~(KB - 1);
+  int j0 = 0;
+  // pv / pc advance to the batch's first element (slot-major: KB/VEC chunk rows per batch)
+  const int64_t adv = PAD ? (KB / VEC) * pp.stride : KB;
+  for (; j0 < full; j0 += KB, pv += adv, pc += adv)
+    bmt_batch_pe<V, PAD, VEC, KB, EM, true>(p, y, xa, bm, pv, pc, pp.stride, j0, len, o.row, o.acc, o.inside, o.first);
+  if (j0 < len)
+    bmt_batch_pe<V, PAD, VEC, KB, EM, false>(p, y, xa, bm, pv, pc, pp.stride, j0, len, o.row, o.acc, o.inside, o.first);
+  return o;
+}
+
 template <class V, bool PAD, int VEC, int KB, int EM>
 __global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
-  static_assert(32 % KB == 0 && KB % VEC == 0, "KB divides 32 and is a multiple of VEC");
   const XGlobal<V> xa{x};
   const Units u = thread_units(p.n_bmt);
   for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x) {
-    // L2 bulk prefetch (cp.async.bulk.prefetch) of the CTA's round p.pf rounds ahead: the
-    // HBM stream of values/columns runs ahead of the latency-bound per-thread batches
-    // without registers or shared memory.  Rounds are contiguous in the CSR order and in
-    // each chunk row of the global slot-major layout.
-    if (p.pf && threadIdx.x < 64) {
-      const int64_t r0 = t - threadIdx.x + (int64_t)p.pf * blockDim.x;
-      const int64_t r1 = min(r0 + (int64_t)blockDim.x, t_e);
-      if (r0 < r1) {
-        if constexpr (PAD) {
-          if (p.n_grp == 1) {
-            const int nch = (int)((p.k + VEC - 1) / VEC);
-            const int c = threadIdx.x >> 1;
-            if (c < nch) {
-              const int64_t slot = (int64_t)c * p.n_bmt * VEC + r0 * VEC;
-              const int64_t cnt = (r1 - r0) * VEC;
-              if (threadIdx.x & 1) bulk_prefetch(p.pad_col + slot, cnt * 4);
-              else bulk_prefetch((const V*)p.pad_val + slot, cnt * (int64_t)sizeof(V));
-            }
-          }
-        } else if (!p.bmt_start && threadIdx.x < 2) {
-          const int64_t e0 = r0 * p.k, e1 = min(r1 * p.k, p.nnz_p);
-          if (threadIdx.x & 1) bulk_prefetch(p.col + e0, (e1 - e0) * 4);
-          else bulk_prefetch((const V*)p.val + e0, (e1 - e0) * (int64_t)sizeof(V));
-        }
-      }
-    }
-    const int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
-    const int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
-    const int len = (int)(e - a);
-    const int64_t row0 = ldm(p.bmt_first_row + t);
-    const uint32_t* bm = p.bitmap + t * p.bm_words;
     PadPos pp{0, 0};
     if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
-    const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;      // batch base
-    const int32_t* pc = PAD ? p.pad_col + pp.base : p.col + a;
-    const bool start_inside = ldm(bm) & 1u;
-    bool inside = start_inside;
-    int32_t row = (int32_t)row0;  // device row indices are int32 (A36)
-    double acc = 0.0, first = 0.0;
-    const int full = len & ~(KB - 1);
-    int j0 = 0;
-    // pv / pc advance to the batch's first element (slot-major: KB/VEC chunk rows per batch)
-    const int64_t adv = PAD ? (KB / VEC) * pp.stride : KB;
-    for (; j0 < full; j0 += KB, pv += adv, pc += adv)
-      bmt_batch_pe<V, PAD, VEC, KB, EM, true>(p, y, xa, bm, pv, pc, pp.stride, j0, len, row, acc, inside, first);
-    if (j0 < len)
-      bmt_batch_pe<V, PAD, VEC, KB, EM, false>(p, y, xa, bm, pv, pc, pp.stride, j0, len, row, acc, inside, first);
+    const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM>(p, y, xa, t, pp);
     // first segment closed inside the BMT but begun before it: straddler
-    if (!start_inside && inside) write_atom(p, y, row0, first);
+    if (!o.s0 && o.inside) write_atom(p, y, ldm(p.bmt_first_row + t), o.first);
     // open last segment: exclusive iff it began at a head here and the next BMT starts a row
     const bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
-    if (inside && ends) write_excl(p, y, row, acc);
-    else write_atom(p, y, row, acc);
+    if (o.inside && ends) write_excl(p, y, o.row, o.acc);
+    else write_atom(p, y, o.row, o.acc);
   }
 }
 
@@ -946,6 +929,74 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
     if (lane == 0 && carry_live) {
       // final open segment: the row of the BMW's last element
       bool ends = (tb1 >= p.n_bmt) ? true : (ldm(p.bitmap + tb1 * p.bm_words) & 1u);
+      if (carry_inside && ends) write_excl(p, y, carry_row, carry);
+      else write_atom(p, y, carry_row, carry);
+    }
+  }
+}
+
+// k_nnz_warp, predicated-emit form: each lane scans its BMT with bmt_scan_pe (rows closed
+// inside the BMT stored by one predicated store, no divergent writer calls), then the same
+// warp combine of (cin, cout, head flag) as above.  Same writes as k_nnz_warp.
+template <class V, int WRED, bool PAD, int VEC, int KB, int EM>
+__global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const XGlobal<V> xa{x};
+  for (int64_t w = warp_units(p.n_bmw).begin, w_e = warp_units(p.n_bmw).end; w < w_e; w += blockDim.x >> 5) {
+    const int64_t tb0 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w) : w * p.bmts_per_bmw;
+    const int64_t tb1 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w + 1) : min(tb0 + p.bmts_per_bmw, p.n_bmt);
+    double carry = 0.0;
+    bool carry_inside = false;  // open segment's row started at a head inside this BMW
+    bool carry_live = false;    // an open segment exists (false only before the first element)
+    int64_t carry_row = 0;
+    for (int64_t base = tb0; base < tb1; base += 32) {
+      const int64_t t = base + lane;
+      const bool active = t < tb1;
+      const int nact = (int)min((int64_t)32, tb1 - base);
+      double cin = 0.0, cout = 0.0;
+      bool hh = false, b0 = false;
+      int64_t head_row = 0;  // row of the first head in this lane
+      int64_t last_row = 0;  // row of this lane's last element
+      if (active) {
+        PadPos pp{0, 0};
+        if constexpr (PAD) {
+          if (p.pad_grp_bmw) pp = PadPos{ldm(p.grp_base + w) + (t - tb0) * VEC, (tb1 - tb0) * VEC};
+          else if (p.n_grp == 1) pp = PadPos{t * VEC, p.n_bmt * VEC};
+          else pp = pad_pos<VEC>(p, t);
+        }
+        const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM>(p, y, xa, t, pp);
+        b0 = o.s0;
+        hh = o.inside;
+        const int64_t row0 = ldm(p.bmt_first_row + t);
+        if (!o.s0) {
+          cin = o.inside ? o.first : o.acc;  // continuation of a row begun in an earlier lane
+          head_row = row0 + 1;
+        } else {
+          head_row = row0;
+        }
+        if (hh) cout = o.acc;
+        last_row = o.row;
+      }
+      double v_end, closing;
+      bool inside_end, closing_inside;
+      warp_combine<WRED>(lane, hh, cin, cout, carry, carry_inside, closing, closing_inside, v_end, inside_end);
+      if (active && hh) {
+        // the row closed at this lane's first head; none only when the BMW itself starts
+        // with a head (lane 0 of the first round, element 0 is a row start)
+        const bool exists = !(lane == 0 && !carry_live && b0);
+        if (exists) {
+          if (closing_inside) write_excl(p, y, head_row - 1, closing);
+          else write_atom(p, y, head_row - 1, closing);
+        }
+      }
+      carry = __shfl_sync(0xffffffffu, v_end, nact - 1);
+      carry_inside = __shfl_sync(0xffffffffu, (int)inside_end, nact - 1);
+      carry_row = __shfl_sync(0xffffffffu, last_row, nact - 1);
+      carry_live = true;
+    }
+    if (lane == 0 && carry_live) {
+      // final open segment: the row of the BMW's last element
+      const bool ends = (tb1 >= p.n_bmt) ? true : (ldm(p.bitmap + tb1 * p.bm_words) & 1u);
       if (carry_inside && ends) write_excl(p, y, carry_row, carry);
       else write_atom(p, y, carry_row, carry);
     }
@@ -1449,17 +1500,33 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
 #undef AS_TILE
         break;
       }
+      // predicated-emit form unless fp32 ADD-mode heavy rows need the scratch path, or the
+      // legacy form is forced (variant + 8: AS_NT_LEGACY)
+      const bool pe = p.variant < 8 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
+      const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin;
+      constexpr int KBW = 4;  // fp64 batches of 8 spill 100-180 bytes next to the warp-combine state
+#define AS_NWPE(WR, PADV, VECV)                                                                  \
+  {                                                                                              \
+    if (em0) k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 0><<<g, tpb, 0, s>>>(p, x, y); \
+    else k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 1><<<g, tpb, 0, s>>>(p, x, y);     \
+  }
 #define AS_NW(WR)                                                              \
-  if (!p.pad) k_nnz_warp<V, WR, false, 1><<<g, tpb, 0, s>>>(p, x, y);          \
+  if (pe) {                                                                    \
+    if (!p.pad) AS_NWPE(WR, false, 1)                                          \
+    else if (p.vec == 1) AS_NWPE(WR, true, 1)                                  \
+    else if (p.vec == 2) AS_NWPE(WR, true, 2)                                  \
+    else AS_NWPE(WR, true, 4)                                                  \
+  } else if (!p.pad) k_nnz_warp<V, WR, false, 1><<<g, tpb, 0, s>>>(p, x, y);   \
   else if (p.vec == 1) k_nnz_warp<V, WR, true, 1><<<g, tpb, 0, s>>>(p, x, y);  \
   else if (p.vec == 2) k_nnz_warp<V, WR, true, 2><<<g, tpb, 0, s>>>(p, x, y);  \
   else k_nnz_warp<V, WR, true, 4><<<g, tpb, 0, s>>>(p, x, y);
-      if (p.variant == 1) {
+      if ((p.variant & 7) == 1) {
         AS_NW(1)
       } else {
         AS_NW(2)
       }
 #undef AS_NW
+#undef AS_NWPE
       break;
     }
     case FAM_WARP_ROW:
@@ -1610,7 +1677,7 @@ const char* fam_kernel_name(const DevPart& p) {
   switch (p.fam) {
     case FAM_THREAD_ROW: return p.pad ? "k_thread_row_pad" : "k_thread_row";
     case FAM_NNZ_THREAD: return "k_nnz_thread";
-    case FAM_NNZ_WARP: return p.variant == 1 ? "k_nnz_warp<seg>" : "k_nnz_warp<bitmap>";
+    case FAM_NNZ_WARP: return (p.variant & 7) == 1 ? "k_nnz_warp<seg>" : "k_nnz_warp<bitmap>";
     case FAM_WARP_ROW: return "k_warp_row";
     case FAM_BLOCK_TOTAL: return "k_block_total";
     case FAM_BLOCK_OFFSET: return "k_block_offset";

@@ -470,9 +470,10 @@ void Plan::upload(cudaStream_t s) {
         bytes_model += (double)(nnz * (4 + sv));
       }
     }
-    if (d.fam == FAM_NNZ_THREAD && std::getenv("AS_NT_LEGACY")) d.variant = 9;  // A/B knob: branching form
-    if (d.fam == FAM_NNZ_THREAD)  // L2 bulk prefetch distance in CTA rounds (A/B knob AS_NT_PF)
-      d.pf = std::getenv("AS_NT_PF") ? std::atoi(std::getenv("AS_NT_PF")) : 0;
+    if (std::getenv("AS_NT_LEGACY")) {  // A/B knob: branching forms of the nnz kernels
+      if (d.fam == FAM_NNZ_THREAD) d.variant = 9;
+      if (d.fam == FAM_NNZ_WARP && !d.tile) d.variant += 8;
+    }
     ck((cudaError_t)prepare_part(d), "kernel attributes");
     // name the kernel form actually chosen (as_plan_info.kernels)
     std::string& fn = host.parts[pi].fam_name;
@@ -511,7 +512,9 @@ void Plan::compute_model() {
     ybytes1 += 2 * at * sv;
   }
   double pre = (double)host.prepass.size();
-  double prebytes0 = pre * (4 + sv), prebytes1 = pre * (4 + 2 * sv);
+  // beta == 0: as_spmv fills all of y instead when that moves fewer bytes (api.cpp run_plan)
+  double prebytes0 = (double)m * sv <= pre * (4 + 32) ? (double)m * sv : pre * (4 + sv);
+  double prebytes1 = pre * (4 + 2 * sv);
   info.bytes_model = bytes_model + host.distinct_cols * sv + ybytes0 + (pre ? prebytes0 : 0);
   info.bytes_model_beta = bytes_model + host.distinct_cols * sv + ybytes1 + (pre ? prebytes1 : 0);
   info.bytes_floor = nnz_real * (sv + 4) + host.n * sv + host.m * sv;
