@@ -106,6 +106,7 @@ def load_config(name, int_mode=False):
             "BIN(t=[32,2048]) { COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED"
             " | COMPRESS; BMTB_NNZ_BLOCK(2048); SHMEM_OFFSET_RED; GMEM_ATOM_RED"
             " | COMPRESS; BMTB_ROW_BLOCK(1); BMW_NNZ_BLOCK(2048); WARP_TOTAL_RED; GMEM_ATOM_RED }",
+            "COMPRESS; BMW_NNZ_BLOCK(2048); BMT_NNZ_BLOCK(64); BMT_PAD(BMW,4); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=512,grid=2); GMEM_ATOM_RED",
             "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,1); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
             "COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=256,grid=16); GMEM_ATOM_RED"]
     if name in ("c3s", "c4s", "c5s"):  # shape-preserving 1/4..1/16-scale instances (dev sweeps)
@@ -115,6 +116,8 @@ def load_config(name, int_mode=False):
         return c, c.name + "-scaled", []
     if name == "c5":
         return synth.c5_band_csr(), "band-irreg-64m", [
+            "COMPRESS; BMW_NNZ_BLOCK(2048); BMT_NNZ_BLOCK(64); BMT_PAD(BMW,4); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=1024,grid=2); GMEM_ATOM_RED",
+            "COMPRESS; BMT_NNZ_BLOCK(64); BMT_PAD(GLOBAL,4); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=1024,grid=2,stages=0); GMEM_ATOM_RED",
             "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
             "COMPRESS; BMTB_ROW_BLOCK(256); SORT_BMTB; BMW_ROW_BLOCK(32); BMT_ROW_BLOCK(1); BMT_PAD(BMW); THREAD_TOTAL_RED; GMEM_ATOM_RED",
             "COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL,2); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=512,grid=2,stages=0); GMEM_ATOM_RED"]

@@ -1,6 +1,7 @@
 // C-ABI entry points (include/as.h).  Every call converts internal exceptions to statuses.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -140,7 +141,8 @@ int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s
     // rows.  A listed row costs its 4-byte index plus a scattered 32-byte sector write (ncu,
     // C5: 16.7 M listed rows took 141 us, 418 MB read + 356 MB written), the fill m*sv bytes
     // streamed: fill when it moves fewer bytes
-    if (b == 0.0 && (double)P.m * sv <= (double)P.n_prepass * (4 + 32))
+    static const int mode = std::getenv("AS_PREPASS") ? std::atoi(std::getenv("AS_PREPASS")) : 0;  // A/B: 1 list, 2 fill
+    if (b == 0.0 && (mode == 2 || (mode == 0 && (double)P.m * sv <= (double)P.n_prepass * (4 + 32))))
       err = (int)cudaMemsetAsync(y, 0, (size_t)P.m * sv, s);
     else
       err = launch_prepass(P.d_prepass, P.n_prepass, b, y, P.dt == AS_R64F ? 1 : 0, s);
