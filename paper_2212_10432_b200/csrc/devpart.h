@@ -94,6 +94,7 @@ struct DevPart {
   // CUDA IPC mappings), fusing the exchange into the SpMV epilogue
   void* peer_y[kMaxFusedPeers] = {nullptr};
   int n_peer = 0;
+  int pipe = 0;  // nnz kernels, predicated-emit form: one batch of load look-ahead
   // launch
   int tpb = 256, grid = 0;
   size_t smem = 0;

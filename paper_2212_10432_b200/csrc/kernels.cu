@@ -527,12 +527,10 @@ __device__ __forceinline__ void emit_excl(const DevPart& p, V* y, bool pred, int
   }
 }
 
-template <class V, bool PAD, int VEC, int KB, int EM, bool FULL, class XA>
-__device__ __forceinline__ void bmt_batch_pe(const DevPart& p, V* y, XA xa, const uint32_t* bm, const V* pv,
-                                             const int32_t* pc, int64_t stride, int j0, int len, int32_t& row,
-                                             double& acc, bool& inside, double& first) {
-  double v[KB];
-  int32_t c[KB];
+// Loads of one batch (values, columns) ...
+template <class V, bool PAD, int VEC, int KB, bool FULL>
+__device__ __forceinline__ void batch_load(const V* pv, const int32_t* pc, int64_t stride, int j0, int len, double* v,
+                                           int32_t* c) {
   if constexpr (PAD) {
 #pragma unroll
     for (int q = 0; q < KB; q += VEC) {
@@ -558,6 +556,13 @@ __device__ __forceinline__ void bmt_batch_pe(const DevPart& p, V* y, XA xa, cons
       }
     }
   }
+}
+
+// ... and their use: x gathers, then the branch-free bitmap-segmented accumulation.
+template <class V, int KB, int EM, bool FULL, class XA>
+__device__ __forceinline__ void batch_use(const DevPart& p, V* y, XA xa, const uint32_t* bm, int j0, int len,
+                                          const double* v, const int32_t* c, int32_t& row, double& acc, bool& inside,
+                                          double& first) {
   double xv[KB];
 #pragma unroll
   for (int q = 0; q < KB; ++q) xv[q] = (FULL || j0 + q < len) ? xa(c[q]) : 0.0;
@@ -582,7 +587,7 @@ struct ScanPE {
   int32_t row;
   bool s0, inside;
 };
-template <class V, bool PAD, int VEC, int KB, int EM, class XA>
+template <class V, bool PAD, int VEC, int KB, int EM, bool PIPE, class XA>
 __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int64_t t, PadPos pp) {
   static_assert(32 % KB == 0 && KB % VEC == 0, "KB divides 32 and is a multiple of VEC");
   const int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
@@ -601,21 +606,47 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   int j0 = 0;
   // pv / pc advance to the batch's first element (slot-major: KB/VEC chunk rows per batch)
   const int64_t adv = PAD ? (KB / VEC) * pp.stride : KB;
-  for (; j0 < full; j0 += KB, pv += adv, pc += adv)
-    bmt_batch_pe<V, PAD, VEC, KB, EM, true>(p, y, xa, bm, pv, pc, pp.stride, j0, len, o.row, o.acc, o.inside, o.first);
-  if (j0 < len)
-    bmt_batch_pe<V, PAD, VEC, KB, EM, false>(p, y, xa, bm, pv, pc, pp.stride, j0, len, o.row, o.acc, o.inside, o.first);
+  double v[KB];
+  int32_t c[KB];
+  if constexpr (PIPE) {
+    // one batch of look-ahead: the next batch's value/column loads are issued before this
+    // batch's x gathers, so the HBM stream overlaps the gather latency
+    if (full > 0) batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, 0, len, v, c);
+    for (; j0 < full; j0 += KB) {
+      double vn[KB];
+      int32_t cn[KB];
+      const bool more = j0 + KB < full;
+      if (more) batch_load<V, PAD, VEC, KB, true>(pv + adv, pc + adv, pp.stride, j0 + KB, len, vn, cn);
+      batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
+      pv += adv;
+      pc += adv;
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        v[q] = vn[q];
+        c[q] = cn[q];
+      }
+    }
+  } else {
+    for (; j0 < full; j0 += KB, pv += adv, pc += adv) {
+      batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, j0, len, v, c);
+      batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
+    }
+  }
+  if (j0 < len) {
+    batch_load<V, PAD, VEC, KB, false>(pv, pc, pp.stride, j0, len, v, c);
+    batch_use<V, KB, EM, false>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
+  }
   return o;
 }
 
-template <class V, bool PAD, int VEC, int KB, int EM>
+template <class V, bool PAD, int VEC, int KB, int EM, bool PIPE>
 __global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const XGlobal<V> xa{x};
   const Units u = thread_units(p.n_bmt);
   for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x) {
     PadPos pp{0, 0};
     if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
-    const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM>(p, y, xa, t, pp);
+    const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM, PIPE>(p, y, xa, t, pp);
     // first segment closed inside the BMT but begun before it: straddler
     if (!o.s0 && o.inside) write_atom(p, y, ldm(p.bmt_first_row + t), o.first);
     // open last segment: exclusive iff it began at a head here and the next BMT starts a row
@@ -938,7 +969,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
 // k_nnz_warp, predicated-emit form: each lane scans its BMT with bmt_scan_pe (rows closed
 // inside the BMT stored by one predicated store, no divergent writer calls), then the same
 // warp combine of (cin, cout, head flag) as above.  Same writes as k_nnz_warp.
-template <class V, int WRED, bool PAD, int VEC, int KB, int EM>
+template <class V, int WRED, bool PAD, int VEC, int KB, int EM, bool PIPE>
 __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const XGlobal<V> xa{x};
@@ -964,7 +995,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __rest
           else if (p.n_grp == 1) pp = PadPos{t * VEC, p.n_bmt * VEC};
           else pp = pad_pos<VEC>(p, t);
         }
-        const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM>(p, y, xa, t, pp);
+        const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM, PIPE>(p, y, xa, t, pp);
         b0 = o.s0;
         hh = o.inside;
         const int64_t row0 = ldm(p.bmt_first_row + t);
@@ -1463,12 +1494,16 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       // timing (variant 9)
       const bool pe = p.variant != 9 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
       const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin;
+      const bool pipe = p.pipe;
 #define AS_NT(PADV, VECV)                                                                                 \
   {                                                                                                       \
     constexpr int KBV = sizeof(V) == 4 && VECV <= 4 ? 4 : 8;                                              \
+    constexpr int KBP = VECV > 4 ? VECV : 4;                                                              \
     if (!pe) k_nnz_thread<V, PADV, VECV, KBV><<<g, tt, 0, s>>>(p, x, y);                                  \
-    else if (em0) k_nnz_thread_pe<V, PADV, VECV, KBV, 0><<<g, tt, 0, s>>>(p, x, y);                       \
-    else k_nnz_thread_pe<V, PADV, VECV, KBV, 1><<<g, tt, 0, s>>>(p, x, y);                                \
+    else if (pipe && em0) k_nnz_thread_pe<V, PADV, VECV, KBP, 0, true><<<g, tt, 0, s>>>(p, x, y);         \
+    else if (pipe) k_nnz_thread_pe<V, PADV, VECV, KBP, 1, true><<<g, tt, 0, s>>>(p, x, y);                \
+    else if (em0) k_nnz_thread_pe<V, PADV, VECV, KBV, 0, false><<<g, tt, 0, s>>>(p, x, y);                \
+    else k_nnz_thread_pe<V, PADV, VECV, KBV, 1, false><<<g, tt, 0, s>>>(p, x, y);                         \
   }
       if (!p.pad) {
         AS_NT(false, 1)
@@ -1507,8 +1542,8 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       constexpr int KBW = 4;  // fp64 batches of 8 spill 100-180 bytes next to the warp-combine state
 #define AS_NWPE(WR, PADV, VECV)                                                                  \
   {                                                                                              \
-    if (em0) k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 0><<<g, tpb, 0, s>>>(p, x, y); \
-    else k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 1><<<g, tpb, 0, s>>>(p, x, y);     \
+    if (em0) k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 0, false><<<g, tpb, 0, s>>>(p, x, y); \
+    else k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 1, false><<<g, tpb, 0, s>>>(p, x, y);     \
   }
 #define AS_NW(WR)                                                              \
   if (pe) {                                                                    \
