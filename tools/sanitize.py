@@ -20,6 +20,8 @@ EXTRA = [
     "DENSE_DECOM(b=64,theta=0.3) { DENSE | COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED }",
     "COMPRESS; BMTB_NNZ_BLOCK(100); SHMEM_OFFSET_RED; SET_RESOURCE(tpb=128,grid=0,stages=2); GMEM_ATOM_RED",
     "COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL,2); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=1024); GMEM_ATOM_RED",
+    "COMPRESS; BMW_NNZ_BLOCK(2048); BMT_NNZ_BLOCK(64); BMT_PAD(BMW,4); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=1024,grid=2); GMEM_ATOM_RED",
+    "COMPRESS; BMT_NNZ_BLOCK(64); BMT_PAD(GLOBAL,4); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=1024,grid=2,stages=0); GMEM_ATOM_RED",
 ]
 
 
@@ -30,19 +32,20 @@ def main():
     for coo, graphs in cases:
         A = asp.Matrix.from_coo(coo.m, coo.n, coo.row, coo.col, coo.val)
         x, y0 = synth.vectors(coo.n, coo.m, 1)
-        yref, bnd = S.spmv_coo(coo.m, coo.row, coo.col, coo.val, x, 1.5, -0.5, y0)
-        for g in graphs:
-            try:
-                P = asp.Plan(A, g, device=0)
-            except asp.AsError as e:
-                print("infeasible", g[:60], e)
-                continue
-            dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y0.copy()).cuda()
-            P.spmv(1.5, dx, -0.5, dy)
-            torch.cuda.synchronize()
-            ok, ratio = S.check(dy.cpu().numpy(), yref, bnd, np.float64)
-            fails += not ok
-            print("ok " if ok else "BAD", P.info()["kernels"], g[:70])
+        for alpha, beta in ((1.5, -0.5), (1.0, 0.0)):  # generic and STORE/beta=0 epilogues
+            yref, bnd = S.spmv_coo(coo.m, coo.row, coo.col, coo.val, x, alpha, beta, y0)
+            for g in graphs:
+                try:
+                    P = asp.Plan(A, g, device=0)
+                except asp.AsError as e:
+                    print("infeasible", g[:60], e)
+                    continue
+                dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y0.copy()).cuda()
+                P.spmv(alpha, dx, beta, dy)
+                torch.cuda.synchronize()
+                ok, ratio = S.check(dy.cpu().numpy(), yref, bnd, np.float64)
+                fails += not ok
+                print("ok " if ok else "BAD", beta, P.info()["kernels"], g[:70])
     print("failures:", fails)
     sys.exit(1 if fails else 0)
 
