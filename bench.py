@@ -206,10 +206,11 @@ def main():
     ap.add_argument("--search-candidates", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--exchange", default="none", choices=["none", "allgather", "halo", "nccl", "peer"],
+    ap.add_argument("--exchange", default="none", choices=["none", "allgather", "halo", "nccl", "peer", "peer_halo"],
                     help="y -> next x exchange after the SpMV (N > 1), timed separately: allgather/halo "
                          "over torch.distributed; nccl/peer = as_spmv_dist (C-ABI: SpMV + AllGatherV, or "
-                         "SpMV + peer-memory push), timed as whole steps")
+                         "SpMV + peer-memory push; peer_halo: only the rows each peer's band reads), "
+                         "timed as whole steps")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no search/baseline/e2e)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1 on c2: weak = the Laplacian grows to 2048 x 2048N and each rank owns one "
@@ -315,15 +316,18 @@ def main():
             e1.record(stream)
         torch.cuda.synchronize()
         gather_ms = None
-        if args.exchange in ("nccl", "peer") and dist:
+        if args.exchange in ("nccl", "peer", "peer_halo") and dist:
             # as_spmv_dist: band SpMV into y_full + the exchange inside the library
             from paper_2212_10432_b200 import dist as D
             d = D.init_dist(rank, world, local, cuts, nccl=args.exchange == "nccl")
             y_full = torch.zeros(m_global, dtype=dy.dtype, device="cuda")
-            if args.exchange == "peer":
+            kind = "peer" if args.exchange == "peer_halo" else args.exchange
+            if kind == "peer":
                 D.register_peers(d, y_full)
+            if args.exchange == "peer_halo":
+                d.set_windows(D.gather_spans(A.col_span()))
             for _ in range(3):
-                d.spmv(P, 1.0, dx, 0.0, y_full, args.exchange, stream)
+                d.spmv(P, 1.0, dx, 0.0, y_full, kind, stream)
             torch.cuda.synchronize()
             dist.barrier()
             gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -332,7 +336,7 @@ def main():
                 if not args.no_flush:
                     flush_l2()
                 g0.record(stream)
-                d.spmv(P, 1.0, dx, 0.0, y_full, args.exchange, stream)
+                d.spmv(P, 1.0, dx, 0.0, y_full, kind, stream)
                 g1.record(stream)
             torch.cuda.synchronize()
             d.check()
@@ -452,7 +456,7 @@ def main():
     }
     if gather_ms is not None:
         line["exchange"] = {"kind": args.exchange, "ms": gather_ms,
-                            "timed": "spmv + exchange per step (as_spmv_dist)" if args.exchange in ("nccl", "peer")
+                            "timed": "spmv + exchange per step (as_spmv_dist)" if args.exchange in ("nccl", "peer", "peer_halo")
                             else "exchange only"}
     if not args.no_cpu_baseline and not args.profile and world == 1:
         line["cpu_baseline"] = cpu_baseline(coo, wl)

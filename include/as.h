@@ -241,6 +241,12 @@ as_status_t as_dist_set_cuts(as_dist_t, const int64_t* cuts);
  * by the caller (any transport), in rank order, then passed to as_dist_open_peers. */
 as_status_t as_dist_ipc_handle(as_dist_t, void* y_full, void* handle);
 as_status_t as_dist_open_peers(as_dist_t, void* y_full, const void* handles /* world x HANDLE_BYTES */);
+/* Halo windows (NEXT-1(ii), banded matrices): lo_hi[2q], lo_hi[2q+1] = first and last row of
+ * y_full rank q reads (its band's column span, as_matrix_col_span; last < first = none).
+ * Afterwards AS_EXCH_PEER sends each peer only the rows of this band inside its window
+ * (fused or pushed), instead of the whole band; the flags are still released to every peer.
+ * Every rank must install the same table.  lo_hi == NULL restores full bands. */
+as_status_t as_dist_set_windows(as_dist_t, const int64_t* lo_hi /* world x 2 */);
 as_status_t as_spmv_dist(as_dist_t, as_plan_t local, const void* alpha, const void* x_full,
                          const void* beta, void* y_full, int exchange, void* stream);
 /* Device-side status of the peer exchange (AS_ERR_CUDA after a wait timeout); synchronizes

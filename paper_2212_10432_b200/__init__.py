@@ -98,6 +98,7 @@ _sig("as_dist_init", [_i32, _i32, _vp, _i32, _P(_vp)])
 _sig("as_dist_set_cuts", [_vp, _vp])
 _sig("as_dist_ipc_handle", [_vp, _vp, _vp])
 _sig("as_dist_open_peers", [_vp, _vp, _vp])
+_sig("as_dist_set_windows", [_vp, _vp])
 _sig("as_spmv_dist", [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp])
 _sig("as_dist_check", [_vp])
 _sig("as_dist_destroy", [_vp], None)
@@ -108,7 +109,7 @@ EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create
             "as_plan_keys", "as_plan_destroy", "as_spmv", "as_spmv_host", "as_search", "as_random_graph",
             "as_dist_row_cuts", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
             "as_dist_set_cuts", "as_dist_ipc_handle", "as_dist_open_peers", "as_spmv_dist", "as_dist_check",
-            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict"]
+            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows"]
 
 
 class AsError(RuntimeError):
@@ -423,6 +424,14 @@ class Dist:
             raise AsError(1, "one handle per rank expected")
         buf = ctypes.create_string_buffer(blob, len(blob))
         _ck(_lib.as_dist_open_peers(self._h, _ptr(y_full), buf))
+
+    def set_windows(self, spans):
+        """Halo windows: spans[q] = (first, last) row of y_full rank q reads (None: full bands)."""
+        if spans is None:
+            _ck(_lib.as_dist_set_windows(self._h, None))
+            return
+        w = np.ascontiguousarray(np.asarray(spans, np.int64).reshape(self.world, 2))
+        _ck(_lib.as_dist_set_windows(self._h, w.ctypes.data))
 
     def spmv(self, plan: Plan, alpha, x_full, beta, y_full, exchange: str = "none", stream=None):
         a, b = plan._scalars(alpha, beta)

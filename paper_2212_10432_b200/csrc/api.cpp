@@ -133,7 +133,8 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
 // launch i is enqueued, after(i) after it (as_spmv_host hooks its copy pipeline there).
 template <class Before, class After>
 int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s, Before before, After after,
-             void* const* peer_y = nullptr, int n_peers = 0) {
+             void* const* peer_y = nullptr, const int64_t* peer_lo = nullptr, const int64_t* peer_hi = nullptr,
+             int n_peers = 0) {
   const size_t sv = P.dt == AS_R64F ? 8 : 4;
   int err = 0;
   if (P.n_prepass) {
@@ -154,7 +155,11 @@ int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s
     d.alpha = a;
     d.beta = b;
     d.n_peer = n_peers;
-    for (int q = 0; q < n_peers; ++q) d.peer_y[q] = peer_y[q];
+    for (int q = 0; q < n_peers; ++q) {
+      d.peer_y[q] = peer_y[q];
+      d.peer_lo[q] = peer_lo[q];
+      d.peer_hi[q] = peer_hi[q];
+    }
     err = launch_part(d, x, y, s);
     if (!err) after(i);
   }
@@ -163,9 +168,10 @@ int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s
 }
 
 int run_plan_peers(Plan& P, const void* x, void* y, double alpha, double beta, void* stream, void* const* peer_y,
-                   int n_peers) {
+                   const int64_t* peer_lo, const int64_t* peer_hi, int n_peers) {
   if (n_peers > kMaxFusedPeers || (n_peers > 0 && !P.single_writer)) return (int)cudaErrorInvalidValue;
-  return run_plan(P, x, y, alpha, beta, (cudaStream_t)stream, [](size_t) {}, [](size_t) {}, peer_y, n_peers);
+  return run_plan(P, x, y, alpha, beta, (cudaStream_t)stream, [](size_t) {}, [](size_t) {}, peer_y, peer_lo, peer_hi,
+                  n_peers);
 }
 
 }  // namespace as

@@ -93,6 +93,7 @@ struct DevPart {
   // also written to the same offset of each peer's y_full band (P2P stores over NVLink into
   // CUDA IPC mappings), fusing the exchange into the SpMV epilogue
   void* peer_y[kMaxFusedPeers] = {nullptr};
+  int64_t peer_lo[kMaxFusedPeers] = {0}, peer_hi[kMaxFusedPeers] = {0};  // plan rows [lo, hi) peer i reads
   int n_peer = 0;
   int pipe = 0;  // nnz kernels, predicated-emit form: one batch of load look-ahead
   // launch
@@ -118,10 +119,13 @@ constexpr int kMaxPeers = 64;  // AS_DIST_MAX_WORLD
 struct PeerPush {
   void* dst[kMaxPeers];                 // peer y_full + band offset (IPC mappings)
   unsigned long long* flag[kMaxPeers];  // peer flag arrays (IPC mappings)
+  int64_t lo[kMaxPeers], hi[kMaxPeers]; // bytes [lo, hi) of the band peer p receives (its halo window)
   int n = 0;
 };
-int launch_push(const void* src, int64_t bytes, const PeerPush& pp, unsigned* ctr, unsigned* target,
-                unsigned long long epoch, int rank, void* stream);
+// Push bytes [pp.lo[p], pp.hi[p]) of src to every pp.dst[p] (empty ranges: flags only), then
+// release the epoch into every peer's flag array.
+int launch_push(const void* src, PeerPush pp, unsigned* ctr, unsigned* target, unsigned long long epoch, int rank,
+                void* stream);
 int launch_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch,
                 unsigned long long timeout_ns, int* status, void* stream);
 

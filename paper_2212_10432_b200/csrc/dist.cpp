@@ -100,6 +100,7 @@ struct as_dist_s {
   std::map<std::string, char*> opened;             // IPC handle bytes -> mapped base (opened once)
   std::vector<unsigned long long*> peer_flags;     // [world], NULL for self / unopened
   std::map<void*, std::vector<char*>> peer_y;      // local y_full -> peers' y_full mappings
+  std::vector<int64_t> win;                        // [2*world]: rows [lo, hi] of y_full rank q reads; empty = all
 };
 
 extern "C" {
@@ -163,6 +164,17 @@ as_status_t as_dist_set_cuts(as_dist_t D, const int64_t* cuts) {
     for (int r = 0; r < D->world; ++r)
       if (cuts[r + 1] < cuts[r]) fail(AS_ERR_INVALID_ARG, "cuts must be non-decreasing");
     D->cuts.assign(cuts, cuts + D->world + 1);
+  });
+}
+
+as_status_t as_dist_set_windows(as_dist_t D, const int64_t* lo_hi) {
+  return guard([&] {
+    if (!D) fail(AS_ERR_INVALID_ARG, "NULL dist");
+    if (!lo_hi) {
+      D->win.clear();
+      return;
+    }
+    D->win.assign(lo_hi, lo_hi + 2 * (size_t)D->world);
   });
 }
 
@@ -256,18 +268,32 @@ as_status_t as_spmv_dist(as_dist_t D, as_plan_t local, const void* alpha, const 
     // y_full directly from the SpMV epilogue; the push kernel then only signals (0 bytes)
     const bool fused = exchange == AS_EXCH_PEER && P.single_writer && D->world - 1 <= kMaxFusedPeers &&
                        !std::getenv("AS_DIST_NO_FUSE");
+    // rows [a, b) of this band peer q receives: all of it, or its halo window
+    auto window = [&](int q, int64_t& a, int64_t& b) {
+      a = 0;
+      b = r1 - r0;
+      if (D->win.empty()) return;
+      a = std::max<int64_t>(0, D->win[2 * q] - r0);
+      b = std::min<int64_t>(r1 - r0, D->win[2 * q + 1] + 1 - r0);
+      if (b < a) b = a;
+    };
     if (fused && P.m > 0) {
       void* pys[kMaxFusedPeers];
+      int64_t plo[kMaxFusedPeers], phi[kMaxFusedPeers];
       int np = 0;
-      for (int q = 0; q < D->world; ++q)
-        if (q != r) pys[np++] = (*peers)[q] + r0 * sv;
+      for (int q = 0; q < D->world; ++q) {
+        if (q == r) continue;
+        window(q, plo[np], phi[np]);
+        if (phi[np] <= plo[np]) continue;  // peer reads none of this band
+        pys[np++] = (*peers)[q] + r0 * sv;
+      }
       const double a = P.dt == AS_R64F ? *(const double*)alpha : (double)*(const float*)alpha;
       const double b = P.dt == AS_R64F ? *(const double*)beta : (double)*(const float*)beta;
       int cur0 = 0;
       cudaGetDevice(&cur0);
       cudaSetDevice(D->device);
       cudaError_t prior = cudaGetLastError();
-      int e = prior != cudaSuccess ? (int)prior : run_plan_peers(P, x_full, band, a, b, stream, pys, np);
+      int e = prior != cudaSuccess ? (int)prior : run_plan_peers(P, x_full, band, a, b, stream, pys, plo, phi, np);
       cudaSetDevice(cur0);
       if (e) fail(AS_ERR_CUDA, std::string("fused band SpMV: ") + cudaGetErrorString((cudaError_t)e));
     } else if (P.m > 0) {
@@ -296,12 +322,16 @@ as_status_t as_spmv_dist(as_dist_t D, as_plan_t local, const void* alpha, const 
     PeerPush pp;
     for (int q = 0; q < D->world; ++q) {
       if (q == r) continue;
+      int64_t a = 0, b = 0;
+      if (!fused) window(q, a, b);  // fused: the SpMV already stored the rows, flags only
       pp.dst[pp.n] = (*peers)[q] + r0 * sv;
       pp.flag[pp.n] = D->peer_flags[q];
+      pp.lo[pp.n] = a * (int64_t)sv;
+      pp.hi[pp.n] = b * (int64_t)sv;
       ++pp.n;
     }
     ++D->epoch;
-    err = launch_push(band, fused ? 0 : (r1 - r0) * (int64_t)sv, pp, D->ctr, &D->target, D->epoch, r, stream);
+    err = launch_push(band, pp, D->ctr, &D->target, D->epoch, r, stream);
     if (!err) err = launch_wait(D->flags, D->world, r, D->epoch, AS_DIST_WAIT_TIMEOUT_NS, D->status, stream);
     cudaSetDevice(cur);
     if (err) fail(AS_ERR_CUDA, std::string("peer exchange: ") + cudaGetErrorString((cudaError_t)err));

@@ -1,6 +1,7 @@
 // Peer-memory exchange of the ROW_DIV multi-GPU path (as_spmv_dist, AS_EXCH_PEER).
 //
-// After the band SpMV, ONE kernel streams this rank's y band into every peer's y_full over
+// After the band SpMV, ONE kernel streams this rank's y band (or, with halo windows, only the
+// rows each peer reads) into every peer's y_full over
 // NVLink (P2P stores into CUDA IPC mappings of the peers' buffers) and, once every CTA's
 // stores are fenced at system scope, the last CTA publishes the call's epoch into each
 // peer's flag array with a release store.  Each rank's stream then runs a one-CTA wait
@@ -32,14 +33,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 template <class E>
-__global__ void __launch_bounds__(512) k_push(const E* __restrict__ src, int64_t cnt, PeerPush pp, unsigned* ctr,
-                                              unsigned target, unsigned long long epoch, int rank) {
+__global__ void __launch_bounds__(512) k_push(const E* __restrict__ src, PeerPush pp, unsigned* ctr, unsigned target,
+                                              unsigned long long epoch, int rank) {
+  // pp.lo / pp.hi in elements of E here (converted by launch_push)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
-    const E v = src[i];
-#pragma unroll 4
-    for (int p = 0; p < pp.n; ++p) ((E*)pp.dst[p])[i] = v;
-  }
+  for (int p = 0; p < pp.n; ++p)
+    for (int64_t i = pp.lo[p] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pp.hi[p]; i += stride)
+      ((E*)pp.dst[p])[i] = src[i];
   __threadfence_system();  // this thread's peer stores before the CTA's arrival
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -68,22 +68,33 @@ __global__ void k_wait(const unsigned long long* flags, int world, int rank, uns
 
 }  // namespace
 
-int launch_push(const void* src, int64_t bytes, const PeerPush& pp, unsigned* ctr, unsigned* target,
-                unsigned long long epoch, int rank, void* stream) {
-  // widest element all addresses and the byte count are aligned to
-  uintptr_t a = (uintptr_t)src | (uintptr_t)bytes;
-  for (int p = 0; p < pp.n; ++p) a |= (uintptr_t)pp.dst[p];
+int launch_push(const void* src, PeerPush pp, unsigned* ctr, unsigned* target, unsigned long long epoch, int rank,
+                void* stream) {
+  // widest element every address and range bound is aligned to
+  uintptr_t a = (uintptr_t)src;
+  int64_t most = 0;
+  for (int p = 0; p < pp.n; ++p) {
+    a |= (uintptr_t)pp.dst[p];
+    if (pp.hi[p] > pp.lo[p]) {
+      a |= (uintptr_t)pp.lo[p] | (uintptr_t)pp.hi[p];
+      most = std::max(most, pp.hi[p] - pp.lo[p]);
+    }
+  }
   const int esz = (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : 4;
-  const int64_t cnt = bytes / esz;
+  for (int p = 0; p < pp.n; ++p) {
+    pp.lo[p] /= esz;
+    pp.hi[p] = pp.hi[p] > pp.lo[p] * esz ? pp.hi[p] / esz : pp.lo[p];
+  }
+  const int64_t cnt = most / esz;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t g = std::max<int64_t>(1, std::min<int64_t>((cnt + 511) / 512, (int64_t)sms * 2));
   *target += (unsigned)g;
   cudaStream_t s = (cudaStream_t)stream;
-  if (esz == 16) k_push<uint4><<<g, 512, 0, s>>>((const uint4*)src, cnt, pp, ctr, *target, epoch, rank);
-  else if (esz == 8) k_push<uint64_t><<<g, 512, 0, s>>>((const uint64_t*)src, cnt, pp, ctr, *target, epoch, rank);
-  else k_push<uint32_t><<<g, 512, 0, s>>>((const uint32_t*)src, cnt, pp, ctr, *target, epoch, rank);
+  if (esz == 16) k_push<uint4><<<g, 512, 0, s>>>((const uint4*)src, pp, ctr, *target, epoch, rank);
+  else if (esz == 8) k_push<uint64_t><<<g, 512, 0, s>>>((const uint64_t*)src, pp, ctr, *target, epoch, rank);
+  else k_push<uint32_t><<<g, 512, 0, s>>>((const uint32_t*)src, pp, ctr, *target, epoch, rank);
   return (int)cudaGetLastError();
 }
 

@@ -116,7 +116,8 @@ __device__ __forceinline__ int64_t heavy_slot(const DevPart& p, int64_t g) {
 template <class V>
 __device__ __forceinline__ void peer_store(const DevPart& p, int64_t g, V v) {
 #pragma unroll 1
-  for (int i = 0; i < p.n_peer; ++i) ((V*)p.peer_y[i])[g] = v;
+  for (int i = 0; i < p.n_peer; ++i)
+    if (g >= p.peer_lo[i] && g < p.peer_hi[i]) ((V*)p.peer_y[i])[g] = v;  // peer i's halo window
 }
 
 template <class V>

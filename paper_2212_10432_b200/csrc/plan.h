@@ -51,9 +51,10 @@ struct Plan {
 };
 
 // Enqueue one SpMV of the plan on `stream` (pre-pass, parts, epilogue); with n_peers > 0
-// every part's final STOREs also go to peer_y[i] (+ the row offset).  Returns cudaError_t.
+// every part's final STORE of a row in [peer_lo[i], peer_hi[i]) also goes to peer_y[i]
+// (+ the row offset).  Returns cudaError_t.
 int run_plan_peers(Plan& P, const void* x, void* y, double alpha, double beta, void* stream, void* const* peer_y,
-                   int n_peers);
+                   const int64_t* peer_lo, const int64_t* peer_hi, int n_peers);
 
 }  // namespace as
 

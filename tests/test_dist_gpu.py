@@ -75,7 +75,7 @@ PEER_GRAPHS = {
 }
 
 
-def _peer_worker(rank, world, port, iters, q, graph="push", no_fuse=False):
+def _peer_worker(rank, world, port, iters, q, graph="push", no_fuse=False, halo=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -94,13 +94,16 @@ def _peer_worker(rank, world, port, iters, q, graph="push", no_fuse=False):
         P = asp.Plan(Ab, PEER_GRAPHS[graph], device=0)
         assert P.info()["single_writer"] == (graph != "push"), P.info()
         d = D.init_dist(rank, world, 0, cuts, nccl=False)
+        span = Ab.col_span()
+        if halo:  # each peer receives only the rows of this band inside its column span
+            d.set_windows(D.gather_spans(span))
         Y = [torch.from_numpy(x).cuda(), torch.full((c.m,), float("nan"), dtype=torch.float64, device="cuda")]
         for y in Y:
             D.register_peers(d, y)
         for k in range(iters):                                   # ping-pong: x_{k+1} = A x_k
             d.spmv(P, 1.0, Y[k % 2], 0.0, Y[(k + 1) % 2], "peer")
         d.check()
-        q.put((rank, Y[iters % 2].cpu().numpy().copy(), None))
+        q.put((rank, (Y[iters % 2].cpu().numpy().copy(), span, (r0, r1)), None))
         dist.barrier()
         d.close()
         dist.destroy_process_group()
@@ -108,18 +111,22 @@ def _peer_worker(rank, world, port, iters, q, graph="push", no_fuse=False):
         q.put((rank, None, repr(e)))
 
 
-@pytest.mark.parametrize("world,graph,no_fuse", [(2, "push", False), (3, "push", False), (2, "fused", False),
-                                                (3, "fused", False), (3, "fused_warp", False),
-                                                (2, "fused", True)])
-def test_dist_peer_push_multiprocess(world, graph, no_fuse):
+@pytest.mark.parametrize("world,graph,no_fuse,halo", [(2, "push", False, False), (3, "push", False, False),
+                                                     (2, "fused", False, False), (3, "fused", False, False),
+                                                     (3, "fused_warp", False, False), (2, "fused", True, False),
+                                                     (3, "push", False, True), (3, "fused", False, True),
+                                                     (2, "fused_warp", False, True)])
+def test_dist_peer_push_multiprocess(world, graph, no_fuse, halo):
     """x_{k+1} = A x_k over peer memory: separate push kernel, or (single-writer plans) peer
-    stores fused into the SpMV epilogue; bit-identical to the oracle on every rank."""
+    stores fused into the SpMV epilogue; with halo windows each rank receives only the rows
+    its band reads.  Bit-identical to the oracle on every row a rank owns or reads."""
     import torch.multiprocessing as mp
     iters = 3
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, iters, q, graph, no_fuse)) for r in range(world)]
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, iters, q, graph, no_fuse, halo))
+             for r in range(world)]
     for p in procs:
         p.start()
     try:
@@ -131,9 +138,18 @@ def test_dist_peer_push_multiprocess(world, graph, no_fuse):
                 p.kill()
     c, x = _band_case()
     ref = _oracle_power(c, x, iters)
-    for rank, y, err in res:
+    for rank, out, err in res:
         assert err is None, (rank, err)
-        assert np.array_equal(y, ref), (rank, np.nonzero(y != ref)[0][:10])
+        y, (lo, hi), (r0, r1) = out
+        if halo:  # rows outside the band and the window are never sent: compare the rest
+            keep = np.zeros(c.m, bool)
+            keep[r0:r1] = True
+            keep[lo:hi + 1] = True
+            assert 0 < keep.sum() < c.m
+            y, ref_r = y[keep], ref[keep]
+        else:
+            ref_r = ref
+        assert np.array_equal(y, ref_r), (rank, np.nonzero(y != ref_r)[0][:10])
 
 
 def test_torch_allocator_hooks():
