@@ -70,6 +70,8 @@ typedef struct {
   char kernels[512]; /* ';'-separated kernel names in launch order */
   int single_writer;  /* every row's final value comes from exactly one STORE: as_spmv_dist
                          with AS_EXCH_PEER fuses the peer stores into the SpMV epilogue */
+  int modeled_arrays; /* index arrays replaced by fitted models (Model-Driven Format
+                         Compression): computed in the kernel instead of loaded */
 } as_plan_info_t;
 
 const char* as_last_error(void);
@@ -166,6 +168,16 @@ typedef struct {
 } as_search_cfg_t;
 as_status_t as_search(as_matrix_t, const as_search_cfg_t*, int device, void* stream,
                       as_plan_t* best, char* best_graph, size_t* len);
+/* Model-Driven Format Compression (§V-D): fit an index array a[n] (n >= 2) to
+ * model(i) = b + k1*(i / w) + k2*(i % w) -- linear (w = 1), periodic linear (w = 2..256,
+ * powers of two), step (k2 = 0, w = first run length) -- with at most `budget` (<= 8)
+ * patches; fewest patches wins, linear before periodic before step on ties.
+ * out[6 + 2*budget] = {kind (1 linear, 2 periodic, 3 step), b, k1, k2, w, n_patches,
+ * (index, value) x n_patches}.  No model within the budget -> AS_ERR_NOT_FOUND.  as_plan
+ * applies it to origin_rows and the NNZ-BMT first rows (as_plan_info_t.modeled_arrays;
+ * AS_NO_MDC in the environment disables it). */
+as_status_t as_fit_array_model(const int64_t* a, size_t n, int budget, int64_t* out);
+
 /* The search's cost model (NEXT-3; the paper's learned performance model of P:369 step 3,
  * P:371-377).  as_graph_features: fixed-length feature vector of a graph -- per operator
  * the occurrence count over all branches (24: ROW_DIV ... SHMEM_OFFSET_RED, SET_RESOURCE),

@@ -48,7 +48,8 @@ class AsPlanInfo(ctypes.Structure):
     _fields_ = [("nnz_real", _i64), ("stored_slots", _i64), ("pads", _i64), ("n_parts", _i64),
                 ("n_launches", _i64), ("prepass_rows", _i64), ("bytes_model", ctypes.c_double),
                 ("bytes_model_beta", ctypes.c_double), ("bytes_floor", ctypes.c_double),
-                ("kernels", ctypes.c_char * 512), ("single_writer", ctypes.c_int)]
+                ("kernels", ctypes.c_char * 512), ("single_writer", ctypes.c_int),
+                ("modeled_arrays", ctypes.c_int)]
 
 
 class AsSearchCfg(ctypes.Structure):
@@ -87,6 +88,7 @@ _sig("as_spmv_host", [_vp, _vp, _vp, _vp, _vp, _vp])
 _sig("as_search", [_vp, _P(AsSearchCfg), _i32, _vp, _P(_vp), ctypes.c_char_p, _P(_sz)])
 _sig("as_random_graph", [_vp, ctypes.c_uint64, ctypes.c_char_p, _P(_sz)])
 _sig("as_graph_features", [_vp, _vp, _P(_sz)])
+_sig("as_fit_array_model", [_vp, _sz, _i32, _vp])
 _sig("as_surrogate_fit_predict", [_vp, _vp, _sz, _sz, _vp, _sz, _vp])
 _sig("as_dist_row_cuts", [_vp, _i32, _vp])
 _sig("as_matrix_col_span", [_vp, _vp, _vp])
@@ -109,7 +111,7 @@ EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create
             "as_plan_keys", "as_plan_destroy", "as_spmv", "as_spmv_host", "as_search", "as_random_graph",
             "as_dist_row_cuts", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
             "as_dist_set_cuts", "as_dist_ipc_handle", "as_dist_open_peers", "as_spmv_dist", "as_dist_check",
-            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows"]
+            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows", "as_fit_array_model"]
 
 
 class AsError(RuntimeError):
@@ -340,6 +342,20 @@ def search(matrix: Matrix, device: int = 0, stream=None, seed: int = 1, max_cand
         text = buf.value.decode()
     p = Plan(matrix, None, device, _handle=h.value)
     return p, text
+
+
+def fit_array_model(a, budget: int = 8):
+    """Model-Driven Format Compression fit (as_fit_array_model): (kind, b, k1, k2, w,
+    [(index, value), ...]) or None."""
+    a = np.ascontiguousarray(a, np.int64)
+    out = np.zeros(6 + 2 * 8, np.int64)
+    st = _lib.as_fit_array_model(a.ctypes.data, a.shape[0], budget, out.ctypes.data)
+    if STATUS.get(st) == "AS_ERR_NOT_FOUND":
+        return None
+    _ck(st)
+    k, np_ = int(out[0]), int(out[5])
+    return (k, int(out[1]), int(out[2]), int(out[3]), int(out[4]),
+            [(int(out[6 + 2 * j]), int(out[7 + 2 * j])) for j in range(np_)])
 
 
 def surrogate_fit_predict(X, y, Xq) -> np.ndarray:

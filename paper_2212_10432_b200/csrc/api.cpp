@@ -318,6 +318,7 @@ as_status_t as_plan_info(as_plan_t P, as_plan_info_t* out) {
     if (!P || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
     *out = P->P->info;
     out->single_writer = P->P->single_writer ? 1 : 0;
+    out->modeled_arrays = P->P->modeled_arrays;
   });
 }
 

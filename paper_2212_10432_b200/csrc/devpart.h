@@ -20,6 +20,17 @@ enum Fam {
 };
 
 constexpr int kMaxDiags = 64;
+constexpr int kMaxPatches = 8;
+
+// Model-Driven Format Compression (§V-D, NEXT-2): an index array replaced by
+// model(i) = b + k1*(i / w) + k2*(i % w) (linear: w = 1; periodic linear; step: k2 = 0) with
+// up to kMaxPatches exceptions (i, value) -- "a small number of errors can be tolerated by
+// adding if statements".  kind 0 = no model.
+struct IdxModel {
+  int64_t b = 0, k1 = 0, k2 = 0, w = 1;
+  int kind = 0, np = 0;
+  int64_t pi[kMaxPatches] = {0}, pv[kMaxPatches] = {0};
+};
 constexpr int kMaxFusedPeers = 7;  // as_spmv_dist fused peer stores: up to 8 ranks
 
 struct DevPart {
@@ -29,8 +40,9 @@ struct DevPart {
   int variant = 0;
   int64_t m_p = 0, nnz_p = 0, n = 0;
   // COMPRESS output
-  const int32_t* origin = nullptr;  // NULL -> origin_base + row
+  const int32_t* origin = nullptr;  // NULL -> org_model(row) if fitted, else origin_base + row
   int64_t origin_base = 0;
+  IdxModel org_model;
   const int32_t* row_ptr = nullptr;
   const int32_t* col = nullptr;
   const void* val = nullptr;
@@ -40,7 +52,8 @@ struct DevPart {
   int64_t s = 0;                          // BMT_ROW size
   const int32_t* bmt_start = nullptr;     // NNZ BMTs: NULL -> t*k
   const int32_t* bmt_row_ptr = nullptr;   // ROW BMTs: NULL -> min(t*s, m_p)
-  const int32_t* bmt_first_row = nullptr;
+  const int32_t* bmt_first_row = nullptr;  // NULL -> fr_model(t) (NNZ BMTs, model-driven compression)
+  IdxModel fr_model;
   const uint32_t* bitmap = nullptr;
   int bm_words = 0;
   const uint32_t* bits = nullptr;         // tile form: packed head bits, 1 per nonzero

@@ -73,6 +73,9 @@ Seq parse_graph(const std::string& text);  // parse + expand replicated branches
 std::string print_graph(const Seq& g);
 bool is_branching(const std::string& name);
 
+// Model-Driven Format Compression (model.cpp, NEXT-2)
+bool fit_array_model(const std::vector<int64_t>& a, int budget, IdxModel* out);
+
 // search cost model (surrogate.cpp, NEXT-3)
 size_t graph_feature_count();
 std::vector<double> graph_features(const Seq& g);

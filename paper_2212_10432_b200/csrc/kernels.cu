@@ -94,8 +94,20 @@ __device__ __forceinline__ uint32_t ldm(const uint32_t* p) { return __ldg(p); }
 __device__ __forceinline__ int64_t ldm(const int64_t* p) { return __ldg(p); }
 
 // ---------------------------------------------------------------- writers
+// Model-Driven Format Compression: evaluate a fitted index model with its patches
+__device__ __forceinline__ int64_t idx_eval(const IdxModel& m, int64_t i) {
+  int64_t v = m.w == 1 ? m.b + m.k1 * i : m.b + m.k1 * (i / m.w) + m.k2 * (i % m.w);
+  for (int j = 0; j < m.np; ++j)
+    if (i == m.pi[j]) v = m.pv[j];
+  return v;
+}
 __device__ __forceinline__ int64_t out_row(const DevPart& p, int64_t r) {
-  return p.origin ? (int64_t)ldm(p.origin + r) : p.origin_base + r;
+  if (p.origin) return (int64_t)ldm(p.origin + r);
+  return p.org_model.kind ? idx_eval(p.org_model, r) : p.origin_base + r;
+}
+// first (compacted) row of NNZ BMT t: stored array, or its fitted model
+__device__ __forceinline__ int64_t bmt_row0(const DevPart& p, int64_t t) {
+  return p.bmt_first_row ? (int64_t)ldm(p.bmt_first_row + t) : idx_eval(p.fr_model, t);
 }
 // fp32 plans: scratch slot of a heavy row (A25), or -1.  A 1-bit-per-row filter (L1/L2
 // resident) answers the common case; only heavy rows pay the binary search.
@@ -475,7 +487,7 @@ template <class V, bool PAD, int VEC, int KB, class XA>
 __device__ __forceinline__ void nnz_thread_bmt(const DevPart& p, XA xa, V* __restrict__ y, int64_t t) {
   int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
   int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
-  int64_t row = ldm(p.bmt_first_row + t);
+  int64_t row = bmt_row0(p, t);
   double acc;
   bool inside;
   PadPos pp{0, 0};
@@ -600,7 +612,7 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   ScanPE o;
   o.s0 = ldm(bm) & 1u;
   o.inside = o.s0;
-  o.row = (int32_t)ldm(p.bmt_first_row + t);  // device row indices are int32 (A36)
+  o.row = (int32_t)bmt_row0(p, t);  // device row indices are int32 (A36)
   o.acc = 0.0;
   o.first = 0.0;
   const int full = len & ~(KB - 1);
@@ -649,7 +661,7 @@ __global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __re
     if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
     const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM, PIPE>(p, y, xa, t, pp);
     // first segment closed inside the BMT but begun before it: straddler
-    if (!o.s0 && o.inside) write_atom(p, y, ldm(p.bmt_first_row + t), o.first);
+    if (!o.s0 && o.inside) write_atom(p, y, bmt_row0(p, t), o.first);
     // open last segment: exclusive iff it began at a head here and the next BMT starts a row
     const bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
     if (o.inside && ends) write_excl(p, y, o.row, o.acc);
@@ -914,7 +926,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
       if (active) {
         int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
         int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
-        int64_t row = ldm(p.bmt_first_row + t);
+        int64_t row = bmt_row0(p, t);
         head_row = row;
         double cur;
         bool in;
@@ -999,7 +1011,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __rest
         const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM, PIPE>(p, y, xa, t, pp);
         b0 = o.s0;
         hh = o.inside;
-        const int64_t row0 = ldm(p.bmt_first_row + t);
+        const int64_t row0 = bmt_row0(p, t);
         if (!o.s0) {
           cin = o.inside ? o.first : o.acc;  // continuation of a row begun in an earlier lane
           head_row = row0 + 1;
@@ -1494,7 +1506,7 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       // (write_excl consults it in ADD mode only), or the legacy form is forced for A/B
       // timing (variant 9)
       const bool pe = p.variant != 9 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
-      const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin;
+      const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin && !p.org_model.kind;
       const bool pipe = p.pipe;
 #define AS_NT(PADV, VECV)                                                                                 \
   {                                                                                                       \
@@ -1539,7 +1551,7 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       // predicated-emit form unless fp32 ADD-mode heavy rows need the scratch path, or the
       // legacy form is forced (variant + 8: AS_NT_LEGACY)
       const bool pe = p.variant < 8 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
-      const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin;
+      const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin && !p.org_model.kind;
       constexpr int KBW = 4;  // fp64 batches of 8 spill 100-180 bytes next to the warp-combine state
 #define AS_NWPE(WR, PADV, VECV)                                                                  \
   {                                                                                              \

@@ -277,6 +277,7 @@ static Plan::Span part_span(const HostPart& h, int64_t n) {
 
 void Plan::upload(cudaStream_t s) {
   const int64_t sv = dt == AS_R64F ? 8 : 4;
+  const bool mdc = !std::getenv("AS_NO_MDC");  // Model-Driven Format Compression (A/B knob)
   int max_smem = device_max_smem_optin(device);
   for (int64_t pi : host.launch_order) {
     const HostPart& h = host.parts[pi];
@@ -319,9 +320,11 @@ void Plan::upload(cudaStream_t s) {
       if (nnz >= INT32_MAX) fail(AS_ERR_PLAN_INFEASIBLE, "part nnz exceeds int32 (reading A36)");
       d.m_p = mp;
       d.nnz_p = nnz;
-      // origin_rows: implicit when affine (A17)
+      // origin_rows: implicit when affine (A17), else a fitted model (NEXT-2), else stored
       if (mp && is_affine(h.origin, 1, h.origin[0])) {
         d.origin_base = h.origin[0];
+      } else if (mdc && fit_array_model(h.origin, kMaxPatches, &d.org_model)) {
+        ++modeled_arrays;
       } else {
         d.origin = up_i32(h.origin, s, "origin_rows");
         bytes_model += (double)(mp * 4);
@@ -375,10 +378,15 @@ void Plan::upload(cudaStream_t s) {
             d.bmt_start = up_i32(T.start, s, "bmt_start");
             bytes_model += (double)(T.start.size() * 4);
           }
-          d.bmt_first_row = up_i32(T.first_row, s, "bmt_first_row");
+          if (mdc && fit_array_model(T.first_row, kMaxPatches, &d.fr_model)) {
+            ++modeled_arrays;  // Model-Driven Format Compression (NEXT-2): computed, not loaded
+          } else {
+            d.bmt_first_row = up_i32(T.first_row, s, "bmt_first_row");
+            bytes_model += (double)(T.first_row.size() * 4);
+          }
           d.bm_words = h.bm_words;
           d.bitmap = (const uint32_t*)up(h.bitmap.data(), h.bitmap.size() * 4, s);
-          bytes_model += (double)(T.first_row.size() * 4 + h.bitmap.size() * 4);
+          bytes_model += (double)(h.bitmap.size() * 4);
           if (h.pad) {  // CSR5-like slot-major tiles (BMT_PAD over NNZ BMTs)
             upload_pad(h, d, s);
             need_colval = false;

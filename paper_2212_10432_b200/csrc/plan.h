@@ -31,6 +31,7 @@ struct Plan {
   // every row's final value is produced by exactly one STORE (no pre-pass, no ADD parts,
   // no atomic rows, no fp32 heavy-row epilogue): as_spmv_dist may fuse peer stores
   bool single_writer = false;
+  int modeled_arrays = 0;  // index arrays replaced by fitted models (NEXT-2)
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // as_spmv_host copy streams (lazy)
   std::vector<cudaEvent_t> evs;                    // as_spmv_host events (lazy)
   cudaEvent_t host_event(size_t i);
