@@ -186,7 +186,7 @@ def cpu_baseline(coo, wl, budget_s=10.0):
             "sample": f"{n} full passes over {wl} ({coo.nnz} nnz), long double, {cores} threads, {t_tot:.1f} s"}
 
 
-E2E_BANDS = 8  # ROW_DIV bands of the pipelined e2e plan
+E2E_BANDS = 4  # ROW_DIV bands of the pipelined e2e plan (C2 sweep: 4 -> 0.94 ms, 8 -> 0.98, 16 -> 1.10)
 
 
 def cdev():

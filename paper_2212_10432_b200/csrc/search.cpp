@@ -334,7 +334,7 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       if (as_spmv(&h, alpha, dx, beta, dy, stream) != AS_OK) fail(AS_ERR_CUDA, as_last_error());
     std::vector<float> ts;
     for (int rep = 0; rep < reps; ++rep) {
-      if (flush) cudaMemsetAsync(flush, rep & 0xff, flush_bytes, s);
+      if (flush) launch_l2_flush(flush, flush_bytes, rep & 0xff, stream);  // clean lines only
       cudaEventRecord(e0, s);
       if (as_spmv(&h, alpha, dx, beta, dy, stream) != AS_OK) fail(AS_ERR_CUDA, as_last_error());
       cudaEventRecord(e1, s);
