@@ -228,6 +228,7 @@ struct Builder {
     if (op.br[0].size() > 1) {
       P.tpb = (int)op.br[0][1].geti("tpb");
       P.grid = (int)op.br[0][1].geti("grid");
+      P.stages = (int)op.br[0][1].geti("stages");
     }
     hp.parts.push_back(std::move(P));
     residual(op, BState{st.rows, mk, true});
@@ -318,6 +319,7 @@ struct Builder {
     if (op.br[0].size() > 1) {
       P.tpb = (int)op.br[0][1].geti("tpb");
       P.grid = (int)op.br[0][1].geti("grid");
+      P.stages = (int)op.br[0][1].geti("stages");
     }
     hp.parts.push_back(std::move(P));
     residual(op, BState{st.rows, mk, true});
