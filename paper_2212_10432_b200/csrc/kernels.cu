@@ -1347,58 +1347,6 @@ __global__ void __launch_bounds__(1024) k_dia(DevPart p, const V* __restrict__ x
   }
 }
 
-// DIA part, TMA-staged form (SET_RESOURCE stages = 2): persistent CTAs own contiguous
-// ranges of T-row tiles; thread 0 streams the D diagonal slices of a tile into shared memory
-// with cp.async.bulk (one mbarrier per stage, kDiaStages tiles in flight), all threads
-// then combine them with x (L1/L2) and store y.  The HBM stream of the diagonals runs ahead
-// of the arithmetic without occupying registers.
-constexpr int kDiaT = 1024;  // rows per tile
-template <class V, int DT>
-__global__ void __launch_bounds__(256) k_dia_tma(DevPart p, const V* __restrict__ x, V* __restrict__ y, int stages) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  V* buf = (V*)smem_raw;                                            // [stages][DT][kDiaT]
-  uint64_t* bars = (uint64_t*)(smem_raw + (size_t)stages * DT * kDiaT * sizeof(V));
-  const V* dv = (const V*)p.dia_val;
-  const int64_t ntile = (p.mb + kDiaT - 1) / kDiaT;
-  const int64_t per = (ntile + gridDim.x - 1) / gridDim.x;
-  const int64_t t0 = (int64_t)blockIdx.x * per, t1 = min(t0 + per, ntile);
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < stages; ++st) mbar_init(&bars[st], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int64_t tile, int st) {  // thread 0
-    const int64_t rows = min((int64_t)kDiaT, p.mb - tile * kDiaT);
-    const uint32_t bytes = (uint32_t)((rows * (int64_t)sizeof(V) + 15) & ~int64_t(15));  // padded stride: in bounds
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&bars[st], bytes * DT);
-#pragma unroll
-    for (int d = 0; d < DT; ++d)
-      bulk_g2s(buf + ((size_t)st * DT + d) * kDiaT, dv + d * p.dia_stride + tile * kDiaT, bytes, &bars[st]);
-  };
-  if (threadIdx.x == 0)
-    for (int k = 0; k < stages && t0 + k < t1; ++k) issue(t0 + k, k);
-  for (int64_t k = 0; t0 + k < t1; ++k) {
-    const int st = (int)(k % stages);
-    mbar_wait(&bars[st], (uint32_t)((k / stages) & 1));
-    const int64_t tile = t0 + k, base = tile * kDiaT;
-    const int64_t rows = min((int64_t)kDiaT, p.mb - base);
-    const V* sb = buf + (size_t)st * DT * kDiaT;
-    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
-      const int64_t r = p.r0 + base + i;
-      double acc = 0.0;
-#pragma unroll
-      for (int d = 0; d < DT; ++d) {
-        const int64_t c = r + p.dia_off[d];
-        if (c >= 0 && c < p.n) acc += (double)sb[d * kDiaT + i] * ldx(x, c);
-      }
-      write_excl(p, y, base + i, acc);
-    }
-    __syncthreads();  // stage st fully consumed
-    if (threadIdx.x == 0 && tile + stages < t1) issue(tile + stages, st);
-  }
-}
-
 // =====================================================================================
 // FAM_DENSE, b = 64, fp64: one warp per tile row; half-warp h takes tile columns j = h,
 // h+2, ...; lane owns 4 consecutive tile rows and reads them with one 256-bit load per
@@ -1648,20 +1596,6 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
     if (p.variant == 1) k_dia<V, K, 32><<<g, tpb, 0, s>>>(p, x, y);            \
     else k_dia<V, K, 16><<<g, tpb, 0, s>>>(p, x, y);                           \
     break;
-      if (p.variant == 2) {  // TMA-staged form (prepare_part sized smem and grid)
-        const int st = (int)p.smem_cap;
-#define AS_DIA_TMA(K) \
-  case K:             \
-    k_dia_tma<V, K><<<p.grid, 256, p.smem, s>>>(p, x, y, st); \
-    break;
-        switch (p.D) {
-          AS_DIA_TMA(1) AS_DIA_TMA(2) AS_DIA_TMA(3) AS_DIA_TMA(4)
-          AS_DIA_TMA(5) AS_DIA_TMA(6) AS_DIA_TMA(7) AS_DIA_TMA(8)
-          default: return (int)cudaErrorInvalidValue;
-        }
-#undef AS_DIA_TMA
-        break;
-      }
       switch (p.D) {
         AS_DIA_CASE(1) AS_DIA_CASE(2) AS_DIA_CASE(3) AS_DIA_CASE(4)
         AS_DIA_CASE(5) AS_DIA_CASE(6) AS_DIA_CASE(7) AS_DIA_CASE(8)
@@ -1742,41 +1676,7 @@ int launch_scale_all(int64_t m, double beta, void* y, int dtype, void* stream) {
   return (int)cudaGetLastError();
 }
 
-template <class V>
-static int prepare_dia_tma(DevPart& p) {
-  const size_t tile = (size_t)p.D * kDiaT * sizeof(V);
-  int dev = 0, optin = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int stages = (int)std::min<size_t>(4, ((size_t)optin - 64) / tile);
-  if (stages < 2) return (int)cudaErrorInvalidValue;
-  p.smem = (size_t)stages * tile + 8 * (size_t)stages;
-  p.smem_cap = stages;
-  cudaError_t e = cudaSuccess;
-  switch (p.D) {
-#define AS_DIA_ATTR(K) \
-  case K: e = cudaFuncSetAttribute(k_dia_tma<V, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem); break;
-    AS_DIA_ATTR(1) AS_DIA_ATTR(2) AS_DIA_ATTR(3) AS_DIA_ATTR(4) AS_DIA_ATTR(5) AS_DIA_ATTR(6) AS_DIA_ATTR(7)
-    AS_DIA_ATTR(8)
-#undef AS_DIA_ATTR
-    default: return (int)cudaErrorInvalidValue;
-  }
-  if (e != cudaSuccess) return (int)e;
-  p.grid = sms;  // persistent: one CTA per SM
-  return 0;
-}
-
 int prepare_part(DevPart& p) {
-  if (p.fam == FAM_DIA && p.variant == 2) {  // TMA-staged DIA (falls back to the direct form)
-    const int e = p.dtype == 1 ? prepare_dia_tma<double>(p) : prepare_dia_tma<float>(p);
-    if (e) {
-      cudaGetLastError();
-      p.variant = 0;
-      p.smem = 0;
-    }
-    return 0;
-  }
   if (p.fam == FAM_BLOCK_OFFSET && p.variant == 1) {  // TMA-staged CSR-stream
     const size_t sv = p.dtype == 1 ? 8 : 4;
     p.smem = 2 * ((size_t)p.smem_cap * (sv + 4) + (size_t)p.smem_rcap * 4) + (size_t)p.smem_cap * 8 + 16;
