@@ -13,6 +13,7 @@ storage, stable sorts and prefix sums.  Each step follows one reading in DESIGN.
   SORT / SORT_SUB / BIN  P:21, P:277 "reorder matrix rows according to their lengths";
                          P:802 "sorted in a decreasing order"                               A7, A8, A9
   DIA_DECOM / DENSE_DECOM P:21 "separate the locally dense parts or diagonal band parts"    A12, A13
+  HYB_DECOM              P:583 "the matrix decomposition strategy of HYB" (NEXT-4)          R-hyb
   COMPRESS               P:22 "pushes non-zeros to the left of each row"                    A6, A14
   *_BLOCK                P:25 "cut adjacent non-zeros of the matrix into blocks"; P:33     A15
   BMT_PAD                P:279 "add zeros to specific positions"; "padded to the max"  A18
@@ -136,6 +137,25 @@ def _run_seq(csr, seq, st, parts, dtype):
             for b, sub in enumerate(op.branches):
                 sel = (lens > lo[b]) & (lens <= hi[b])
                 _run_seq(csr, sub, State(st.rows[sel], st.mask, False), parts, dtype)
+            return
+        if nm == "HYB_DECOM":
+            # HYB split (reading R-hyb; the decomposition P:583 names as missing):
+            # in every row of the branch, its first w live nonzeros (column order) go to
+            # branch 0 (ELL part), the remaining live ones to branch 1 (COO part).
+            w = op.params["w"]
+            ell = np.zeros_like(st.mask)
+            rest = np.zeros_like(st.mask)
+            for r in st.rows:
+                k = 0
+                for e in range(csr.row_ptr[r], csr.row_ptr[r + 1]):
+                    if st.mask[e]:
+                        if k < w:
+                            ell[e] = True
+                        else:
+                            rest[e] = True
+                        k += 1
+            _run_seq(csr, op.branches[0], State(st.rows, ell, st.contiguous), parts, dtype)
+            _run_seq(csr, op.branches[1], State(st.rows, rest, st.contiguous), parts, dtype)
             return
         if nm == "DIA_DECOM":
             _dia_decom(csr, op, st, parts, dtype)

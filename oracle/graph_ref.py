@@ -22,7 +22,7 @@ import dataclasses
 import re
 from typing import Any
 
-CONVERTING = {"ROW_DIV", "COL_DIV", "SORT", "SORT_SUB", "BIN", "DIA_DECOM", "DENSE_DECOM"}
+CONVERTING = {"ROW_DIV", "COL_DIV", "SORT", "SORT_SUB", "BIN", "DIA_DECOM", "DENSE_DECOM", "HYB_DECOM"}
 MAPPING = {"BMTB_ROW_BLOCK", "BMTB_NNZ_BLOCK", "BMW_ROW_BLOCK", "BMW_NNZ_BLOCK",
            "BMT_ROW_BLOCK", "BMT_NNZ_BLOCK", "BMT_PAD", "SORT_BMTB"}
 REDUCTIONS = {"THREAD_TOTAL_RED": "BMT", "THREAD_BITMAP_RED_G": "BMT",
@@ -30,7 +30,7 @@ REDUCTIONS = {"THREAD_TOTAL_RED": "BMT", "THREAD_BITMAP_RED_G": "BMT",
               "SHMEM_TOTAL_RED": "BMTB", "SHMEM_OFFSET_RED": "BMTB", "GMEM_ATOM_RED": "GMEM"}
 IMPLEMENTING = set(REDUCTIONS) | {"SET_RESOURCE"}
 TERMINAL = {"DIA", "DENSE"}
-BRANCHING = {"ROW_DIV", "COL_DIV", "BIN", "DIA_DECOM", "DENSE_DECOM"}
+BRANCHING = {"ROW_DIV", "COL_DIV", "BIN", "DIA_DECOM", "DENSE_DECOM", "HYB_DECOM"}
 SORT_FAMILY = {"SORT", "SORT_SUB", "BIN"}
 LEVEL_ORDER = {"BMTB": 0, "BMW": 1, "BMT": 2}
 RED_ORDER = {"BMT": 0, "BMW": 1, "BMTB": 2, "GMEM": 3}
@@ -44,6 +44,7 @@ SCHEMA: dict[str, list[tuple[str, str, Any]]] = {
     "BIN": [("t", "ilist", None)],
     "DIA_DECOM": [("theta", "float", None), ("max", "int", 8)],
     "DENSE_DECOM": [("b", "int", None), ("theta", "float", None)],
+    "HYB_DECOM": [("w", "int", None)],   # NEXT-4: the HYB split P:583 names as missing
     "COMPRESS": [],
     "DIA": [],
     "DENSE": [],
@@ -231,7 +232,7 @@ def n_branches(op: Op) -> int:
         return len(op.params["cuts"]) + 1
     if op.name == "BIN":
         return len(op.params["t"]) + 1
-    if op.name in ("DIA_DECOM", "DENSE_DECOM"):
+    if op.name in ("DIA_DECOM", "DENSE_DECOM", "HYB_DECOM"):
         return 2
     return 0
 
@@ -250,7 +251,7 @@ def _expand(seq):
     for op in seq:
         for b in op.branches:
             _expand(b)
-        if op.name in ("ROW_DIV", "COL_DIV", "BIN") and len(op.branches) == 1:
+        if op.name in ("ROW_DIV", "COL_DIV", "BIN", "HYB_DECOM") and len(op.branches) == 1:
             k = n_branches(op)
             op.branches = [_clone(op.branches[0]) for _ in range(k)]
 
@@ -304,6 +305,9 @@ def _check_params(op: Op, nid: int):
     elif op.name == "DENSE_DECOM":
         if not (0.0 < p["theta"] <= 1.0) or p["b"] < 1:
             bad("0 < theta <= 1, b >= 1")
+    elif op.name == "HYB_DECOM":
+        if p["w"] < 1:
+            bad("w >= 1")
     elif op.name.endswith("_BLOCK"):
         v = p.get("rows", p.get("nnz"))
         if v < 1:

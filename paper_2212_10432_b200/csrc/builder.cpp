@@ -136,6 +136,25 @@ struct Builder {
         }
         return;
       }
+      if (nm == "HYB_DECOM") {
+        // HYB decomposition (NEXT-4; the operator P:583 names as missing): the first w live
+        // nonzeros of every row form branch 0 (the ELL part), the rest branch 1 (the COO
+        // part); both are ordinary sub-graphs and their partial sums meet in y.
+        const int64_t w = op.geti("w");
+        auto m0 = std::make_shared<std::vector<uint8_t>>(A.nnz(), 0);
+        auto m1 = std::make_shared<std::vector<uint8_t>>(A.nnz(), 0);
+        parallel_for((int64_t)st.rows.size(), [&](int64_t a, int64_t e) {
+          for (int64_t i = a; i < e; ++i) {
+            const int64_t r = st.rows[i];
+            int64_t k = 0;
+            for (int64_t j = A.row_ptr[r]; j < A.row_ptr[r + 1]; ++j)
+              if (live(st, j)) ((k++ < w) ? (*m0)[j] : (*m1)[j]) = 1;
+          }
+        });
+        run(op.br[0], BState{st.rows, m0, st.contiguous});
+        run(op.br[1], BState{st.rows, m1, st.contiguous});
+        return;
+      }
       if (nm == "DIA_DECOM") {
         dia_decom(op, st);
         return;

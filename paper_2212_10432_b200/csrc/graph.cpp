@@ -41,6 +41,7 @@ const std::vector<OpSpec>& specs() {
       {"BIN", 0, {{"t", P_LIST, false, 0, nullptr}}},
       {"DIA_DECOM", 0, {{"theta", P_FLOAT, false, 0, nullptr}, {"max", P_INT, true, 8, nullptr}}},
       {"DENSE_DECOM", 0, {{"b", P_INT, false, 0, nullptr}, {"theta", P_FLOAT, false, 0, nullptr}}},
+      {"HYB_DECOM", 0, {{"w", P_INT, false, 0, nullptr}}},
       {"COMPRESS", 1, {}},
       {"DIA", 4, {}},
       {"DENSE", 4, {}},
@@ -327,14 +328,14 @@ struct Parser {
 int64_t n_branches(const Op& o) {
   if (o.name == "ROW_DIV" || o.name == "COL_DIV") return (int64_t)o.getl("cuts").size() + 1;
   if (o.name == "BIN") return (int64_t)o.getl("t").size() + 1;
-  if (o.name == "DIA_DECOM" || o.name == "DENSE_DECOM") return 2;
+  if (o.name == "DIA_DECOM" || o.name == "DENSE_DECOM" || o.name == "HYB_DECOM") return 2;
   return 0;
 }
 
 void expand(Seq& s) {
   for (auto& o : s) {
     for (auto& b : o.br) expand(b);
-    if ((o.name == "ROW_DIV" || o.name == "COL_DIV" || o.name == "BIN") && o.br.size() == 1) {
+    if ((o.name == "ROW_DIV" || o.name == "COL_DIV" || o.name == "BIN" || o.name == "HYB_DECOM") && o.br.size() == 1) {
       int64_t k = n_branches(o);
       Seq one = o.br[0];
       o.br.assign((size_t)k, one);
@@ -373,6 +374,8 @@ void check_params(const Op& o) {
   } else if (o.name == "DENSE_DECOM") {
     double th = o.getf("theta");
     if (!(th > 0.0 && th <= 1.0) || o.geti("b") < 1) bad("0 < theta <= 1, b >= 1");
+  } else if (o.name == "HYB_DECOM") {
+    if (o.geti("w") < 1) bad("w >= 1");
   } else if (block_level(o.name) >= 0 && o.name.size() > 6 && o.name.substr(o.name.size() - 6) == "_BLOCK") {
     int64_t v = o.params[0].second.i;
     if (v < 1) bad("block size >= 1");
@@ -559,7 +562,7 @@ void print_seq(const Seq& s, std::string& out) {
 }  // namespace
 
 bool is_branching(const std::string& n) {
-  return n == "ROW_DIV" || n == "COL_DIV" || n == "BIN" || n == "DIA_DECOM" || n == "DENSE_DECOM";
+  return n == "ROW_DIV" || n == "COL_DIV" || n == "BIN" || n == "DIA_DECOM" || n == "DENSE_DECOM" || n == "HYB_DECOM";
 }
 
 int64_t Op::geti(const char* k) const {

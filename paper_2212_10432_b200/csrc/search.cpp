@@ -154,6 +154,7 @@ std::string gen_path(Rng& r, const Stats& st, bool can_decom, bool can_sort, boo
   if (can_decom && depth < 2) {
     ops.push_back(5);  // DIA_DECOM
     ops.push_back(6);  // DENSE_DECOM
+    if (st.var > 16 && st.maxlen > 2 * st.avg) ops.push_back(7);  // HYB_DECOM: balanced rows + a few long ones
   }
   int op = r.pick(ops);
   switch (op) {
@@ -200,6 +201,11 @@ std::string gen_path(Rng& r, const Stats& st, bool can_decom, bool can_sort, boo
                       ",theta=" + std::string(r.pick(std::vector<const char*>{"0.5", "0.75", "0.9"})) + ") { DENSE | " +
                       gen_path(r, st, false, can_sort, false, depth + 1) + " }";
       return s;
+    }
+    case 7: {  // HYB (NEXT-4): ELL part of width ~ the typical row, COO-like rest
+      const int64_t w = std::max<int64_t>(1, (int64_t)std::llround(st.avg * r.pick(std::vector<double>{0.5, 1.0, 1.5, 2.0})));
+      return "HYB_DECOM(w=" + std::to_string(w) + ") { " + gen_path(r, st, false, can_sort, false, depth + 1) + " | " +
+             gen_path(r, st, false, can_sort, false, depth + 1) + " }";
     }
     default:
       return gen_kernel(r, st);

@@ -220,6 +220,9 @@ FAMILY_GRAPHS = [
     "DIA_DECOM(theta=0.2,max=3) { DIA | COMPRESS; BMT_NNZ_BLOCK(5); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
     "DENSE_DECOM(b=4,theta=0.25) { DENSE | DIA_DECOM(0.3) { DIA | COMPRESS; BMW_ROW_BLOCK(1); WARP_TOTAL_RED; GMEM_ATOM_RED } }",
     "ROW_DIV(cuts=[9]) { DENSE_DECOM(b=3,theta=0.3) { DENSE | COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED } | DIA_DECOM(0.25, 2) { DIA; SET_RESOURCE(64) | SORT; COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED } }",
+    "HYB_DECOM(w=3) { COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED | COMPRESS; BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
+    "SORT; HYB_DECOM(w=2) { COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL,1); THREAD_TOTAL_RED; GMEM_ATOM_RED | COMPRESS; BMW_ROW_BLOCK(1); WARP_TOTAL_RED; GMEM_ATOM_RED }",
+    "DIA_DECOM(theta=0.2,max=3) { DIA | HYB_DECOM(w=1) { COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED } }",
 ]
 
 

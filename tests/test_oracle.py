@@ -271,7 +271,26 @@ FUZZ_GRAPHS = [
     "BIN(t=[2, 6]) { COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED }",
     "DIA_DECOM(theta=0.3,max=3) { DIA | COMPRESS; BMT_NNZ_BLOCK(5); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
     "DENSE_DECOM(b=4,theta=0.3) { DENSE | DIA_DECOM(0.5) { DIA | COMPRESS; BMW_ROW_BLOCK(1); WARP_TOTAL_RED; GMEM_ATOM_RED } }",
+    "HYB_DECOM(w=2) { COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED | COMPRESS; BMT_NNZ_BLOCK(3); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
+    "BIN(t=[3]) { HYB_DECOM(w=1) { COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED } }",
 ]
+
+
+@pytest.mark.parametrize("w", [1, 2, 5])
+def test_hyb_split_is_first_w_per_row(w):
+    """R-hyb: the ELL branch of HYB_DECOM(w) holds exactly the first min(len, w) nonzeros of
+    every row (column order), the COO branch the rest -- checked against a direct count."""
+    A = synth.random_matrix(40, 30, 0.25, 7, int_mode=True, dense_rows=1)
+    ex, parts = _build(f"HYB_DECOM(w={w}) {{ COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED"
+                       " | COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED }", A)
+    rows = {}
+    for r, c in zip(A.row.tolist(), A.col.tolist()):
+        rows.setdefault(r, []).append(c)
+    for b, part in enumerate(parts):
+        orig, rp, col = ex[f"p{b}.origin_rows"], ex[f"p{b}.row_ptr"], ex[f"p{b}.col"]
+        got = {int(orig[i]): col[rp[i]:rp[i + 1]].tolist() for i in range(len(orig))}
+        want = {r: (cs[:w] if b == 0 else cs[w:]) for r, cs in rows.items() if (cs[:w] if b == 0 else cs[w:])}
+        assert got == want
 
 
 @pytest.mark.parametrize("graph", FUZZ_GRAPHS)
