@@ -98,6 +98,9 @@ def load_config(name, int_mode=False):
     if name == "c4":
         coo, _ = synth.c4_blockdense_csr()
         return coo, "blockdense-8m", [
+            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMTB_ROW_BLOCK(32); BMT_ROW_BLOCK(1); BMT_PAD(BMTB); THREAD_TOTAL_RED; SET_RESOURCE(64); GMEM_ATOM_RED }",
+            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMW_NNZ_BLOCK(1024); BMT_NNZ_BLOCK(32); BMT_PAD(BMW,2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=512,grid=2); GMEM_ATOM_RED }",
+            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL,2); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=512,grid=2,stages=0); GMEM_ATOM_RED }",
             "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
             "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMTB_ROW_BLOCK(64); BMT_ROW_BLOCK(1); BMT_PAD(BMTB); THREAD_TOTAL_RED; SET_RESOURCE(128); GMEM_ATOM_RED }",
             "COMPRESS; BMTB_ROW_BLOCK(64); BMT_ROW_BLOCK(1); BMT_PAD(BMTB); THREAD_TOTAL_RED; SET_RESOURCE(128); GMEM_ATOM_RED"]
