@@ -8,3 +8,9 @@ for c in 3 4 5; do
   ncu --metrics $M --clock-control none --csv --log-file gpurun_out/launches3_c$c.csv python tools/run_graphs.py c$c "$G" > /dev/null 2>&1
   ncu --set full --clock-control none --import-source on -k regex:k_nnz -s 2 -c 1 -o gpurun_out/prof3_c$c python tools/run_graphs.py c$c "$G" > gpurun_out/prof3_c$c.log 2>&1
 done
+# export the summaries on the box and drop the large reports (gpurun_out is capped at 64 MiB)
+for c in 3 4 5; do
+  ncu -i gpurun_out/prof3_c$c.ncu-rep --page raw --csv > gpurun_out/prof3_c$c.raw.csv 2>/dev/null
+  ncu -i gpurun_out/prof3_c$c.ncu-rep --page details --csv > gpurun_out/prof3_c$c.details.csv 2>/dev/null
+done
+rm -f gpurun_out/prof3_c*.ncu-rep
