@@ -109,7 +109,6 @@ struct DevPart {
   int64_t peer_lo[kMaxFusedPeers] = {0}, peer_hi[kMaxFusedPeers] = {0};  // plan rows [lo, hi) peer i reads
   int n_peer = 0;
   int pipe = 0;  // nnz kernels, predicated-emit form: one batch of load look-ahead
-  int xcg = 0;   // nnz kernels, predicated-emit form: x gathers with ld.global.cg (no L1 allocation)
   // launch
   int tpb = 256, grid = 0;
   size_t smem = 0;

@@ -402,16 +402,6 @@ struct XGlobal {
   const V* __restrict__ x;
   __device__ __forceinline__ double operator()(int64_t c) const { return ldx(x, c); }
 };
-// x gathers that skip L1 allocation (ld.global.cg, L2 only): for gathers with no reuse inside
-// an SM (scattered columns, C3/C4 residual) -- A/B knob AS_X_CG
-__device__ __forceinline__ double ldx_cg(const double* x, int64_t c) { return __ldcg(x + c); }
-__device__ __forceinline__ double ldx_cg(const float* x, int64_t c) { return (double)__ldcg(x + c); }
-template <class V>
-struct XGlobalSel {
-  const V* __restrict__ x;
-  bool cg;
-  __device__ __forceinline__ double operator()(int64_t c) const { return cg ? ldx_cg(x, c) : ldx(x, c); }
-};
 template <class V>
 struct XRing {
   const V* ring;
@@ -664,7 +654,7 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
 
 template <class V, bool PAD, int VEC, int KB, int EM, bool PIPE>
 __global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
-  const XGlobalSel<V> xa{x, p.xcg != 0};
+  const XGlobal<V> xa{x};
   const Units u = thread_units(p.n_bmt);
   for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x) {
     PadPos pp{0, 0};
@@ -995,7 +985,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
 template <class V, int WRED, bool PAD, int VEC, int KB, int EM, bool PIPE>
 __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const int lane = threadIdx.x & 31;
-  const XGlobalSel<V> xa{x, p.xcg != 0};
+  const XGlobal<V> xa{x};
   for (int64_t w = warp_units(p.n_bmw).begin, w_e = warp_units(p.n_bmw).end; w < w_e; w += blockDim.x >> 5) {
     const int64_t tb0 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w) : w * p.bmts_per_bmw;
     const int64_t tb1 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w + 1) : min(tb0 + p.bmts_per_bmw, p.n_bmt);

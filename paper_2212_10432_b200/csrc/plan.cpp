@@ -478,8 +478,6 @@ void Plan::upload(cudaStream_t s) {
         bytes_model += (double)(nnz * (4 + sv));
       }
     }
-    if (std::getenv("AS_X_CG") && (d.fam == FAM_NNZ_THREAD || d.fam == FAM_NNZ_WARP))  // A/B knob
-      d.xcg = std::atoi(std::getenv("AS_X_CG"));
     if (std::getenv("AS_NT_PIPE") && d.fam == FAM_NNZ_THREAD)  // A/B knob
       d.pipe = std::atoi(std::getenv("AS_NT_PIPE"));
     if (std::getenv("AS_NT_LEGACY")) {  // A/B knob: branching forms of the nnz kernels
