@@ -118,6 +118,7 @@ void as_graph_destroy(as_graph_t);
  * Blocking.  The plan owns its device arrays and keeps no reference to the matrix.
  * flags: AS_PLAN_KEEP_HOST keeps the logical metadata on the host for as_plan_export. */
 #define AS_PLAN_KEEP_HOST 1
+#define AS_PLAN_SPMM 2      /* also upload the plain CSR arrays of CSR-family parts (as_spmm) */
 as_status_t as_plan(as_matrix_t, as_graph_t, int device, void* stream, as_plan_t* out);
 as_status_t as_plan_ex(as_matrix_t, as_graph_t, int device, void* stream, int flags,
                        as_plan_t* out);
@@ -148,6 +149,17 @@ as_status_t as_spmv(as_plan_t, const void* alpha, const void* x, const void* bet
  * result is identical either way (same kernels, same order on the device). */
 as_status_t as_spmv_host(as_plan_t, const void* alpha, const void* x_host, const void* beta,
                          void* y_host, void* stream);
+
+/* SpMM (NEXT-4): Y = alpha*A*X + beta*Y with k right-hand sides.  X[n x k] and Y[m x k]
+ * are row-major device arrays of the plan's dtype with leading dimensions ldx, ldy >= k;
+ * they must not overlap.  The plan must be built with AS_PLAN_SPMM.  Parts run in the SpMV's
+ * writer-rule order (beta pre-pass, STORE / ADD per row): DENSE tiles as tensor-core
+ * contractions (fp64 DMMA m8n8k4; fp32 tiles widened exactly), DIA parts per (row, column),
+ * CSR-family parts by a row-parallel CSR SpMM over their COMPRESS arrays (rows summed in
+ * fp64 by one thread group).  Asynchronous on `stream`.  Tolerance per element as the SpMV
+ * (O2). */
+as_status_t as_spmm(as_plan_t, int64_t k, const void* alpha, const void* X, int64_t ldx,
+                    const void* beta, void* Y, int64_t ldy, void* stream);
 
 /* ---------------------------------------------------------------- a7: search
  * Random dependency-respecting graphs ("operators ... randomly chosen and connected

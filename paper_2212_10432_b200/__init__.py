@@ -27,6 +27,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 AS_R32F, AS_R64F = 0, 1
 AS_PLAN_KEEP_HOST = 1
+AS_PLAN_SPMM = 2
 STATUS = {0: "AS_OK", 1: "AS_ERR_INVALID_ARG", 2: "AS_ERR_MALFORMED", 3: "AS_ERR_INDEX_OUT_OF_RANGE",
           4: "AS_ERR_DUPLICATE", 5: "AS_ERR_GRAPH_PARSE", 6: "AS_ERR_GRAPH_ILLEGAL", 7: "AS_ERR_PLAN_INFEASIBLE",
           8: "AS_ERR_OOM", 9: "AS_ERR_CUDA", 10: "AS_ERR_NO_FEASIBLE", 11: "AS_ERR_DTYPE", 12: "AS_ERR_NOT_FOUND",
@@ -85,6 +86,7 @@ _sig("as_plan_keys", [_vp, ctypes.c_char_p, _P(_sz)])
 _sig("as_plan_destroy", [_vp], None)
 _sig("as_spmv", [_vp, _vp, _vp, _vp, _vp, _vp])
 _sig("as_spmv_host", [_vp, _vp, _vp, _vp, _vp, _vp])
+_sig("as_spmm", [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp])
 _sig("as_search", [_vp, _P(AsSearchCfg), _i32, _vp, _P(_vp), ctypes.c_char_p, _P(_sz)])
 _sig("as_random_graph", [_vp, ctypes.c_uint64, ctypes.c_char_p, _P(_sz)])
 _sig("as_graph_features", [_vp, _vp, _P(_sz)])
@@ -111,7 +113,7 @@ EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create
             "as_plan_keys", "as_plan_destroy", "as_spmv", "as_spmv_host", "as_search", "as_random_graph",
             "as_dist_row_cuts", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
             "as_dist_set_cuts", "as_dist_ipc_handle", "as_dist_open_peers", "as_spmv_dist", "as_dist_check",
-            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows", "as_fit_array_model"]
+            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows", "as_fit_array_model", "as_spmm"]
 
 
 class AsError(RuntimeError):
@@ -266,7 +268,8 @@ def _ptr(t):
 class Plan:
     """a2-a4: the graph executed on the Matrix Metadata Set into a device-resident format."""
 
-    def __init__(self, matrix: Matrix, graph, device: int = 0, stream=None, keep_host: bool = False, _handle=None):
+    def __init__(self, matrix: Matrix, graph, device: int = 0, stream=None, keep_host: bool = False, _handle=None,
+                 spmm: bool = False):
         self.dtype = np.dtype(matrix.dtype) if matrix is not None else None
         self.device = device
         if _handle is not None:
@@ -276,7 +279,8 @@ class Plan:
             graph = Graph(graph)
         h = _vp()
         s = 0 if device < 0 else _stream_handle(stream)
-        _ck(_lib.as_plan_ex(matrix._h, graph._h, device, s, AS_PLAN_KEEP_HOST if keep_host else 0, ctypes.byref(h)))
+        flags = (AS_PLAN_KEEP_HOST if keep_host else 0) | (AS_PLAN_SPMM if spmm else 0)
+        _ck(_lib.as_plan_ex(matrix._h, graph._h, device, s, flags, ctypes.byref(h)))
         self._h = h
 
     def info(self) -> dict:
@@ -311,6 +315,15 @@ class Plan:
         """y = alpha*A*x + beta*y on device tensors (asynchronous on `stream`)."""
         a, b = self._scalars(alpha, beta)
         _ck(_lib.as_spmv(self._h, ctypes.byref(a), _ptr(x), ctypes.byref(b), _ptr(y), _stream_handle(stream)))
+
+    def spmm(self, alpha, X, beta, Y, stream=None):
+        """a5 with k right-hand sides (as_spmm): X (n x k), Y (m x k) row-major device tensors
+        with unit column stride; plan built with spmm=True."""
+        if X.dim() != 2 or Y.dim() != 2 or X.stride(1) != 1 or Y.stride(1) != 1 or X.shape[1] != Y.shape[1]:
+            raise AsError(1, "X (n x k) and Y (m x k) must be 2-D row-major with matching k")
+        a, b = self._scalars(alpha, beta)
+        _ck(_lib.as_spmm(self._h, X.shape[1], ctypes.byref(a), _ptr(X), X.stride(0), ctypes.byref(b), _ptr(Y),
+                         Y.stride(0), _stream_handle(stream)))
 
     def spmv_host(self, alpha, x: np.ndarray, beta, y: np.ndarray, stream=None):
         """Same with host arrays (copies inside; synchronous)."""

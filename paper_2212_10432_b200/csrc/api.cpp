@@ -90,6 +90,7 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
       check_cuda(cudaSetDevice(device), "cudaSetDevice");
       try {
         P->upload((cudaStream_t)stream);
+        if (flags & AS_PLAN_SPMM) P->upload_spmm((cudaStream_t)stream);
       } catch (...) {
         cudaSetDevice(cur);
         throw;
@@ -484,6 +485,42 @@ as_status_t as_spmv_host(as_plan_t h, const void* alpha, const void* x_host, con
     }
     check_cuda(cudaStreamSynchronize(s), "sync");
     cudaSetDevice(cur);
+  });
+}
+
+as_status_t as_spmm(as_plan_t h, int64_t k, const void* alpha, const void* X, int64_t ldx, const void* beta, void* Y,
+                    int64_t ldy, void* stream) {
+  return guard([&] {
+    if (!h || !alpha || !beta) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    Plan& P = *h->P;
+    if (P.device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan cannot run as_spmm");
+    if (!P.spmm) fail(AS_ERR_INVALID_ARG, "plan built without AS_PLAN_SPMM");
+    if (k < 1 || ldx < k || ldy < k) fail(AS_ERR_INVALID_ARG, "need k >= 1, ldx >= k, ldy >= k");
+    if ((P.n > 0 && !X) || (P.m > 0 && !Y)) fail(AS_ERR_INVALID_ARG, "NULL X or Y");
+    const size_t sv = P.dt == AS_R64F ? 8 : 4;
+    if (((uintptr_t)X | (uintptr_t)Y) & (sv - 1)) fail(AS_ERR_INVALID_ARG, "X and Y must be aligned to the value size");
+    const char *xa = (const char*)X, *xe = xa + (size_t)(P.n ? (P.n - 1) * ldx + k : 0) * sv;
+    const char *ya = (const char*)Y, *ye = ya + (size_t)(P.m ? (P.m - 1) * ldy + k : 0) * sv;
+    if (X && Y && xa < ye && ya < xe) fail(AS_ERR_INVALID_ARG, "X and Y alias");
+    const double a = P.dt == AS_R64F ? *(const double*)alpha : (double)*(const float*)alpha;
+    const double b = P.dt == AS_R64F ? *(const double*)beta : (double)*(const float*)beta;
+    cudaError_t prior = cudaGetLastError();
+    if (prior != cudaSuccess) fail(AS_ERR_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(prior));
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != P.device) cudaSetDevice(P.device);
+    const int dtc = P.dt == AS_R64F ? 1 : 0;
+    int err = 0;
+    if (P.n_prepass) {  // same rule as the SpMV: a fill of all rows when it moves fewer bytes (beta == 0)
+      if (b == 0.0 && (double)P.m * sv <= (double)P.n_prepass * (4 + 32))
+        err = launch_spmm_prepass(nullptr, 0, P.m, 0.0, Y, ldy, k, dtc, stream);
+      else
+        err = launch_spmm_prepass(P.d_prepass, P.n_prepass, P.m, b, Y, ldy, k, dtc, stream);
+    }
+    for (size_t i = 0; i < P.launches.size() && !err; ++i)
+      err = launch_spmm_part(P.launches[i], P.spmm_parts[i], a, b, X, ldx, Y, ldy, k, stream);
+    if (cur != P.device) cudaSetDevice(cur);
+    if (err) fail(AS_ERR_CUDA, std::string("spmm launch: ") + cudaGetErrorString((cudaError_t)err));
   });
 }
 

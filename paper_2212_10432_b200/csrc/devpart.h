@@ -128,6 +128,21 @@ int device_max_smem_optin(int device);
 int device_sm_count(int device);
 int xw_ctas_per_sm(int dtype, int pad, int vec, int tpb, size_t smem);
 
+// spmm.cu (NEXT-4): the plain CSR arrays of a CSR-family part, uploaded with AS_PLAN_SPMM
+struct SpmmPart {
+  const int32_t* rows = nullptr;  // m_p global output rows
+  const int32_t* rp = nullptr;    // m_p + 1
+  const int32_t* col = nullptr;
+  const void* val = nullptr;
+  const uint8_t* add = nullptr;   // per row: 1 = add alpha*s (atomic-class or ADD-mode row), 0 = store
+  int64_t m_p = 0;
+};
+int launch_spmm_part(const DevPart& p, const SpmmPart& s, double alpha, double beta, const void* X, int64_t ldx,
+                     void* Y, int64_t ldy, int64_t k, void* stream);
+// rows != NULL: y[r][:] = beta*y[r][:] for the n listed rows; else for all m rows
+int launch_spmm_prepass(const int32_t* rows, int64_t n, int64_t m, double beta, void* Y, int64_t ldy, int64_t k,
+                        int dtype, void* stream);
+
 // dist_kernels.cu: peer-memory exchange of as_spmv_dist (AS_EXCH_PEER)
 constexpr int kMaxPeers = 64;  // AS_DIST_MAX_WORLD
 struct PeerPush {

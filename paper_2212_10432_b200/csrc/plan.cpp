@@ -504,6 +504,32 @@ void Plan::upload(cudaStream_t s) {
   ck(cudaStreamSynchronize(s), "upload");
 }
 
+// SpMM (NEXT-4): the plain COMPRESS arrays of every CSR-family part plus a per-row "add"
+// flag (ADD-mode part, or a row that straddles writer units in the SpMV -- those rows are in
+// the beta pre-pass, so SpMM adds its whole-row partial to them).
+void Plan::upload_spmm(cudaStream_t s) {
+  std::vector<uint8_t> atom((size_t)m, 0);
+  for (int64_t pi : host.launch_order)
+    for (int64_t r : host.parts[pi].atom) atom[(size_t)r] = 1;
+  for (int64_t pi : host.launch_order) {
+    const HostPart& h = host.parts[pi];
+    SpmmPart sp;
+    if (h.kind == "csr") {
+      sp.m_p = (int64_t)h.origin.size();
+      sp.rows = up_i32(h.origin, s, "spmm rows");
+      sp.rp = up_i32(h.row_ptr, s, "spmm row_ptr");
+      sp.col = (const int32_t*)up(h.col.data(), h.col.size() * 4, s);
+      sp.val = up_vals(h.val, s);
+      std::vector<uint8_t> add((size_t)sp.m_p);
+      for (int64_t i = 0; i < sp.m_p; ++i) add[(size_t)i] = (h.mode == 1 || atom[(size_t)h.origin[i]]) ? 1 : 0;
+      sp.add = (const uint8_t*)up(add.data(), add.size(), s);
+      ck(cudaStreamSynchronize(s), "spmm upload");
+    }
+    spmm_parts.push_back(sp);
+  }
+  spmm = true;
+}
+
 void Plan::compute_model() {
   const double sv = dt == AS_R64F ? 8 : 4;
   // x: compulsory distinct columns; y per writer rule

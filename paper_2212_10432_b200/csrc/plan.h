@@ -32,6 +32,9 @@ struct Plan {
   // no atomic rows, no fp32 heavy-row epilogue): as_spmv_dist may fuse peer stores
   bool single_writer = false;
   int modeled_arrays = 0;  // index arrays replaced by fitted models (NEXT-2)
+  bool spmm = false;              // AS_PLAN_SPMM: SpMM arrays of the CSR-family parts uploaded
+  std::vector<SpmmPart> spmm_parts;  // per launch (empty for DIA / DENSE parts)
+  void upload_spmm(cudaStream_t s);
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // as_spmv_host copy streams (lazy)
   std::vector<cudaEvent_t> evs;                    // as_spmv_host events (lazy)
   cudaEvent_t host_event(size_t i);
