@@ -505,14 +505,14 @@ void Plan::upload(cudaStream_t s) {
 }
 
 // SpMM (NEXT-4): the plain COMPRESS arrays of every CSR-family part plus a per-row "add"
-// flag (ADD-mode part, or a row that straddles writer units in the SpMV -- those rows are in
-// the beta pre-pass, so SpMM adds its whole-row partial to them).
+// flag: the part is in ADD mode, or the row is one of ITS atomic rows (it straddles writer
+// units of this part in the SpMV, so its value was initialised by the pre-pass or an earlier
+// part; SpMM adds this part's whole-row partial).  Exclusive rows of a STORE part store.
 void Plan::upload_spmm(cudaStream_t s) {
   std::vector<uint8_t> atom((size_t)m, 0);
-  for (int64_t pi : host.launch_order)
-    for (int64_t r : host.parts[pi].atom) atom[(size_t)r] = 1;
   for (int64_t pi : host.launch_order) {
     const HostPart& h = host.parts[pi];
+    for (int64_t r : h.atom) atom[(size_t)r] = 1;  // this part's atomic rows (cleared below)
     SpmmPart sp;
     if (h.kind == "csr") {
       sp.m_p = (int64_t)h.origin.size();
@@ -525,6 +525,7 @@ void Plan::upload_spmm(cudaStream_t s) {
       sp.add = (const uint8_t*)up(add.data(), add.size(), s);
       ck(cudaStreamSynchronize(s), "spmm upload");
     }
+    for (int64_t r : h.atom) atom[(size_t)r] = 0;
     spmm_parts.push_back(sp);
   }
   spmm = true;
