@@ -63,7 +63,30 @@ __global__ void __launch_bounds__(256) k_spmm_csr(SpmmPart s, double alpha, doub
     const bool add = s.add[i] != 0;
     for (int64_t c0 = 0; c0 < k; c0 += 4 * G) {  // 4 columns per lane in flight
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int64_t j = a; j < e; ++j) {
+      int64_t j = a;
+      // 4 nonzeros per step: their column indices / values first, then 4 x 4 X loads in
+      // flight (the X rows are scattered, so the gathers' latency is what bounds this loop)
+      for (; j + 4 <= e; j += 4) {
+        double v[4];
+        const V* xr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          v[u] = (double)__ldg(val + j + u);
+          xr[u] = X + (int64_t)__ldg(s.col + j + u) * ldx;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t c = c0 + lane + q * G;
+          if (c < k) {
+            double xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) xv[u] = (double)__ldg(xr[u] + c);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[q] += v[u] * xv[u];
+          }
+        }
+      }
+      for (; j < e; ++j) {
         const double v = (double)__ldg(val + j);
         const V* xr = X + (int64_t)__ldg(s.col + j) * ldx;
 #pragma unroll
