@@ -184,76 +184,6 @@ __global__ void __launch_bounds__(256) k_spmm_dense_dmma(DevPart p, double alpha
   }
 }
 
-// fp64, b = 64, 16-byte aligned X rows: the same contraction with the next tile and X panel
-// streamed into the other shared-memory stage by cp.async (16-byte chunks, zero-filled past
-// k / n) while the tensor cores work on the current one.
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(src_bytes)
-               : "memory");
-}
-__global__ void __launch_bounds__(256) k_spmm_dense_dmma_pipe(DevPart p, double alpha, double beta,
-                                                              const double* __restrict__ X, int64_t ldx,
-                                                              double* __restrict__ Y, int64_t ldy, int64_t k) {
-  extern __shared__ double smem_d[];
-  const double* tv = (const double*)p.tile_val;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
-  auto sT = [&](int st) { return smem_d + (size_t)st * 2 * kTB * kLd; };
-  auto sX = [&](int st) { return smem_d + (size_t)st * 2 * kTB * kLd + kTB * kLd; };
-  for (int64_t tr = blockIdx.x; tr < p.n_tile_rows; tr += gridDim.x) {
-    const int64_t I = __ldg(p.tile_row_id + tr);
-    const int64_t t0 = __ldg(p.tile_row_ptr + tr), t1 = __ldg(p.tile_row_ptr + tr + 1);
-    for (int64_t c0 = 0; c0 < k; c0 += kTB) {
-      auto issue = [&](int64_t t, int st) {
-        const int64_t J = __ldg(p.tile_col + t);
-        double* dT = sT(st);
-        double* dX = sX(st);
-        for (int q = threadIdx.x; q < kTB * kTB / 2; q += blockDim.x) {  // 2048 chunks each
-          const int j = q >> 5, i2 = (q & 31) * 2;                       // tile column j, rows i2, i2+1
-          cp_async16(dT + j * kLd + i2, tv + t * kTB * kTB + j * kTB + i2, 16);
-          const int64_t xr = J * kTB + j, c = c0 + i2;                     // X row xr, columns c, c+1
-          const int nb = (xr < p.n && c < k) ? (c + 1 < k ? 16 : 8) : 0;
-          cp_async16(dX + j * kLd + i2, nb ? (const void*)(X + xr * ldx + c) : (const void*)X, nb);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      };
-      double acc[8][2];
-#pragma unroll
-      for (int nb = 0; nb < 8; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
-      if (t0 < t1) issue(t0, 0);
-      for (int64_t t = t0; t < t1; ++t) {
-        const int st = (int)((t - t0) & 1);
-        if (t + 1 < t1) {
-          issue(t + 1, st ^ 1);
-          asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-          asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        __syncthreads();
-        const double* cT = sT(st);
-        const double* cX = sX(st);
-#pragma unroll 4
-        for (int kk = 0; kk < kTB; kk += 4) {
-          const double a = cT[(kk + tig) * kLd + warp * 8 + g];
-#pragma unroll
-          for (int nb = 0; nb < 8; ++nb) dmma_8x8x4(acc[nb][0], acc[nb][1], a, cX[(kk + tig) * kLd + nb * 8 + g]);
-        }
-        __syncthreads();  // stage st consumed before it is refilled
-      }
-      const int64_t row = I * kTB + warp * 8 + g;
-      if (row >= p.row_lo && row < p.row_hi) {
-#pragma unroll
-        for (int nb = 0; nb < 8; ++nb)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int64_t c = c0 + nb * 8 + 2 * tig + h;
-            if (c < k) put(Y + row * ldy + c, acc[nb][h], alpha, beta, p.mode == 1);
-          }
-      }
-    }
-  }
-}
-
 int grid_of(int64_t work, int tpb) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -269,20 +199,6 @@ int spmm_part_t(const DevPart& p, const SpmmPart& s, double alpha, double beta, 
     k_spmm_dia<V><<<grid_of(p.mb * k, 256), 256, 0, st>>>(p, alpha, beta, X, ldx, Y, ldy, k);
   } else if (p.fam == FAM_DENSE) {
     if (p.b > kTB) return (int)cudaErrorInvalidValue;
-    if constexpr (sizeof(V) == 8) {
-      if (p.b == kTB && !(((uintptr_t)X | (uintptr_t)(ldx * 8)) & 15)) {  // pipelined form
-        static bool attr2 = false;
-        if (!attr2) {
-          cudaError_t e = cudaFuncSetAttribute(k_spmm_dense_dmma_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)(2 * kDenseSmem));
-          if (e != cudaSuccess) return (int)e;
-          attr2 = true;
-        }
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(p.n_tile_rows, 148 * 8));
-        k_spmm_dense_dmma_pipe<<<g, 256, 2 * kDenseSmem, st>>>(p, alpha, beta, (const double*)X, ldx, (double*)Y, ldy, k);
-        return (int)cudaGetLastError();
-      }
-    }
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(k_spmm_dense_dmma<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
