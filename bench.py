@@ -425,6 +425,26 @@ def main():
                "graph": g_e, "launches_per_step": l_e,
                "candidates_ms": {("pipelined" if i else "searched"): r[0] for i, r in enumerate(res)}}
 
+    # CUDA-graph replay of the same plan (AS_PLAN_GRAPH): the launch-latency floor of small
+    # matrices ("C1 also reports CUDA-Graph replay time"); small workloads only
+    graph_replay = None
+    if not args.profile and nnz_local < 50_000_000:
+        Pg = asp.Plan(A, graph, device=local, graph_replay=True)
+        for _ in range(3):
+            Pg.spmv(1.0, dx, 0.0, dy, stream)
+        gts = []
+        for _ in range(args.steps):
+            if not args.no_flush:
+                flush_l2()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            Pg.spmv(1.0, dx, 0.0, dy, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            gts.append(e0.elapsed_time(e1))
+        graph_replay = {"ms_per_step": statistics.mean(gts), "gflops": 2.0 * nnz_local / (statistics.mean(gts) * 1e-3) / 1e9}
+        del Pg
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -457,6 +477,8 @@ def main():
         "clocks": clk.summary(),
         "e2e": e2e,
     }
+    if graph_replay is not None:
+        line["graph_replay"] = graph_replay
     if gather_ms is not None:
         line["exchange"] = {"kind": args.exchange, "ms": gather_ms,
                             "timed": "spmv + exchange per step (as_spmv_dist)" if args.exchange in ("nccl", "peer", "peer_halo")

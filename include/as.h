@@ -119,6 +119,8 @@ void as_graph_destroy(as_graph_t);
  * flags: AS_PLAN_KEEP_HOST keeps the logical metadata on the host for as_plan_export. */
 #define AS_PLAN_KEEP_HOST 1
 #define AS_PLAN_SPMM 2      /* also upload the plain CSR arrays of CSR-family parts (as_spmm) */
+#define AS_PLAN_GRAPH 4     /* as_spmv captures its launch sequence into a CUDA graph once per
+                               (x, y, alpha, beta) and replays it: one launch per call */
 as_status_t as_plan(as_matrix_t, as_graph_t, int device, void* stream, as_plan_t* out);
 as_status_t as_plan_ex(as_matrix_t, as_graph_t, int device, void* stream, int flags,
                        as_plan_t* out);

@@ -91,6 +91,7 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
       try {
         P->upload((cudaStream_t)stream);
         if (flags & AS_PLAN_SPMM) P->upload_spmm((cudaStream_t)stream);
+        P->graph_mode = (flags & AS_PLAN_GRAPH) != 0;
       } catch (...) {
         cudaSetDevice(cur);
         throw;
@@ -368,7 +369,30 @@ as_status_t as_spmv(as_plan_t h, const void* alpha, const void* x, const void* b
     int cur = -1;
     cudaGetDevice(&cur);
     if (cur != P.device) cudaSetDevice(P.device);
-    int err = run_plan(P, x, y, a, b, (cudaStream_t)stream, [](size_t) {}, [](size_t) {});
+    int err = 0;
+    if (P.graph_mode) {
+      // AS_PLAN_GRAPH: the launch sequence is captured once per (x, y, alpha, beta) into a
+      // CUDA graph and replayed (one launch instead of one per part: latency-bound plans)
+      if (!P.gexec || P.gx != x || P.gy != y || P.ga != a || P.gb != b) {
+        if (P.gexec) cudaGraphExecDestroy(P.gexec);
+        P.gexec = nullptr;
+        if (!P.cap_stream) check_cuda(cudaStreamCreateWithFlags(&P.cap_stream, cudaStreamNonBlocking), "capture stream");
+        check_cuda(cudaStreamBeginCapture(P.cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+        err = run_plan(P, x, y, a, b, P.cap_stream, [](size_t) {}, [](size_t) {});
+        cudaGraph_t graph = nullptr;
+        cudaError_t e2 = cudaStreamEndCapture(P.cap_stream, &graph);
+        if (!err && e2 == cudaSuccess) err = (int)cudaGraphInstantiate(&P.gexec, graph, 0);
+        else if (!err) err = (int)e2;
+        if (graph) cudaGraphDestroy(graph);
+        P.gx = x;
+        P.gy = y;
+        P.ga = a;
+        P.gb = b;
+      }
+      if (!err) err = (int)cudaGraphLaunch(P.gexec, (cudaStream_t)stream);
+    } else {
+      err = run_plan(P, x, y, a, b, (cudaStream_t)stream, [](size_t) {}, [](size_t) {});
+    }
     if (cur != P.device) cudaSetDevice(cur);
     if (err) fail(AS_ERR_CUDA, std::string("launch: ") + cudaGetErrorString((cudaError_t)err));
   });

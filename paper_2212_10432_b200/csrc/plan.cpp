@@ -229,6 +229,8 @@ Plan::~Plan() {
     if (d_y) dev_free(d_y, stream);
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
     if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     if (s_d2h) cudaStreamDestroy(s_d2h);
     cudaSetDevice(cur);
   }

@@ -33,6 +33,12 @@ struct Plan {
   bool single_writer = false;
   int modeled_arrays = 0;  // index arrays replaced by fitted models (NEXT-2)
   bool spmm = false;              // AS_PLAN_SPMM: SpMM arrays of the CSR-family parts uploaded
+  bool graph_mode = false;        // AS_PLAN_GRAPH: as_spmv replays a captured CUDA graph
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  const void* gx = nullptr;       // (x, y, alpha, beta) the graph was captured with
+  void* gy = nullptr;
+  double ga = 0, gb = 0;
   std::vector<SpmmPart> spmm_parts;  // per launch (empty for DIA / DENSE parts)
   void upload_spmm(cudaStream_t s);
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // as_spmv_host copy streams (lazy)

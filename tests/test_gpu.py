@@ -153,6 +153,23 @@ def test_spmv_host_path():
     assert S.check(y, yref, bound, np.float64)[0]
 
 
+@pytest.mark.parametrize("graph", FAMILY_GRAPHS[::4] + [
+    "COL_DIV(cuts=[500]) { COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }"])
+def test_graph_replay(graph):
+    """AS_PLAN_GRAPH: the captured launch sequence replays to the same y; a new (x, y, alpha,
+    beta) triggers a re-capture."""
+    coo = synth.c1_uniform(int_mode=True)
+    A = _mat(coo)
+    P = asp.Plan(A, graph, device=0, graph_replay=True)
+    for seed, (al, be) in enumerate([(1.0, 0.0), (1.0, 0.0), (2.0, -1.0), (2.0, -1.0)]):
+        x, y0 = synth.vectors(coo.n, coo.m, seed // 2, np.float64, True)
+        dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y0.copy()).cuda()
+        P.spmv(al, dx, be, dy)
+        torch.cuda.synchronize()
+        yref, _ = S.spmv_coo(coo.m, coo.row, coo.col, coo.val, x, al, be, y0)
+        assert np.array_equal(dy.cpu().numpy(), yref), (graph, seed)
+
+
 LAP_CUTS = "cuts=[262144,524288,786432]"
 PIPE_GRAPHS = [
     f"ROW_DIV({LAP_CUTS}) {{ DIA_DECOM(theta=0.5) {{ DIA }} }}",
