@@ -1306,6 +1306,19 @@ struct LdN<double, 16> {
     o[1] = t.y;
   }
 };
+template <class V>
+struct LdN<V, 8> {  // one row per thread (variant 3: <= 32 registers, 2048 resident threads/SM)
+  static constexpr int R = sizeof(V) == 8 ? 1 : 2;
+  static __device__ __forceinline__ void ld(const V* p, double* o) {
+    if constexpr (sizeof(V) == 8) {
+      o[0] = ld_stream(p);
+    } else {
+      float2 t = ld_stream2(p);
+      o[0] = t.x;
+      o[1] = t.y;
+    }
+  }
+};
 template <>
 struct LdN<float, 16> {
   static constexpr int R = 4;
@@ -1319,7 +1332,7 @@ struct LdN<float, 16> {
 };
 
 template <class V, int DT, int BYTES>
-__global__ void __launch_bounds__(1024) k_dia(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+__global__ void __launch_bounds__(1024, BYTES == 8 ? 2 : 1) k_dia(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   constexpr int R = LdN<V, BYTES>::R;
   const V* dv = (const V*)p.dia_val;
   for (int64_t i0 = gtid() * R; i0 < p.mb; i0 += gthreads() * R) {
@@ -1591,9 +1604,11 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       // variant 0: 16-byte row groups (higher occupancy), 1: 32-byte (sm_100 256-bit loads)
       const int R = p.variant == 1 ? LdN<V, 32>::R : LdN<V, 16>::R;
       int64_t g = grid_for(p, (p.mb + R - 1) / R, tpb);
+      const int64_t g3 = grid_for(p, (p.mb + LdN<V, 8>::R - 1) / LdN<V, 8>::R, tpb);
 #define AS_DIA_CASE(K)                                                          \
   case K:                                                                       \
     if (p.variant == 1) k_dia<V, K, 32><<<g, tpb, 0, s>>>(p, x, y);            \
+    else if (p.variant == 3) k_dia<V, K, 8><<<g3, tpb, 0, s>>>(p, x, y);       \
     else k_dia<V, K, 16><<<g, tpb, 0, s>>>(p, x, y);                           \
     break;
       switch (p.D) {
