@@ -1601,7 +1601,9 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       else k_block_offset<V><<<grid_for(p, p.n_bmtb, 1), tpb, p.smem, s>>>(p, x, y);
       break;
     case FAM_DIA: {
-      // variant 0: 16-byte row groups (higher occupancy), 1: 32-byte (sm_100 256-bit loads)
+      // variant 3 (default): 8-byte loads, one fp64 row per thread, <= 32 registers -> 2048
+      // resident threads per SM (C2: 35.9 us); 0: 16-byte row pairs, 64 registers (42.0 us);
+      // 1: 32-byte (sm_100 256-bit loads, 46-48 us)
       const int R = p.variant == 1 ? LdN<V, 32>::R : LdN<V, 16>::R;
       int64_t g = grid_for(p, (p.mb + R - 1) / R, tpb);
       const int64_t g3 = grid_for(p, (p.mb + LdN<V, 8>::R - 1) / LdN<V, 8>::R, tpb);
