@@ -263,7 +263,7 @@ std::string mutate_graph(const Seq& g0, Rng& r) {
   else if (k == "vec") step({0, 1, 2, 4});
   else if (k == "max") step({4, 8, 16, 32});
   else if (k == "b") step({16, 32, 64, 128});
-  else if (k == "theta") v.f = v.f >= 0.85 ? 0.5 : v.f + 0.2;
+  else if (k == "theta") v.f = v.f >= 0.85 ? 0.5 : std::round((v.f + 0.2) * 100.0) / 100.0;
   else if (v.k == Value::INT) v.i = std::max<int64_t>(1, r.coin(0.5) ? v.i * 2 : v.i / 2);  // block sizes, g
   std::string s = print_graph(g);
   try {
