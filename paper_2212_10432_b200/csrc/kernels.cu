@@ -600,7 +600,7 @@ struct ScanPE {
   int32_t row;
   bool s0, inside;
 };
-template <class V, bool PAD, int VEC, int KB, int EM, bool PIPE, class XA>
+template <class V, bool PAD, int VEC, int KB, int EM, class XA>
 __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int64_t t, PadPos pp) {
   static_assert(32 % KB == 0 && KB % VEC == 0, "KB divides 32 and is a multiple of VEC");
   const int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
@@ -621,29 +621,9 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   const int64_t adv = PAD ? (KB / VEC) * pp.stride : KB;
   double v[KB];
   int32_t c[KB];
-  if constexpr (PIPE) {
-    // one batch of look-ahead: the next batch's value/column loads are issued before this
-    // batch's x gathers, so the HBM stream overlaps the gather latency
-    if (full > 0) batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, 0, len, v, c);
-    for (; j0 < full; j0 += KB) {
-      double vn[KB];
-      int32_t cn[KB];
-      const bool more = j0 + KB < full;
-      if (more) batch_load<V, PAD, VEC, KB, true>(pv + adv, pc + adv, pp.stride, j0 + KB, len, vn, cn);
-      batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
-      pv += adv;
-      pc += adv;
-#pragma unroll
-      for (int q = 0; q < KB; ++q) {
-        v[q] = vn[q];
-        c[q] = cn[q];
-      }
-    }
-  } else {
-    for (; j0 < full; j0 += KB, pv += adv, pc += adv) {
-      batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, j0, len, v, c);
-      batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
-    }
+  for (; j0 < full; j0 += KB, pv += adv, pc += adv) {
+    batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, j0, len, v, c);
+    batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
   }
   if (j0 < len) {
     batch_load<V, PAD, VEC, KB, false>(pv, pc, pp.stride, j0, len, v, c);
@@ -652,14 +632,16 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   return o;
 }
 
-template <class V, bool PAD, int VEC, int KB, int EM, bool PIPE>
-__global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+// LEAN: <= 512 threads per CTA, 3 CTAs per SM -> <= 42 registers and 1536 resident threads per
+// SM instead of 1024 (more occupancy was the lever that took the DIA kernel from 42 to 36 us)
+template <class V, bool PAD, int VEC, int KB, int EM, int LEAN>
+__global__ void __launch_bounds__(LEAN ? 512 : 1024, LEAN ? 3 : 1) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const XGlobal<V> xa{x};
   const Units u = thread_units(p.n_bmt);
   for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x) {
     PadPos pp{0, 0};
     if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
-    const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM, PIPE>(p, y, xa, t, pp);
+    const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM>(p, y, xa, t, pp);
     // first segment closed inside the BMT but begun before it: straddler
     if (!o.s0 && o.inside) write_atom(p, y, bmt_row0(p, t), o.first);
     // open last segment: exclusive iff it began at a head here and the next BMT starts a row
@@ -982,7 +964,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
 // k_nnz_warp, predicated-emit form: each lane scans its BMT with bmt_scan_pe (rows closed
 // inside the BMT stored by one predicated store, no divergent writer calls), then the same
 // warp combine of (cin, cout, head flag) as above.  Same writes as k_nnz_warp.
-template <class V, int WRED, bool PAD, int VEC, int KB, int EM, bool PIPE>
+template <class V, int WRED, bool PAD, int VEC, int KB, int EM>
 __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const XGlobal<V> xa{x};
@@ -1008,7 +990,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __rest
           else if (p.n_grp == 1) pp = PadPos{t * VEC, p.n_bmt * VEC};
           else pp = pad_pos<VEC>(p, t);
         }
-        const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM, PIPE>(p, y, xa, t, pp);
+        const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM>(p, y, xa, t, pp);
         b0 = o.s0;
         hh = o.inside;
         const int64_t row0 = bmt_row0(p, t);
@@ -1520,16 +1502,16 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       // timing (variant 9)
       const bool pe = p.variant != 9 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
       const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin && !p.org_model.kind;
-      const bool pipe = p.pipe;
+      const bool lean = p.lean && tt <= 512;
 #define AS_NT(PADV, VECV)                                                                                 \
   {                                                                                                       \
     constexpr int KBV = sizeof(V) == 4 && VECV <= 4 ? 4 : 8;                                              \
-    constexpr int KBP = VECV > 4 ? VECV : 4;                                                              \
+    constexpr int KBL = VECV > 4 ? VECV : 4;                                                              \
     if (!pe) k_nnz_thread<V, PADV, VECV, KBV><<<g, tt, 0, s>>>(p, x, y);                                  \
-    else if (pipe && em0) k_nnz_thread_pe<V, PADV, VECV, KBP, 0, true><<<g, tt, 0, s>>>(p, x, y);         \
-    else if (pipe) k_nnz_thread_pe<V, PADV, VECV, KBP, 1, true><<<g, tt, 0, s>>>(p, x, y);                \
-    else if (em0) k_nnz_thread_pe<V, PADV, VECV, KBV, 0, false><<<g, tt, 0, s>>>(p, x, y);                \
-    else k_nnz_thread_pe<V, PADV, VECV, KBV, 1, false><<<g, tt, 0, s>>>(p, x, y);                         \
+    else if (lean && em0) k_nnz_thread_pe<V, PADV, VECV, KBL, 0, 1><<<g, tt, 0, s>>>(p, x, y);            \
+    else if (lean) k_nnz_thread_pe<V, PADV, VECV, KBL, 1, 1><<<g, tt, 0, s>>>(p, x, y);                   \
+    else if (em0) k_nnz_thread_pe<V, PADV, VECV, KBV, 0, 0><<<g, tt, 0, s>>>(p, x, y);                    \
+    else k_nnz_thread_pe<V, PADV, VECV, KBV, 1, 0><<<g, tt, 0, s>>>(p, x, y);                             \
   }
       if (!p.pad) {
         AS_NT(false, 1)
@@ -1568,8 +1550,8 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       constexpr int KBW = 4;  // fp64 batches of 8 spill 100-180 bytes next to the warp-combine state
 #define AS_NWPE(WR, PADV, VECV)                                                                  \
   {                                                                                              \
-    if (em0) k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 0, false><<<g, tpb, 0, s>>>(p, x, y); \
-    else k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 1, false><<<g, tpb, 0, s>>>(p, x, y);     \
+    if (em0) k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 0><<<g, tpb, 0, s>>>(p, x, y); \
+    else k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 1><<<g, tpb, 0, s>>>(p, x, y);     \
   }
 #define AS_NW(WR)                                                              \
   if (pe) {                                                                    \
