@@ -108,7 +108,6 @@ struct DevPart {
   void* peer_y[kMaxFusedPeers] = {nullptr};
   int64_t peer_lo[kMaxFusedPeers] = {0}, peer_hi[kMaxFusedPeers] = {0};  // plan rows [lo, hi) peer i reads
   int n_peer = 0;
-  int lean = 0;  // k_nnz_thread_pe: <= 42-register form (3 x 512 resident threads per SM)
   // launch
   int tpb = 256, grid = 0;
   size_t smem = 0;

@@ -632,10 +632,8 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   return o;
 }
 
-// LEAN: <= 512 threads per CTA, 3 CTAs per SM -> <= 42 registers and 1536 resident threads per
-// SM instead of 1024 (more occupancy was the lever that took the DIA kernel from 42 to 36 us)
-template <class V, bool PAD, int VEC, int KB, int EM, int LEAN>
-__global__ void __launch_bounds__(LEAN ? 512 : 1024, LEAN ? 3 : 1) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+template <class V, bool PAD, int VEC, int KB, int EM>
+__global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const XGlobal<V> xa{x};
   const Units u = thread_units(p.n_bmt);
   for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x) {
@@ -1502,16 +1500,12 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       // timing (variant 9)
       const bool pe = p.variant != 9 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
       const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin && !p.org_model.kind;
-      const bool lean = p.lean && tt <= 512;
 #define AS_NT(PADV, VECV)                                                                                 \
   {                                                                                                       \
     constexpr int KBV = sizeof(V) == 4 && VECV <= 4 ? 4 : 8;                                              \
-    constexpr int KBL = VECV > 4 ? VECV : 4;                                                              \
     if (!pe) k_nnz_thread<V, PADV, VECV, KBV><<<g, tt, 0, s>>>(p, x, y);                                  \
-    else if (lean && em0) k_nnz_thread_pe<V, PADV, VECV, KBL, 0, 1><<<g, tt, 0, s>>>(p, x, y);            \
-    else if (lean) k_nnz_thread_pe<V, PADV, VECV, KBL, 1, 1><<<g, tt, 0, s>>>(p, x, y);                   \
-    else if (em0) k_nnz_thread_pe<V, PADV, VECV, KBV, 0, 0><<<g, tt, 0, s>>>(p, x, y);                    \
-    else k_nnz_thread_pe<V, PADV, VECV, KBV, 1, 0><<<g, tt, 0, s>>>(p, x, y);                             \
+    else if (em0) k_nnz_thread_pe<V, PADV, VECV, KBV, 0><<<g, tt, 0, s>>>(p, x, y);                       \
+    else k_nnz_thread_pe<V, PADV, VECV, KBV, 1><<<g, tt, 0, s>>>(p, x, y);                                \
   }
       if (!p.pad) {
         AS_NT(false, 1)

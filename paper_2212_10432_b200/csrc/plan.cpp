@@ -481,8 +481,6 @@ void Plan::upload(cudaStream_t s) {
         bytes_model += (double)(nnz * (4 + sv));
       }
     }
-    if (std::getenv("AS_NT_LEAN") && d.fam == FAM_NNZ_THREAD)  // A/B knob
-      d.lean = std::atoi(std::getenv("AS_NT_LEAN"));
     if (std::getenv("AS_NT_LEGACY")) {  // A/B knob: branching forms of the nnz kernels
       if (d.fam == FAM_NNZ_THREAD) d.variant = 9;
       if (d.fam == FAM_NNZ_WARP && !d.tile) d.variant += 8;
