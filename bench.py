@@ -142,7 +142,7 @@ def to_csr(obj):
     return synth.Csr(obj.m, obj.n, csr_of(obj), obj.col.astype(np.int32), obj.val, obj.name)
 
 
-def reference_arm(args, coo, wl):
+def reference_arm(args, coo, wl, scaling="strong"):
     """The oracle (long-double CSR SpMV, oracle/spmv_ref.c) on the host cores."""
     from oracle import spmv as S
     rp = csr_of(coo)
@@ -165,7 +165,7 @@ def reference_arm(args, coo, wl):
     sample = f"first {frac_rows} rows ({nnz_s} nnz) of {wl} per step, long double, {cores} threads"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64x", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64x", "data": "synthetic",
             "config": {"workload": wl, "nnz": coo.nnz, "rows": coo.m},
             "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -237,7 +237,7 @@ def main():
         coo = to_csr(coo)
     if args.impl == "reference":
         if rank == 0:
-            reference_arm(args, coo, wl)
+            reference_arm(args, coo, wl, "weak" if args.config == "c2" and args.scaling == "weak" else "strong")
         return
 
     import torch
