@@ -46,6 +46,17 @@ def main():
                 ok, ratio = S.check(dy.cpu().numpy(), yref, bnd, np.float64)
                 fails += not ok
                 print("ok " if ok else "BAD", beta, P.info()["kernels"], g[:70])
+    # SpMM kernels (DMMA dense tiles, DIA, CSR parts), k = 70 (ragged column chunk)
+    coo = synth.random_powerlaw(900, 800, 3, 300)
+    A = asp.Matrix.from_coo(coo.m, coo.n, coo.row, coo.col, coo.val)
+    for g in ["DENSE_DECOM(b=64,theta=0.02) { DENSE | COMPRESS; BMW_ROW_BLOCK(1); WARP_TOTAL_RED; GMEM_ATOM_RED }",
+              "DIA_DECOM(theta=0.01,max=8) { DIA | COMPRESS; BMT_NNZ_BLOCK(5); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }"]:
+        P = asp.Plan(A, g, device=0, spmm=True)
+        X = torch.rand((coo.n, 70), dtype=torch.float64, device="cuda")
+        Y = torch.rand((coo.m, 70), dtype=torch.float64, device="cuda")
+        P.spmm(1.5, X, -0.5, Y)
+        torch.cuda.synchronize()
+        print("ok  spmm", P.info()["kernels"], g[:60])
     print("failures:", fails)
     sys.exit(1 if fails else 0)
 
