@@ -125,6 +125,11 @@ __global__ void k_spmm_dia(DevPart p, double alpha, double beta, const V* __rest
 // warp w computes output rows [8w, 8w + 8) x 64 columns with m8n8k4 DMMA (8 accumulator
 // blocks), for b <= 64 (tile rows/cols beyond b are zero-filled).  Columns are processed in
 // chunks of 64.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
 constexpr int kTB = 64;
 constexpr int kLd = kTB + 8;  // padded row stride: the 4 k-rows a DMMA fragment reads hit 2 bank halves
 constexpr size_t kDenseSmem = 2 * (size_t)kTB * kLd * sizeof(double);
@@ -142,6 +147,7 @@ __global__ void __launch_bounds__(256) k_spmm_dense_dmma(DevPart p, double alpha
   const int b = (int)p.b;
   const V* tv = (const V*)p.tile_val;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  const bool async16 = sizeof(V) == 8 && b == kTB && !(((uintptr_t)X | (uintptr_t)(ldx * 8)) & 15);
   for (int64_t tr = blockIdx.x; tr < p.n_tile_rows; tr += gridDim.x) {
     const int64_t I = __ldg(p.tile_row_id + tr);
     const int64_t t0 = __ldg(p.tile_row_ptr + tr), t1 = __ldg(p.tile_row_ptr + tr + 1);
@@ -152,11 +158,24 @@ __global__ void __launch_bounds__(256) k_spmm_dense_dmma(DevPart p, double alpha
       for (int64_t t = t0; t < t1; ++t) {
         const int64_t J = __ldg(p.tile_col + t);
         __syncthreads();  // previous tile consumed
-        for (int e = threadIdx.x; e < kTB * kTB; e += blockDim.x) {
-          const int i = e & 63, j = e >> 6;
-          sT[j * kLd + i] = (i < b && j < b) ? (double)__ldg(tv + t * b * b + (int64_t)j * b + i) : 0.0;
-          const int64_t xr = J * b + j, c = c0 + i;  // panel element (j, c0 + i)
-          sX[j * kLd + i] = (j < b && xr < p.n && c < k) ? (double)__ldg(X + xr * ldx + c) : 0.0;
+        if (async16) {
+          // fp64, b = 64, 16-byte aligned X rows: 16-byte cp.async chunks (zero-filled past k
+          // and n), all 16 per thread in flight at once
+          for (int q = threadIdx.x; q < kTB * kTB / 2; q += blockDim.x) {
+            const int j = q >> 5, i2 = (q & 31) * 2;
+            cp_async16(sT + j * kLd + i2, (const double*)tv + t * kTB * kTB + j * kTB + i2, 16);
+            const int64_t xr = J * kTB + j, c = c0 + i2;
+            const int nb = (xr < p.n && c < k) ? (c + 1 < k ? 16 : 8) : 0;
+            cp_async16(sX + j * kLd + i2, nb ? (const void*)(X + xr * ldx + c) : (const void*)X, nb);
+          }
+          asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
+        } else {
+          for (int e = threadIdx.x; e < kTB * kTB; e += blockDim.x) {
+            const int i = e & 63, j = e >> 6;
+            sT[j * kLd + i] = (i < b && j < b) ? (double)__ldg(tv + t * b * b + (int64_t)j * b + i) : 0.0;
+            const int64_t xr = J * b + j, c = c0 + i;  // panel element (j, c0 + i)
+            sX[j * kLd + i] = (j < b && xr < p.n && c < k) ? (double)__ldg(X + xr * ldx + c) : 0.0;
+          }
         }
         __syncthreads();
 #pragma unroll 4
