@@ -632,21 +632,25 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   return o;
 }
 
+// one BMT of THREAD_BITMAP_RED_G in predicated-emit form, with the BMT's two boundary writes
+template <class V, bool PAD, int VEC, int KB, int EM, class XA>
+__device__ __forceinline__ void nnz_thread_bmt_pe(const DevPart& p, XA xa, V* __restrict__ y, int64_t t) {
+  PadPos pp{0, 0};
+  if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
+  const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM>(p, y, xa, t, pp);
+  // first segment closed inside the BMT but begun before it: straddler
+  if (!o.s0 && o.inside) write_atom(p, y, bmt_row0(p, t), o.first);
+  // open last segment: exclusive iff it began at a head here and the next BMT starts a row
+  const bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
+  if (o.inside && ends) write_excl(p, y, o.row, o.acc);
+  else write_atom(p, y, o.row, o.acc);
+}
+
 template <class V, bool PAD, int VEC, int KB, int EM>
 __global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
-  const XGlobal<V> xa{x};
   const Units u = thread_units(p.n_bmt);
-  for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x) {
-    PadPos pp{0, 0};
-    if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
-    const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM>(p, y, xa, t, pp);
-    // first segment closed inside the BMT but begun before it: straddler
-    if (!o.s0 && o.inside) write_atom(p, y, bmt_row0(p, t), o.first);
-    // open last segment: exclusive iff it began at a head here and the next BMT starts a row
-    const bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
-    if (o.inside && ends) write_excl(p, y, o.row, o.acc);
-    else write_atom(p, y, o.row, o.acc);
-  }
+  for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x)
+    nnz_thread_bmt_pe<V, PAD, VEC, KB, EM>(p, XGlobal<V>{x}, y, t);
 }
 
 // =====================================================================================
@@ -656,7 +660,8 @@ __global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __re
 // buffer, loading only the part of each window beyond what it already holds, so the
 // gathers read shared memory instead of moving a 32-byte L1/L2 sector per nonzero.
 // =====================================================================================
-template <class V, bool PAD, int VEC>
+// EM >= 0: predicated-emit scan (bmt_scan_pe) on the ring; EM < 0: branching form
+template <class V, bool PAD, int VEC, int EM>
 __global__ void __launch_bounds__(1024) k_nnz_thread_xw(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   V* ring = (V*)smem_raw;
@@ -672,7 +677,10 @@ __global__ void __launch_bounds__(1024) k_nnz_thread_xw(DevPart p, const V* __re
     if (hi > have_hi) have_hi = hi;
     __syncthreads();
     const int64_t t = b0 + i * blockDim.x + threadIdx.x;
-    if (t < b1) nnz_thread_bmt<V, PAD, VEC, 8>(p, XRing<V>{ring, mask}, y, t);
+    if (t < b1) {
+      if constexpr (EM >= 0) nnz_thread_bmt_pe<V, PAD, VEC, (sizeof(V) == 4 ? 4 : 8), EM>(p, XRing<V>{ring, mask}, y, t);
+      else nnz_thread_bmt<V, PAD, VEC, 8>(p, XRing<V>{ring, mask}, y, t);
+    }
     __syncthreads();  // the next window update overwrites entries this round may read
   }
 }
@@ -1485,10 +1493,17 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
     case FAM_NNZ_THREAD: {
       if (p.xwin) {
         const int64_t g = p.xw_grid;
-        if (!p.pad) k_nnz_thread_xw<V, false, 1><<<g, tpb, p.smem, s>>>(p, x, y);
-        else if (p.vec == 1) k_nnz_thread_xw<V, true, 1><<<g, tpb, p.smem, s>>>(p, x, y);
-        else if (p.vec == 2) k_nnz_thread_xw<V, true, 2><<<g, tpb, p.smem, s>>>(p, x, y);
-        else k_nnz_thread_xw<V, true, 4><<<g, tpb, p.smem, s>>>(p, x, y);
+        const bool pex = p.variant != 9 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
+#define AS_XW(PADV, VECV)                                                          \
+  {                                                                                \
+    if (!pex) k_nnz_thread_xw<V, PADV, VECV, -1><<<g, tpb, p.smem, s>>>(p, x, y);  \
+    else k_nnz_thread_xw<V, PADV, VECV, 1><<<g, tpb, p.smem, s>>>(p, x, y);        \
+  }
+        if (!p.pad) AS_XW(false, 1)
+        else if (p.vec == 1) AS_XW(true, 1)
+        else if (p.vec == 2) AS_XW(true, 2)
+        else AS_XW(true, 4)
+#undef AS_XW
         break;
       }
       int64_t g = grid_for(p, p.n_bmt, tpb);
@@ -1710,10 +1725,13 @@ static int xw_occ_t(int pad, int vec, int tpb, size_t smem) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, tpb, smem) != cudaSuccess) return 0;
     return n;
   };
-  if (!pad) return occ(k_nnz_thread_xw<V, false, 1>);
-  if (vec == 1) return occ(k_nnz_thread_xw<V, true, 1>);
-  if (vec == 2) return occ(k_nnz_thread_xw<V, true, 2>);
-  return occ(k_nnz_thread_xw<V, true, 4>);
+  // both forms (branching -1, predicated-emit 1) get the shared-memory opt-in; the smaller
+  // occupancy of the two decides the grid
+  auto both = [&](auto k0, auto k1) { return std::min(occ(k0), occ(k1)); };
+  if (!pad) return both(k_nnz_thread_xw<V, false, 1, -1>, k_nnz_thread_xw<V, false, 1, 1>);
+  if (vec == 1) return both(k_nnz_thread_xw<V, true, 1, -1>, k_nnz_thread_xw<V, true, 1, 1>);
+  if (vec == 2) return both(k_nnz_thread_xw<V, true, 2, -1>, k_nnz_thread_xw<V, true, 2, 1>);
+  return both(k_nnz_thread_xw<V, true, 4, -1>, k_nnz_thread_xw<V, true, 4, 1>);
 }
 int xw_ctas_per_sm(int dtype, int pad, int vec, int tpb, size_t smem) {
   int n = dtype == 1 ? xw_occ_t<double>(pad, vec, tpb, smem) : xw_occ_t<float>(pad, vec, tpb, smem);
