@@ -120,7 +120,9 @@ void as_graph_destroy(as_graph_t);
 #define AS_PLAN_KEEP_HOST 1
 #define AS_PLAN_SPMM 2      /* also upload the plain CSR arrays of CSR-family parts (as_spmm) */
 #define AS_PLAN_GRAPH 4     /* as_spmv captures its launch sequence into a CUDA graph once per
-                               (x, y, alpha, beta) and replays it: one launch per call */
+                               (x, y, alpha, beta) and replays it: one launch per call.  The
+                               plan then caches one graph: calls on the same plan must not run
+                               concurrently from several host threads */
 as_status_t as_plan(as_matrix_t, as_graph_t, int device, void* stream, as_plan_t* out);
 as_status_t as_plan_ex(as_matrix_t, as_graph_t, int device, void* stream, int flags,
                        as_plan_t* out);
