@@ -228,8 +228,8 @@ std::string json_escape(const std::string& s) {
 }
 
 // Fine-grained neighbour of a graph: one numeric parameter moved to an adjacent grid value
-// (the paper's fine parameter grid, P:369 step 3, explored by local search instead of an
-// XGBoost surrogate).  Returns "" when the graph has no mutable parameter.
+// (the paper's fine parameter grid, P:369 step 3): proposals for the cost-model stage and
+// the annealing stage.  Returns "" when the graph has no mutable parameter.
 void collect_params(Seq& g, std::vector<std::pair<Op*, size_t>>& out) {
   for (auto& op : g) {
     for (size_t j = 0; j < op.params.size(); ++j) {
