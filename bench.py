@@ -271,6 +271,9 @@ def main():
     stream = torch.cuda.current_stream()
 
     t_plan = time.perf_counter()
+    if args.config == "c1" and not args.graph:
+        # BASELINE configs[0] names a single graph (COMPRESS + BMT_NNZ_BLOCK(4) + thread reduction)
+        args.graph = seeds[0]
     if args.graph:
         P = asp.Plan(A, args.graph, device=local)
         graph = str(asp.Graph(args.graph))
