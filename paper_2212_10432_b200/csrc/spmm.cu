@@ -104,6 +104,48 @@ __global__ void __launch_bounds__(256) k_spmm_csr(SpmmPart s, double alpha, doub
   }
 }
 
+// CSR part, fp64 with 16-byte aligned X / Y rows and even k: lane pairs of columns read as
+// one double2 (half the load instructions of k_spmm_csr), G lanes per row cover 2G columns
+// per pass, 4 nonzeros in flight
+template <int G>
+__global__ void __launch_bounds__(256) k_spmm_csr2(SpmmPart s, double alpha, double beta, const double* __restrict__ X,
+                                                   int64_t ldx, double* __restrict__ Y, int64_t ldy, int64_t k) {
+  const int64_t grp = gtid_s() / G, ngrp = gthreads_s() / G;
+  const int lane = threadIdx.x % G;
+  const double* val = (const double*)s.val;
+  for (int64_t i = grp; i < s.m_p; i += ngrp) {
+    const int64_t a = __ldg(s.rp + i), e = __ldg(s.rp + i + 1);
+    const int64_t r = __ldg(s.rows + i);
+    const bool add = s.add[i] != 0;
+    for (int64_t c0 = 2 * lane; c0 < k; c0 += 2 * G) {
+      double2 acc = make_double2(0.0, 0.0);
+      int64_t j = a;
+      for (; j + 4 <= e; j += 4) {
+        double v[4];
+        double2 xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          v[u] = __ldg(val + j + u);
+          xv[u] = __ldg((const double2*)(X + (int64_t)__ldg(s.col + j + u) * ldx + c0));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc.x += v[u] * xv[u].x;
+          acc.y += v[u] * xv[u].y;
+        }
+      }
+      for (; j < e; ++j) {
+        const double v = __ldg(val + j);
+        const double2 xv = __ldg((const double2*)(X + (int64_t)__ldg(s.col + j) * ldx + c0));
+        acc.x += v * xv.x;
+        acc.y += v * xv.y;
+      }
+      put(Y + r * ldy + c0, acc.x, alpha, beta, add);
+      put(Y + r * ldy + c0 + 1, acc.y, alpha, beta, add);
+    }
+  }
+}
+
 // DIA part: one thread per (row, column)
 template <class V>
 __global__ void k_spmm_dia(DevPart p, double alpha, double beta, const V* __restrict__ X, int64_t ldx,
@@ -229,6 +271,24 @@ int spmm_part_t(const DevPart& p, const SpmmPart& s, double alpha, double beta, 
     k_spmm_dense_dmma<V><<<g, 256, kDenseSmem, st>>>(p, alpha, beta, X, ldx, Y, ldy, k);
   } else {
     if (!s.m_p) return 0;
+    if constexpr (sizeof(V) == 8) {
+      if (!(k & 1) && !(((uintptr_t)X | (uintptr_t)(ldx * 8)) & 15)) {  // double2 form
+        const int64_t half = std::min<int64_t>(k / 2, 32);
+        const int G = half <= 1 ? 1 : half <= 2 ? 2 : half <= 4 ? 4 : half <= 8 ? 8 : half <= 16 ? 16 : 32;
+        const int g = grid_of(s.m_p * G, 256);
+        const double* Xd = (const double*)X;
+        double* Yd = (double*)Y;
+        switch (G) {
+          case 1: k_spmm_csr2<1><<<g, 256, 0, st>>>(s, alpha, beta, Xd, ldx, Yd, ldy, k); break;
+          case 2: k_spmm_csr2<2><<<g, 256, 0, st>>>(s, alpha, beta, Xd, ldx, Yd, ldy, k); break;
+          case 4: k_spmm_csr2<4><<<g, 256, 0, st>>>(s, alpha, beta, Xd, ldx, Yd, ldy, k); break;
+          case 8: k_spmm_csr2<8><<<g, 256, 0, st>>>(s, alpha, beta, Xd, ldx, Yd, ldy, k); break;
+          case 16: k_spmm_csr2<16><<<g, 256, 0, st>>>(s, alpha, beta, Xd, ldx, Yd, ldy, k); break;
+          default: k_spmm_csr2<32><<<g, 256, 0, st>>>(s, alpha, beta, Xd, ldx, Yd, ldy, k); break;
+        }
+        return (int)cudaGetLastError();
+      }
+    }
     const int64_t kk = std::min<int64_t>(k, 32);
     const int G = kk <= 1 ? 1 : kk <= 2 ? 2 : kk <= 4 ? 4 : kk <= 8 ? 8 : kk <= 16 ? 16 : 32;
     const int g = grid_of(s.m_p * G, 256);
