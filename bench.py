@@ -475,6 +475,12 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                      "frac": achieved_gbs / hbm, "traffic": traffic, "peak_kind": hbm_kind,
                      "frac_of_8tbs": achieved_gbs / 8000.0,
+                     # measured DRAM bytes of the dominant kernel (ncu, committed) over the same
+                     # time: the model counts x and y in full although part of them stays in
+                     # L2, and a read-dominated stream can beat the copy peak, so frac may
+                     # exceed 1 where frac_dram does not
+                     "achieved_dram": (traffic / (t_ms * 1e-3) / 1e9) if traffic else None,
+                     "frac_dram": (traffic / (t_ms * 1e-3) / 1e9 / hbm) if traffic else None,
                      "note": "achieved = plan bytes model per as_spmv / mean event time of the step"
                              + (" (single launch)" if launches == 1 else f" ({launches} launches)")},
         "gpu_launches": launches * args.steps,
