@@ -454,7 +454,8 @@ def main():
             dist.destroy_process_group()
         return
     traffic = None
-    prof = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
+    # weak-scaled C2 bands run the same per-rank kernel as C2 itself
+    prof = os.path.join(ROOT, "profiles", f"traffic_{'lap2d-2048' if weak else wl}.json")
     if os.path.exists(prof):
         try:
             tj = json.load(open(prof))
