@@ -186,8 +186,25 @@ def cpu_baseline(coo, wl, budget_s=10.0):
         S.spmv_csr(rp, col, val, x, nthreads=cores)
         t_tot += time.perf_counter() - t0
         n += 1
+    # single-threaded beside all cores, on the first rows holding <= 2e7 nonzeros
+    r1 = int(np.searchsorted(rp, min(int(rp[-1]), 20_000_000), side="right")) - 1
+    nz1 = int(rp[r1])
+    t0 = time.perf_counter()
+    S.spmv_csr(rp[:r1 + 1], col[:nz1], val[:nz1], x, nthreads=1)
+    t1 = max(time.perf_counter() - t0, 1e-9)
+    cpu = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    import platform
     return {"value": 2.0 * coo.nnz * n / t_tot / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
-            "sample": f"{n} full passes over {wl} ({coo.nnz} nnz), long double, {cores} threads, {t_tot:.1f} s"}
+            "sample": f"{n} full passes over {wl} ({coo.nnz} nnz), long double, {cores} threads, {t_tot:.1f} s",
+            "value_1thread": 2.0 * nz1 / t1 / 1e9, "sample_1thread": f"first {r1} rows ({nz1} nnz)", "cpu": cpu,
+            "long_double": "x87 80-bit extended" if platform.machine() in ("x86_64", "AMD64") else platform.machine()}
 
 
 E2E_BANDS = 4  # ROW_DIV bands of the pipelined e2e plan (C2 sweep: 4 -> 0.94 ms, 8 -> 0.98, 16 -> 1.10)
@@ -429,6 +446,21 @@ def main():
                "graph": g_e, "launches_per_step": l_e,
                "candidates_ms": {("pipelined" if i else "searched"): r[0] for i, r in enumerate(res)}}
 
+    # warm steady state: back-to-back calls in one event window, no
+    # flush -- for C2 the working set is a small multiple of L2
+    warm = None
+    if not args.profile:
+        nw = 100 if t_ms < 1.0 else 20
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        w0.record(stream)
+        for _ in range(nw):
+            step()
+        w1.record(stream)
+        torch.cuda.synchronize()
+        wm = w0.elapsed_time(w1) / nw
+        warm = {"ms_per_step": wm, "gflops": 2.0 * nnz_local / (wm * 1e-3) / 1e9, "calls": nw}
+
     # CUDA-graph replay of the same plan (AS_PLAN_GRAPH): the launch-latency floor of small
     # matrices ("C1 also reports CUDA-Graph replay time"); small workloads only
     graph_replay = None
@@ -490,6 +522,8 @@ def main():
     }
     if graph_replay is not None:
         line["graph_replay"] = graph_replay
+    if warm is not None:
+        line["warm"] = warm
     if gather_ms is not None:
         line["exchange"] = {"kind": args.exchange, "ms": gather_ms,
                             "timed": "spmv + exchange per step (as_spmv_dist)" if args.exchange in ("nccl", "peer", "peer_halo")
