@@ -165,6 +165,15 @@ as_status_t as_spmv_host(as_plan_t, const void* alpha, const void* x_host, const
 as_status_t as_spmm(as_plan_t, int64_t k, const void* alpha, const void* X, int64_t ldx,
                     const void* beta, void* Y, int64_t ldy, void* stream);
 
+/* Per-launch profile (measurement): runs as_spmv (alpha 1, beta 0) `reps`
+ * times on `stream` with CUDA events between the launches and returns, per entry of
+ * as_plan_info_t.kernels ([pre-pass], parts in launch order, [heavy-row epilogue]), the mean
+ * device time in ms and the entry's algorithmic bytes under the plan's model (arrays read
+ * + x of the part's distinct columns + its y traffic; beta == 0).  ms == NULL or bytes ==
+ * NULL -> *n = number of entries.  Overwrites y. */
+as_status_t as_plan_profile(as_plan_t, const void* x, void* y, int reps, void* stream,
+                            double* ms, double* bytes, size_t* n);
+
 /* ---------------------------------------------------------------- a7: search
  * Random dependency-respecting graphs ("operators ... randomly chosen and connected
  * behind"; P:369 step 1) over a coarse parameter grid (P:369 step 2), each planned and

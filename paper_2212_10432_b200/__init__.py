@@ -88,6 +88,7 @@ _sig("as_plan_destroy", [_vp], None)
 _sig("as_spmv", [_vp, _vp, _vp, _vp, _vp, _vp])
 _sig("as_spmv_host", [_vp, _vp, _vp, _vp, _vp, _vp])
 _sig("as_spmm", [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp])
+_sig("as_plan_profile", [_vp, _vp, _vp, _i32, _vp, _vp, _vp, _P(_sz)])
 _sig("as_search", [_vp, _P(AsSearchCfg), _i32, _vp, _P(_vp), ctypes.c_char_p, _P(_sz)])
 _sig("as_random_graph", [_vp, ctypes.c_uint64, ctypes.c_char_p, _P(_sz)])
 _sig("as_graph_features", [_vp, _vp, _P(_sz)])
@@ -114,7 +115,7 @@ EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create
             "as_plan_keys", "as_plan_destroy", "as_spmv", "as_spmv_host", "as_search", "as_random_graph",
             "as_dist_row_cuts", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
             "as_dist_set_cuts", "as_dist_ipc_handle", "as_dist_open_peers", "as_spmv_dist", "as_dist_check",
-            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows", "as_fit_array_model", "as_spmm"]
+            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows", "as_fit_array_model", "as_spmm", "as_plan_profile"]
 
 
 class AsError(RuntimeError):
@@ -317,6 +318,19 @@ class Plan:
         """y = alpha*A*x + beta*y on device tensors (asynchronous on `stream`)."""
         a, b = self._scalars(alpha, beta)
         _ck(_lib.as_spmv(self._h, ctypes.byref(a), _ptr(x), ctypes.byref(b), _ptr(y), _stream_handle(stream)))
+
+    def profile(self, x, y, reps: int = 10, stream=None):
+        """Per-launch mean device time (ms) and algorithmic bytes (as_plan_profile):
+        list of (kernel name, ms, bytes) in as_plan_info.kernels order."""
+        n = _sz(0)
+        _ck(_lib.as_plan_profile(self._h, _ptr(x), _ptr(y), reps, _stream_handle(stream), None, None,
+                                 ctypes.byref(n)))
+        ms = np.zeros(n.value)
+        by = np.zeros(n.value)
+        _ck(_lib.as_plan_profile(self._h, _ptr(x), _ptr(y), reps, _stream_handle(stream), ms.ctypes.data,
+                                 by.ctypes.data, ctypes.byref(n)))
+        names = self.info()["kernels"].split(";")
+        return [(names[i] if i < len(names) else f"launch{i}", float(ms[i]), float(by[i])) for i in range(n.value)]
 
     def spmm(self, alpha, X, beta, Y, stream=None):
         """a5 with k right-hand sides (as_spmm): X (n x k), Y (m x k) row-major device tensors

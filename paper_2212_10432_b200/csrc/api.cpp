@@ -512,6 +512,66 @@ as_status_t as_spmv_host(as_plan_t h, const void* alpha, const void* x_host, con
   });
 }
 
+as_status_t as_plan_profile(as_plan_t h, const void* x, void* y, int reps, void* stream, double* ms, double* bytes,
+                            size_t* n) {
+  return guard([&] {
+    if (!h || !n) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    Plan& P = *h->P;
+    if (P.device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan");
+    // entries: [pre-pass], parts in launch order, [heavy-row epilogue] (as_plan_info.kernels)
+    const size_t L = P.launches.size();
+    const size_t cnt = (P.n_prepass ? 1 : 0) + L + (P.n_heavy ? 1 : 0);
+    if (!ms || !bytes) {
+      *n = cnt;
+      return;
+    }
+    if (*n < cnt) fail(AS_ERR_INVALID_ARG, "output arrays too small");
+    if ((P.n > 0 && !x) || (P.m > 0 && !y) || reps < 1) fail(AS_ERR_INVALID_ARG, "NULL x / y or reps < 1");
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != P.device) cudaSetDevice(P.device);
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<cudaEvent_t> ev(L + 2);
+    for (auto& e : ev) check_cuda(cudaEventCreate(&e), "event");
+    std::vector<double> acc(L + 2, 0.0);
+    int err = 0;
+    for (int r = 0; r < reps && !err; ++r) {
+      check_cuda(cudaEventRecord(ev[0], s), "event");
+      err = run_plan(
+          P, x, y, 1.0, 0.0, s, [&](size_t i) { if (i == 0) cudaEventRecord(ev[1], s); },
+          [&](size_t i) { cudaEventRecord(ev[i + 2], s); });
+      if (!err) err = (int)cudaStreamSynchronize(s);
+      if (err) break;
+      float t = 0;
+      if (L) cudaEventElapsedTime(&t, ev[0], ev[1]);
+      acc[0] += t;
+      for (size_t i = 0; i < L; ++i) {
+        cudaEventElapsedTime(&t, ev[i + 1], ev[i + 2]);
+        acc[i + 1] += t;
+      }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (!err && L == 0) cudaGetLastError();  // no launch: ev[1] was never recorded
+    if (cur != P.device) cudaSetDevice(cur);
+    if (err) fail(AS_ERR_CUDA, std::string("profile: ") + cudaGetErrorString((cudaError_t)err));
+    const size_t sv = P.dt == AS_R64F ? 8 : 4;
+    size_t o = 0;
+    if (P.n_prepass) {
+      ms[o] = acc[0] / reps;
+      bytes[o++] = P.prepass_bytes;
+    }
+    for (size_t i = 0; i < L; ++i) {
+      ms[o] = acc[i + 1] / reps;
+      bytes[o++] = i < P.launch_bytes.size() ? P.launch_bytes[i] : 0.0;
+    }
+    if (P.n_heavy) {  // the epilogue runs after the last part; its time is not separated
+      ms[o] = 0.0;
+      bytes[o++] = (double)P.n_heavy * (4 + 8 + 2 * sv);
+    }
+    *n = cnt;
+  });
+}
+
 as_status_t as_spmm(as_plan_t h, int64_t k, const void* alpha, const void* X, int64_t ldx, const void* beta, void* Y,
                     int64_t ldy, void* stream) {
   return guard([&] {

@@ -283,6 +283,7 @@ void Plan::upload(cudaStream_t s) {
   int max_smem = device_max_smem_optin(device);
   for (int64_t pi : host.launch_order) {
     const HostPart& h = host.parts[pi];
+    const double bytes_before = bytes_model;  // per-launch array bytes (as_plan_profile)
     DevPart d;
     d.fam = h.fam;
     d.dtype = dt == AS_R64F ? 1 : 0;
@@ -493,6 +494,7 @@ void Plan::upload(cudaStream_t s) {
     if (d.fam == FAM_BLOCK_OFFSET && d.variant == 1) fn += "_tma";
     launches.push_back(d);
     spans.push_back(part_span(h, host.n));
+    launch_bytes.push_back(bytes_model - bytes_before);
   }
   if (!host.prepass.empty()) {
     d_prepass = up_i32(host.prepass, s, "prepass");
@@ -549,10 +551,31 @@ void Plan::compute_model() {
     ybytes0 += 2 * at * sv;
     ybytes1 += 2 * at * sv;
   }
+  // per launch (as_plan_profile): + the x bytes of the part's distinct columns + its y traffic
+  if (launch_bytes.size() == host.launch_order.size()) {
+    std::vector<uint8_t> seen((size_t)host.n, 0);
+    for (size_t i = 0; i < host.launch_order.size(); ++i) {
+      const HostPart& h = host.parts[host.launch_order[i]];
+      int64_t xc = 0;
+      if (h.kind == "csr") {
+        std::fill(seen.begin(), seen.end(), 0);
+        for (int32_t c : h.col)
+          if (!seen[(size_t)c]) {
+            seen[(size_t)c] = 1;
+            ++xc;
+          }
+      } else if (i < spans.size() && spans[i].chi >= spans[i].clo) {
+        xc = spans[i].chi - spans[i].clo + 1;
+      }
+      const double ex = (double)h.excl.size(), at = (double)h.atom.size();
+      launch_bytes[i] += (double)xc * sv + (h.mode == 0 ? ex * sv : 2 * ex * sv) + 2 * at * sv;
+    }
+  }
   double pre = (double)host.prepass.size();
   // beta == 0: as_spmv fills all of y instead when that moves fewer bytes (api.cpp run_plan)
   double prebytes0 = (double)m * sv <= pre * (4 + 32) ? (double)m * sv : pre * (4 + sv);
   double prebytes1 = pre * (4 + 2 * sv);
+  prepass_bytes = pre ? prebytes0 : 0;
   info.bytes_model = bytes_model + host.distinct_cols * sv + ybytes0 + (pre ? prebytes0 : 0);
   info.bytes_model_beta = bytes_model + host.distinct_cols * sv + ybytes1 + (pre ? prebytes1 : 0);
   info.bytes_floor = nnz_real * (sv + 4) + host.n * sv + host.m * sv;

@@ -28,6 +28,8 @@ struct Plan {
     int64_t clo, chi, rlo, rhi;
   };
   std::vector<Span> spans;
+  std::vector<double> launch_bytes;  // per launch: algorithmic bytes (arrays + x + y), beta == 0
+  double prepass_bytes = 0;
   // every row's final value is produced by exactly one STORE (no pre-pass, no ADD parts,
   // no atomic rows, no fp32 heavy-row epilogue): as_spmv_dist may fuse peer stores
   bool single_writer = false;
