@@ -170,6 +170,28 @@ def test_graph_replay(graph):
         assert np.array_equal(dy.cpu().numpy(), yref), (graph, seed)
 
 
+@pytest.mark.parametrize("graph", [
+    "DIA_DECOM(theta=0.5) { DIA }",
+    "COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED",
+    "BIN(t=[4]) { COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED }"])
+def test_plan_profile(graph):
+    """as_plan_profile: one entry per kernel of as_plan_info.kernels, positive times, and
+    per-launch bytes that add up to the plan's bytes model when the parts' column sets are
+    disjoint (one part) -- the bench's dominant-kernel roofline rests on it."""
+    coo = synth.c2_lap2d(256)
+    P = asp.Plan(_mat(coo), graph, device=0)
+    x = torch.rand(coo.n, dtype=torch.float64, device="cuda")
+    y = torch.zeros(coo.m, dtype=torch.float64, device="cuda")
+    prof = P.profile(x, y, reps=3)
+    info = P.info()
+    assert [p[0] for p in prof] == info["kernels"].split(";")
+    assert all(p[1] > 0 for p in prof)
+    if info["n_parts"] == 1:
+        assert sum(p[2] for p in prof) == pytest.approx(info["bytes_model"], rel=1e-12)
+    P.spmv(1.0, x, 0.0, y)  # the plan still runs normally afterwards
+    torch.cuda.synchronize()
+
+
 LAP_CUTS = "cuts=[262144,524288,786432]"
 PIPE_GRAPHS = [
     f"ROW_DIV({LAP_CUTS}) {{ DIA_DECOM(theta=0.5) {{ DIA }} }}",
