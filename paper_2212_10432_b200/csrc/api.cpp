@@ -390,32 +390,6 @@ as_status_t as_spmv(as_plan_t h, const void* alpha, const void* x, const void* b
         P.gb = b;
       }
       if (!err) err = (int)cudaGraphLaunch(P.gexec, (cudaStream_t)stream);
-    } else if (std::getenv("AS_L2_PERSIST") && x && P.n > 0) {
-      // A/B knob: x inside an L2 access-policy window (persisting hits, streaming misses)
-      // for the duration of the call, so the matrix stream cannot evict it; the persisting
-      // lines are reset afterwards (no carry-over to the next call)
-      static int64_t persist_max = -1, window_max = 0;
-      if (persist_max < 0) {
-        int v = 0, w = 0;
-        cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, P.device);
-        cudaDeviceGetAttribute(&w, cudaDevAttrMaxAccessPolicyWindowSize, P.device);
-        persist_max = v;
-        window_max = w;
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v);
-      }
-      const size_t sv = P.dt == AS_R64F ? 8 : 4;
-      const size_t bytes = std::min<size_t>((size_t)P.n * sv, (size_t)window_max);
-      cudaStreamAttrValue at{}, old{};
-      cudaStreamGetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &old);
-      at.accessPolicyWindow.base_ptr = const_cast<void*>(x);
-      at.accessPolicyWindow.num_bytes = bytes;
-      at.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist_max / (double)std::max<size_t>(bytes, 1));
-      at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &at);
-      err = run_plan(P, x, y, a, b, (cudaStream_t)stream, [](size_t) {}, [](size_t) {});
-      cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &old);
-      if (!err) err = (int)cudaCtxResetPersistingL2Cache();
     } else {
       err = run_plan(P, x, y, a, b, (cudaStream_t)stream, [](size_t) {}, [](size_t) {});
     }
