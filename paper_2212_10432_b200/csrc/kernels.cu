@@ -1449,10 +1449,6 @@ __global__ void k_heavy_epilogue(const int32_t* __restrict__ rows, const double*
   }
 }
 
-template <class V>
-__global__ void k_scale_all(int64_t m, double beta, V* __restrict__ y) {
-  for (int64_t i = gtid(); i < m; i += gthreads()) y[i] = beta == 0.0 ? (V)0 : (V)(beta * (double)y[i]);
-}
 
 int sm_count() {
   static int n = 0;
@@ -1676,13 +1672,6 @@ int launch_l2_flush(void* buf, size_t bytes, int pattern, void* stream) {
   return (int)cudaGetLastError();
 }
 
-int launch_scale_all(int64_t m, double beta, void* y, int dtype, void* stream) {
-  if (m <= 0) return 0;
-  int64_t g = std::min<int64_t>((m + 255) / 256, 148 * 16);
-  if (dtype == 1) k_scale_all<double><<<g, 256, 0, (cudaStream_t)stream>>>(m, beta, (double*)y);
-  else k_scale_all<float><<<g, 256, 0, (cudaStream_t)stream>>>(m, beta, (float*)y);
-  return (int)cudaGetLastError();
-}
 
 int prepare_part(DevPart& p) {
   if (p.fam == FAM_BLOCK_OFFSET && p.variant == 1) {  // TMA-staged CSR-stream
