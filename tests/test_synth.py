@@ -56,3 +56,24 @@ def test_value_modes():
     assert set(np.unique(v).tolist()) <= {-4, -3, -2, -1, 1, 2, 3, 4}
     v = synth._fast_values(3, 10000, np.float64, False)
     assert v.min() >= -1 and v.max() < 1 and abs(v.mean()) < 0.05
+
+
+def test_lap2d_band_weak_scaling():
+    """bench.py's weak-scaled C2: band r of the grid x (grid*P) Laplacian; one band of a square
+    grid is C2 itself, and the P bands stacked are the whole taller Laplacian (nnz closed form
+    5*g*ny - 2*g - 2*ny)."""
+    import numpy as np
+    import synth
+    g = 32
+    full = synth.c2_lap2d(g)
+    b = synth.c2_lap2d_band(g, g, 0, g)
+    rp = np.zeros(full.m + 1, np.int64)
+    np.add.at(rp, full.row + 1, 1)
+    assert np.array_equal(np.cumsum(rp), b.row_ptr) and np.array_equal(full.col, b.col)
+    assert np.array_equal(full.val, b.val)
+    P = 3
+    bands = [synth.c2_lap2d_band(g, g * P, g * r, g * (r + 1)) for r in range(P)]
+    tall = synth.c2_lap2d_band(g, g * P, 0, g * P)
+    assert sum(x.nnz for x in bands) == tall.nnz == 5 * g * (g * P) - 2 * g - 2 * (g * P)
+    assert np.array_equal(np.concatenate([x.col for x in bands]), tall.col)
+    assert all(x.n == g * g * P for x in bands)
