@@ -164,7 +164,7 @@ __global__ void k_spmm_dia(DevPart p, double alpha, double beta, const V* __rest
 
 // DENSE part on the tensor cores: one CTA (8 warps) per tile row; per tile, the b x b tile
 // (column-major in HBM) and the b x 64 panel of X are staged in shared memory as fp64, and
-// warp w computes output rows [8w, 8w + 8) x 64 columns with m8n8k4 DMMA (8 accumulator
+// warp w computes a 16-row x 32-column block of Y with m8n8k4 DMMA (2 x 4 accumulator
 // blocks), for b <= 64 (tile rows/cols beyond b are zero-filled).  Columns are processed in
 // chunks of 64.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
@@ -194,9 +194,14 @@ __global__ void __launch_bounds__(256) k_spmm_dense_dmma(DevPart p, double alpha
     const int64_t I = __ldg(p.tile_row_id + tr);
     const int64_t t0 = __ldg(p.tile_row_ptr + tr), t1 = __ldg(p.tile_row_ptr + tr + 1);
     for (int64_t c0 = 0; c0 < k; c0 += kTB) {
-      double acc[8][2];
+      // warp w: rows [16*rp, 16*rp + 16) (two 8-row fragments) x columns [32*ch, 32*ch + 32)
+      // (four 8-column blocks): 2 A + 4 B fragment loads per 8 DMMAs
+      const int rp = warp >> 1, ch = warp & 1;
+      double acc[2][4][2];
 #pragma unroll
-      for (int nb = 0; nb < 8; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) acc[h][nb][0] = acc[h][nb][1] = 0.0;
       for (int64_t t = t0; t < t1; ++t) {
         const int64_t J = __ldg(p.tile_col + t);
         __syncthreads();  // previous tile consumed
@@ -222,24 +227,31 @@ __global__ void __launch_bounds__(256) k_spmm_dense_dmma(DevPart p, double alpha
         __syncthreads();
 #pragma unroll 4
         for (int kk = 0; kk < kTB; kk += 4) {
-          const double a = sT[(kk + tig) * kLd + warp * 8 + g];  // A[8w + g][kk + tig]
+          const double* tk = sT + (kk + tig) * kLd + rp * 16 + g;  // A[16rp + 8h + g][kk + tig]
+          const double a0 = tk[0], a1 = tk[8];
 #pragma unroll
-          for (int nb = 0; nb < 8; ++nb) {
-            const double bb = sX[(kk + tig) * kLd + nb * 8 + g];  // B[kk + tig][8nb + g]
-            dmma_8x8x4(acc[nb][0], acc[nb][1], a, bb);
+          for (int nb = 0; nb < 4; ++nb) {
+            const double bb = sX[(kk + tig) * kLd + ch * 32 + nb * 8 + g];  // B[kk + tig][32ch + 8nb + g]
+            dmma_8x8x4(acc[0][nb][0], acc[0][nb][1], a0, bb);
+            dmma_8x8x4(acc[1][nb][0], acc[1][nb][1], a1, bb);
           }
         }
       }
-      // D[g][2*tig + {0,1}] of block nb -> Y row 8w + g, columns c0 + 8nb + 2tig + {0,1}
-      const int64_t row = I * b + warp * 8 + g;
-      if (warp * 8 + g < b && row >= p.row_lo && row < p.row_hi) {
+      // D[g][2*tig + e] of (row fragment h, column block nb) -> Y row 16rp + 8h + g,
+      // column c0 + 32ch + 8nb + 2tig + e
 #pragma unroll
-        for (int nb = 0; nb < 8; ++nb)
+      for (int h = 0; h < 2; ++h) {
+        const int lr = rp * 16 + h * 8 + g;
+        const int64_t row = I * b + lr;
+        if (lr < b && row >= p.row_lo && row < p.row_hi) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int64_t c = c0 + nb * 8 + 2 * tig + h;
-            if (c < k) put(Y + row * ldy + c, acc[nb][h], alpha, beta, p.mode == 1);
-          }
+          for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int64_t c = c0 + ch * 32 + nb * 8 + 2 * tig + e;
+              if (c < k) put(Y + row * ldy + c, acc[h][nb][e], alpha, beta, p.mode == 1);
+            }
+        }
       }
     }
   }
