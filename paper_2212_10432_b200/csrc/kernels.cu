@@ -78,19 +78,14 @@ __device__ __forceinline__ uint64_t pol_el() {
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-#ifdef AS_X_L1_EVICT_LAST  // A/B build: x lines also kept longer in L1
-#define AS_XL1 ".L1::evict_last"
-#else
-#define AS_XL1 ""
-#endif
 __device__ __forceinline__ double ldx(const double* x, int64_t c) {
   double v;
-  asm volatile("ld.global.nc" AS_XL1 ".L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
   return v;
 }
 __device__ __forceinline__ double ldx(const float* x, int64_t c) {
   float v;
-  asm volatile("ld.global.nc" AS_XL1 ".L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
   return (double)v;
 }
 // metadata: small, reused by neighbours -> plain non-coherent load
