@@ -634,10 +634,20 @@ struct Builder {
       P.fam = FAM_BLOCK_OFFSET;
       P.fam_name = "block_offset";
     } else {
-      fail(AS_ERR_PLAN_INFEASIBLE, "no kernel in the sm_100a family implements this mapping/reduction combination");
+      P.fam = FAM_COMPOSE;
     }
-    if (P.pad && P.fam != FAM_THREAD_ROW && P.fam != FAM_NNZ_THREAD && P.fam != FAM_NNZ_WARP)
-      fail(AS_ERR_PLAN_INFEASIBLE, "BMT_PAD is implemented for the THREAD_ROW and NNZ kernels only");
+    // BMT_PAD is read by the THREAD_ROW and NNZ families and by the composed kernel
+    if (P.pad && P.fam != FAM_THREAD_ROW && P.fam != FAM_NNZ_THREAD && P.fam != FAM_NNZ_WARP) P.fam = FAM_COMPOSE;
+    if (P.fam == FAM_COMPOSE) {
+      // the Kernel Builder's per-level fragments: name = levels + reductions
+      static const char* rn[] = {"", "total", "bitmap", "seg", "offset"};
+      P.fam_name = "compose";
+      const char* ln[] = {"b", "w", "t"};
+      for (int l = 0; l < 3; ++l)
+        if (P.lv[l].present || P.red[l] != RED_NONE)
+          P.fam_name += std::string("_") + ln[l] + (P.red[l] != RED_NONE ? rn[P.red[l]] : "");
+      if (P.pad) P.fam_name += "_pad";
+    }
   }
 };
 

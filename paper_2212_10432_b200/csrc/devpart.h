@@ -16,8 +16,12 @@ enum Fam {
   FAM_BLOCK_TOTAL,   // BMTB_* (single-row) + SHMEM_TOTAL_RED
   FAM_BLOCK_OFFSET,  // BMTB_* + SHMEM_OFFSET_RED (CSR-stream)
   FAM_DIA,           // DIA part of DIA_DECOM
-  FAM_DENSE          // DENSE part of DENSE_DECOM
+  FAM_DENSE,         // DENSE part of DENSE_DECOM
+  FAM_COMPOSE        // any other legal level/reduction composition (compose.cu, P:313/P:322 adapters)
 };
+
+// reduction of one level (BMTB, BMW, BMT) of the implementing stage
+enum Red { RED_NONE = 0, RED_TOTAL = 1, RED_BITMAP = 2, RED_SEG = 3, RED_OFFSET = 4 };
 
 constexpr int kMaxDiags = 64;
 constexpr int kMaxPatches = 8;
@@ -76,6 +80,12 @@ struct DevPart {
   // CTA, and per (CTA, round) the [lo, hi] x range
   int64_t xw_size = 0, xw_grid = 0, xw_rpc = 0;
   const int32_t* xwin = nullptr;
+  // FAM_COMPOSE: per-level reductions (Red), which levels exist (a missing BMT level is
+  // uploaded as NNZ_BLOCK(1) BMTs), BMTB -> child block range (BMWs, else BMTs), and whether
+  // no level reduces below GMEM (every nonzero written on its own)
+  int tred = 0, wred = 0, bred = 0;
+  int has_w = 0, has_b = 0, per_elem = 0;
+  const int32_t* bmtb_child = nullptr;
   // BMT_PAD (slot-major interleaved)
   int pad = 0, vec = 1;
   int64_t n_grp = 0, grp_regular = 0;     // BMTs per group if regular, else 0
@@ -121,6 +131,9 @@ int launch_prepass(const int32_t* rows, int64_t n, double beta, void* y, int dty
 int launch_l2_flush(void* buf, size_t bytes, int pattern, void* stream);  // memset + read-back
 int launch_heavy_epilogue(const int32_t* rows, const double* acc, int64_t n, void* y, void* stream);  // fp32 y
 int prepare_part(DevPart& p);  // per-kernel attributes (smem opt-in); returns cudaError_t
+// compose.cu
+int launch_compose(const DevPart& p, const void* x, void* y, void* stream);
+int prepare_compose(DevPart& p);
 const char* fam_kernel_name(const DevPart& p);
 int device_max_smem_optin(int device);
 int device_sm_count(int device);

@@ -93,7 +93,6 @@ struct Matrix {
 };
 
 // ------------------------------------------------------------------ built format (host side)
-enum Red { RED_NONE = 0, RED_TOTAL = 1, RED_BITMAP = 2, RED_SEG = 3, RED_OFFSET = 4 };
 
 struct Level {
   bool present = false;

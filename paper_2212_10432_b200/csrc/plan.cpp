@@ -468,6 +468,98 @@ void Plan::upload(cudaStream_t s) {
           }
           break;
         }
+        case FAM_COMPOSE: {
+          // composed levels (compose.cu): packed row-head bits + each present level's block
+          // starts / first rows / child ranges; a missing BMT level runs as NNZ_BLOCK(1)
+          d.tred = h.red[2];
+          d.wred = h.red[1];
+          d.bred = h.red[0];
+          d.has_w = W.present;
+          d.has_b = B.present;
+          d.per_elem = h.red[0] == RED_NONE && h.red[1] == RED_NONE && h.red[2] == RED_NONE;
+          std::vector<uint32_t> bits((size_t)(nnz / 32 + 2), 0u);
+          for (int64_t r = 0; r < mp; ++r) bits[(size_t)(h.row_ptr[r] >> 5)] |= 1u << (h.row_ptr[r] & 31);
+          d.bits = (const uint32_t*)up(bits.data(), bits.size() * 4, s);
+          cudaStreamSynchronize(s);
+          bytes_model += (double)(bits.size() * 4);
+          std::vector<int64_t> tstart, tfirst;
+          const std::vector<int64_t>* ts = &T.start;
+          const std::vector<int64_t>* tf = &T.first_row;
+          if (!T.present) {
+            tstart.resize((size_t)nnz + 1);
+            tfirst.resize((size_t)nnz);
+            for (int64_t e = 0; e <= nnz; ++e) tstart[(size_t)e] = e;
+            for (int64_t r = 0; r < mp; ++r)
+              for (int64_t e = h.row_ptr[r]; e < h.row_ptr[r + 1]; ++e) tfirst[(size_t)e] = r;
+            ts = &tstart;
+            tf = &tfirst;
+          }
+          const int64_t nt = (int64_t)ts->size() - 1;
+          d.n_bmt = nt;
+          d.k = T.present ? (T.nnz ? T.size : 0) : 1;
+          std::vector<int64_t> st0(ts->begin(), ts->end() - 1);
+          if (!(d.k > 0 && is_affine(st0, d.k, 0))) {
+            d.k = 0;
+            d.bmt_start = up_i32(*ts, s, "bmt_start");
+            bytes_model += (double)(ts->size() * 4);
+          }
+          if (mdc && fit_array_model(*tf, kMaxPatches, &d.fr_model)) {
+            ++modeled_arrays;
+          } else {
+            d.bmt_first_row = up_i32(*tf, s, "bmt_first_row");
+            bytes_model += (double)(tf->size() * 4);
+          }
+          // child block range of every block of `lv` at the next present level
+          auto child_ptr = [&](const Level& lv, const std::vector<int64_t>& cstart) {
+            std::vector<int64_t> ptr((size_t)lv.count() + 1, 0);
+            int64_t c = 0;
+            const int64_t nc = (int64_t)cstart.size() - 1;
+            for (int64_t b = 0; b < lv.count(); ++b) {
+              ptr[(size_t)b] = c;
+              while (c < nc && cstart[(size_t)c] < lv.start[(size_t)b + 1]) ++c;
+            }
+            ptr[(size_t)lv.count()] = c;
+            return ptr;
+          };
+          if (W.present) {
+            d.n_bmw = W.count();
+            std::vector<int64_t> ptr = child_ptr(W, *ts);
+            const int64_t per = W.count() ? ptr[1] - ptr[0] : 0;
+            if (per > 0 && is_affine(ptr, per, 0, nt)) {
+              d.bmts_per_bmw = per;
+            } else {
+              d.bmw_bmt_ptr = up_i32(ptr, s, "bmw_bmt_ptr");
+              bytes_model += (double)(ptr.size() * 4);
+            }
+          }
+          if (B.present) {
+            d.n_bmtb = B.count();
+            std::vector<int64_t> bst(B.start.begin(), B.start.end() - 1);
+            if (B.nnz && is_affine(bst, B.size, 0)) {
+              d.k1 = B.size;
+            } else {
+              d.bmtb_start = up_i32(B.start, s, "bmtb_start");
+              bytes_model += (double)(B.start.size() * 4);
+            }
+            d.bmtb_first_row = up_i32(B.first_row, s, "bmtb_first_row");
+            std::vector<int64_t> cp = child_ptr(B, W.present ? W.start : *ts);
+            d.bmtb_child = up_i32(cp, s, "bmtb_child");
+            bytes_model += (double)((B.first_row.size() + cp.size()) * 4);
+            int64_t mx = 0;
+            for (int64_t b = 0; b < B.count(); ++b) mx = std::max(mx, B.start[b + 1] - B.start[b]);
+            d.max_block_nnz = mx;
+            if (h.red[0] == RED_OFFSET && mx * 8 > max_smem)
+              fail(AS_ERR_PLAN_INFEASIBLE, "P2: SHMEM_OFFSET_RED block of " + std::to_string(mx) +
+                                               " nonzeros exceeds the shared-memory opt-in limit");
+          }
+          need_rowptr = h.red[0] == RED_OFFSET;
+          if (h.pad) {
+            upload_pad(h, d, s);
+            need_colval = false;
+            d.pad_grp_bmw = (W.present && h.pad_scope == 1) ? 1 : 0;
+          }
+          break;
+        }
         default:
           fail(AS_ERR_PLAN_INFEASIBLE, "part without a kernel");
       }

@@ -19,7 +19,7 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 asp = pytest.importorskip("paper_2212_10432_b200")
 
-from test_host import FAMILY_GRAPHS, compare_export  # noqa: E402
+from test_host import COMPOSE_GRAPHS, FAMILY_GRAPHS, assert_infeasible_justified, compare_export  # noqa: E402
 
 
 def _mat(coo):
@@ -47,7 +47,7 @@ def run_check(coo, graph, alpha=1.0, beta=0.0, int_mode=False, seed=0, keep_host
     return P, ratio
 
 
-@pytest.mark.parametrize("graph", FAMILY_GRAPHS)
+@pytest.mark.parametrize("graph", FAMILY_GRAPHS + COMPOSE_GRAPHS)
 @pytest.mark.parametrize("seed", range(3))
 def test_family_integer_exact(graph, seed):
     coo = synth.random_matrix(33 + 40 * seed, 29 + 17 * seed, 0.12 + 0.06 * seed, seed, int_mode=True,
@@ -56,19 +56,19 @@ def test_family_integer_exact(graph, seed):
     try:
         P, _ = run_check(coo, graph, *ab, int_mode=True, seed=seed, keep_host=True)
     except asp.AsError as e:
-        assert e.status == "AS_ERR_PLAN_INFEASIBLE"
+        assert_infeasible_justified(coo, graph, e)
         return
     compare_export(P, coo, graph)
 
 
-@pytest.mark.parametrize("graph", FAMILY_GRAPHS)
+@pytest.mark.parametrize("graph", FAMILY_GRAPHS + COMPOSE_GRAPHS)
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_family_real(graph, dtype):
     coo = synth.random_powerlaw(700, 650, 3, 300).astype(dtype)
     try:
         run_check(coo, graph, 1.5, -0.5, seed=3)
     except asp.AsError as e:
-        assert e.status == "AS_ERR_PLAN_INFEASIBLE"
+        assert_infeasible_justified(coo, graph, e)
 
 
 @pytest.mark.parametrize("seed", range(30))
@@ -80,7 +80,7 @@ def test_random_graphs(seed):
     try:
         run_check(coo, text, 1.0 if seed % 4 else 2.0, 0.0 if seed % 3 else 1.0, int_mode=seed % 3 == 0, seed=seed)
     except asp.AsError as e:
-        assert e.status == "AS_ERR_PLAN_INFEASIBLE", (text, e)
+        assert_infeasible_justified(coo, text, e)
 
 
 @pytest.mark.parametrize("graph", [
@@ -125,7 +125,7 @@ def test_empty_and_degenerate():
         try:
             run_check(coo, g, 1.0, -1.0)
         except asp.AsError as e:
-            assert e.status == "AS_ERR_PLAN_INFEASIBLE"
+            assert_infeasible_justified(coo, g, e)
     coo = synth.random_matrix(300, 1, 1.0, 2)
     run_check(coo, "COMPRESS; BMT_NNZ_BLOCK(7); THREAD_BITMAP_RED_G; GMEM_ATOM_RED", 1.0, -1.0)
 

@@ -17,8 +17,8 @@ from oracle import spmv as S
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "canonical_4x4.json")))
 
 
-def _A():
-    a = GOLD["matrix"]
+def _A(name="matrix"):
+    a = GOLD[name]
     return a["m"], a["n"], np.array(a["row"]), np.array(a["col"]), np.array(a["val"], float)
 
 
@@ -112,7 +112,10 @@ def test_check_tolerance():
     bnd = np.array([1.0, 0.0], np.longdouble)
     assert S.check(np.array([1.0 + 5e-13, 2.0]), yref, bnd, np.float64)[0]
     assert not S.check(np.array([1.0 + 5e-12, 2.0]), yref, bnd, np.float64)[0]
-    assert not S.check(np.array([1.0, 2.0]), yref, np.array([1.0, 0.0], np.longdouble) * 0, np.float64)[0] or True
+    # a row whose bound is 0 (all its terms are 0) accepts only +-0, however small the error
+    y1, b1 = np.array([1.0, 0.0], np.longdouble), np.array([1.0, 0.0], np.longdouble)
+    assert not S.check(np.array([1.0, 1e-300]), y1, b1, np.float64)[0]
+    assert S.check(np.array([1.0, -0.0]), y1, b1, np.float64)[0]
     z = np.array([0.0], np.longdouble)
     assert S.check(np.array([-0.0]), z, z, np.float64)[0]          # bound 0 => y must be +-0
     assert not S.check(np.array([1e-300]), z, z, np.float64)[0]
@@ -168,9 +171,9 @@ def test_parse_errors():
 
 
 # ------------------------------------------------------------------ builder
-def _build(graph, coo=None, dtype=np.float64):
+def _build(graph, coo=None, dtype=np.float64, matrix="matrix"):
     if coo is None:
-        m, n, r, c, v = _A()
+        m, n, r, c, v = _A(matrix)
     else:
         m, n, r, c, v = coo.m, coo.n, coo.row, coo.col, coo.val
     csr = B.Csr(m, n, r, c, v)
@@ -180,11 +183,56 @@ def _build(graph, coo=None, dtype=np.float64):
 
 @pytest.mark.parametrize("case", GOLD["graphs"], ids=lambda c: c["graph"][:40])
 def test_builder_golden(case):
-    ex, _ = _build(case["graph"])
+    ex, _ = _build(case["graph"], matrix=case.get("matrix", "matrix"))
     for k, want in case["expect"].items():
         assert k in ex, k
         got = ex[k]
         assert got.tolist() == want, (k, got.tolist(), want)
+
+
+def _golden_failures():
+    bad = 0
+    for case in GOLD["graphs"]:
+        try:
+            ex, _ = _build(case["graph"], matrix=case.get("matrix", "matrix"))
+        except Exception:
+            bad += 1
+            continue
+        bad += any(k not in ex or ex[k].tolist() != w for k, w in case["expect"].items())
+    return bad
+
+
+@pytest.mark.parametrize("mutation", ["ascending", "unstable", "unrestarted_nnz", "unrestarted_row", "sort_sub_global"])
+def test_golden_pins_catch_mutations(monkeypatch, mutation):
+    """The hand-derived goldens must fail on plausible mistakes in the oracle's row
+    permutations (A7, A8, A19) and block cutting (A15): a reversed sort, an unstable sort,
+    children cut without restarting at their parent, SORT_SUB applied globally."""
+    assert _golden_failures() == 0
+    if mutation == "ascending":
+        monkeypatch.setattr(B, "_stable_desc", lambda L: np.argsort(np.asarray(L), kind="stable"))
+    elif mutation == "unstable":
+        # ties broken by descending position (a valid descending sort, but not stable)
+        monkeypatch.setattr(B, "_stable_desc", lambda L: np.lexsort((-np.arange(len(L)), -np.asarray(L))))
+    elif mutation == "sort_sub_global":
+        orig = B._stable_desc
+        monkeypatch.setattr(B, "_run_seq", _patched_run_seq_sort_sub_global(B._run_seq))
+    else:
+        kind = "NNZ" if mutation == "unrestarted_nnz" else "ROW"
+        orig_cut = B._cut
+
+        def cut(row_ptr, parents, k, size):
+            if k == kind and parents:   # ignore the parents: one global cut
+                return orig_cut(row_ptr, [(parents[0][0], parents[-1][1])], k, size)
+            return orig_cut(row_ptr, parents, k, size)
+        monkeypatch.setattr(B, "_cut", cut)
+    assert _golden_failures() > 0, mutation
+
+
+def _patched_run_seq_sort_sub_global(run_seq):
+    def patched(csr, seq, st, parts, dtype):
+        seq = [G.Op("SORT", {}, []) if op.name == "SORT_SUB" else op for op in seq]
+        return run_seq(csr, seq, st, parts, dtype)
+    return patched
 
 
 def reconstruct(ex, parts, m):

@@ -14,7 +14,7 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 asp = pytest.importorskip("paper_2212_10432_b200")
 
-from test_host import FAMILY_GRAPHS  # noqa: E402
+from test_host import COMPOSE_GRAPHS, FAMILY_GRAPHS, assert_infeasible_justified  # noqa: E402
 
 EXTRA = [
     "DIA_DECOM(theta=0.2,max=6) { DIA | COMPRESS; BMT_NNZ_BLOCK(5); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
@@ -69,7 +69,7 @@ def test_spmm_integer_exact(graph, k):
     try:
         run(coo, graph, k, 2.0, -1.0, True, k)
     except asp.AsError as e:
-        assert e.status == "AS_ERR_PLAN_INFEASIBLE"
+        assert_infeasible_justified(coo, graph, e)
 
 
 @pytest.mark.parametrize("graph", EXTRA + FAMILY_GRAPHS[::5])
@@ -80,7 +80,7 @@ def test_spmm_real(graph, dtype, k, beta):
     try:
         run(coo, graph, k, 1.5, beta, False, 7, pad=5)
     except asp.AsError as e:
-        assert e.status == "AS_ERR_PLAN_INFEASIBLE"
+        assert_infeasible_justified(coo, graph, e)
 
 
 def test_spmm_dense_tensor_core_blocks():

@@ -1,0 +1,192 @@
+// Gather roofline (developer measurement tool, not part of the product path).
+//
+// The irregular configs (C3 rmat-24, the C4 residual) are bound by the x gathers, not by
+// HBM: each nonzero reads one 32-byte L2 sector of x for 4 (fp32) or 8 (fp64) useful bytes.
+// These kernels measure the ceiling any SpMV over the same nonzeros must respect: stream
+// every (val, col) pair once and gather x[col] for it, with no reduction by row and no y
+// traffic.  Loads use the same cache policies as the product kernels (matrix streams
+// L1::no_allocate + L2 evict_first; x gathers through L1 with L2 evict_last), so the time
+// of k_gather on a matrix's own column array is the gather roofline of that matrix.
+//
+//   k_stream      : val + col only (no gather)            -> streaming floor
+//   k_gather      : val + col + x[col]                    -> gather roofline
+//   k_gather_hash : x[hash(i) % n], no col stream         -> random-sector L2 rate alone
+//   k_gather_hot  : as k_gather, columns < 0 read a shared-memory copy of the hot x entries
+//                   (~col), the rest x[col]               -> the hot-x cache's ceiling
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace {
+
+__device__ __forceinline__ uint64_t pol_ef() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_el() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_s4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol_ef()));
+  return v;
+}
+__device__ __forceinline__ double2 ld_s2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p), "l"(pol_ef()));
+  return v;
+}
+__device__ __forceinline__ int4 ld_si4(const int32_t* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol_ef()));
+  return v;
+}
+__device__ __forceinline__ int2 ld_si2(const int32_t* p) {
+  int2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p), "l"(pol_ef()));
+  return v;
+}
+__device__ __forceinline__ double ldx(const float* x, int64_t c) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  return (double)v;
+}
+__device__ __forceinline__ double ldx(const double* x, int64_t c) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
+  return v;
+}
+
+// 4 (fp32) / 2 (fp64) elements per vector, UNR vectors in flight per thread
+template <class V>
+struct Vec;
+template <>
+struct Vec<float> {
+  static constexpr int W = 4;
+  static __device__ __forceinline__ void ld(const float* v, const int32_t* c, double* vo, int32_t* co) {
+    float4 a = ld_s4(v);
+    int4 b = ld_si4(c);
+    vo[0] = a.x, vo[1] = a.y, vo[2] = a.z, vo[3] = a.w;
+    co[0] = b.x, co[1] = b.y, co[2] = b.z, co[3] = b.w;
+  }
+};
+template <>
+struct Vec<double> {
+  static constexpr int W = 2;
+  static __device__ __forceinline__ void ld(const double* v, const int32_t* c, double* vo, int32_t* co) {
+    double2 a = ld_s2(v);
+    int2 b = ld_si2(c);
+    vo[0] = a.x, vo[1] = a.y;
+    co[0] = b.x, co[1] = b.y;
+  }
+};
+
+constexpr int UNR = 4;
+
+template <class V, int MODE>  // MODE 0 stream, 1 gather, 2 gather with hot smem
+__global__ void __launch_bounds__(1024) k_gather(const V* __restrict__ val, const int32_t* __restrict__ col,
+                                                 const V* __restrict__ x, const V* __restrict__ xh, int nh,
+                                                 int64_t nnz, double* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  V* sh = (V*)smem;
+  if (MODE == 2) {
+    for (int i = threadIdx.x; i < nh; i += blockDim.x) sh[i] = xh[i];
+    __syncthreads();
+  }
+  constexpr int W = Vec<V>::W;
+  const int64_t nv = nnz / W;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (UNR - 1) * T < nv; i += UNR * T) {
+    double v[UNR * W];
+    int32_t c[UNR * W];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) Vec<V>::ld(val + (i + u * T) * W, col + (i + u * T) * W, v + u * W, c + u * W);
+    double xv[UNR * W];
+#pragma unroll
+    for (int q = 0; q < UNR * W; ++q) {
+      if (MODE == 0) xv[q] = (double)c[q];
+      else if (MODE == 1) xv[q] = ldx(x, c[q]);
+      else xv[q] = c[q] < 0 ? (double)sh[~c[q]] : ldx(x, c[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < UNR * W; ++q) acc += v[q] * xv[q];
+  }
+  for (; i < nv; i += T) {
+    double v[W];
+    int32_t c[W];
+    Vec<V>::ld(val + i * W, col + i * W, v, c);
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      double xv = MODE == 0 ? (double)c[q] : MODE == 1 ? ldx(x, c[q]) : (c[q] < 0 ? (double)sh[~c[q]] : ldx(x, c[q]));
+      acc += v[q] * xv;
+    }
+  }
+  if (acc == 1234.5678) out[0] = acc;  // keeps the loads live; practically never stores
+}
+
+__device__ __forceinline__ uint32_t mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return (uint32_t)(z ^ (z >> 31));
+}
+template <class V>
+__global__ void __launch_bounds__(1024) k_gather_hash(const V* __restrict__ x, int64_t n, int64_t count, double* out) {
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 7 * T < count; i += 8 * T) {
+    double xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xv[u] = ldx(x, (int64_t)(mix(i + u * T) % (uint64_t)n));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += xv[u];
+  }
+  for (; i < count; i += T) acc += ldx(x, (int64_t)(mix(i) % (uint64_t)n));
+  if (acc == 1234.5678) out[0] = acc;
+}
+
+}  // namespace
+
+extern "C" {
+// dtype 0 = fp32, 1 = fp64; mode 0 stream, 1 gather, 2 hot smem; returns cudaError_t
+int gr_launch(int dtype, int mode, const void* val, const int32_t* col, const void* x, const void* xh, int nh,
+              int64_t nnz, double* out, int grid, int tpb, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t sm = mode == 2 ? (size_t)nh * (dtype ? 8 : 4) : 0;
+#define L(V, M)                                                                                           \
+  do {                                                                                                    \
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_gather<V, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             (int)sm);                                                    \
+    k_gather<V, M><<<grid, tpb, sm, s>>>((const V*)val, col, (const V*)x, (const V*)xh, nh, nnz, out);    \
+  } while (0)
+  if (dtype == 0) {
+    if (mode == 0) L(float, 0);
+    else if (mode == 1) L(float, 1);
+    else L(float, 2);
+  } else {
+    if (mode == 0) L(double, 0);
+    else if (mode == 1) L(double, 1);
+    else L(double, 2);
+  }
+#undef L
+  return (int)cudaGetLastError();
+}
+int gr_launch_hash(int dtype, const void* x, int64_t n, int64_t count, double* out, int grid, int tpb, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == 0) k_gather_hash<float><<<grid, tpb, 0, s>>>((const float*)x, n, count, out);
+  else k_gather_hash<double><<<grid, tpb, 0, s>>>((const double*)x, n, count, out);
+  return (int)cudaGetLastError();
+}
+}

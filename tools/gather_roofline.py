@@ -1,0 +1,142 @@
+"""Gather roofline of the irregular configs (developer measurement tool; see gather_roofline.cu).
+
+    python tools/gather_roofline.py [--configs c3 c4] [--reps 15] > gpurun_out/gather.jsonl
+
+For each matrix: time (CUDA events, L2 flushed before every rep, median) of
+  stream   : read val + col once (no x)                      -> streaming floor
+  gather   : read val + col + x[col] in CSR order            -> the matrix's gather roofline
+  hot K    : gather with the K most referenced columns read from a shared-memory copy
+and of random-sector gathers from the same x (hash indices, no index stream).  Prints one JSON
+line per measurement with GB/s of algorithmic bytes (val + col + x + y as in the plan bytes
+model) and gathers/s.
+"""
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libgather_roofline.so")
+
+
+def build():
+    src = os.path.join(HERE, "gather_roofline.cu")
+    if not os.path.exists(SO) or os.path.getmtime(SO) < os.path.getmtime(src):
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                               "-lineinfo", "-shared", "-Xcompiler", "-fPIC", "-o", SO, src])
+    lib = ctypes.CDLL(SO)
+    lib.gr_launch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                              ctypes.c_int, ctypes.c_void_p]
+    lib.gr_launch_hash.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                   ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+    return lib
+
+
+def timeit(fn, reps, flush):
+    import torch
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(reps):
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts), min(ts)
+
+
+def load(name):
+    import synth
+    if name == "c3":
+        A = synth.c3_rmat_csr()
+        return "rmat-24", A.m, A.n, A.col, A.val
+    if name == "c4":
+        A, tiles = synth.c4_blockdense_csr()
+        b = 64
+        rows = np.repeat(np.arange(A.m, dtype=np.int64), np.diff(A.row_ptr))
+        key = (rows // b) * ((A.n + b - 1) // b) + A.col.astype(np.int64) // b
+        planted = tiles[:, 0] * ((A.n + b - 1) // b) + tiles[:, 1]
+        resid = ~np.isin(key, planted)
+        return "blockdense-8m residual", A.m, A.n, np.ascontiguousarray(A.col[resid]), np.ascontiguousarray(A.val[resid])
+    if name == "c5":
+        A = synth.c5_band_csr()
+        return "band-irreg-64m", A.m, A.n, A.col, A.val
+    raise ValueError(name)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", nargs="+", default=["c3", "c4"])
+    ap.add_argument("--reps", type=int, default=15)
+    ap.add_argument("--hot", nargs="+", type=int, default=[8192, 16384, 32768, 49152])
+    args = ap.parse_args()
+    import torch
+    lib = build()
+    dev = torch.device("cuda:0")
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    flush_buf = torch.empty(2 * torch.cuda.get_device_properties(0).L2_cache_size, dtype=torch.uint8, device=dev)
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def flush():
+        flush_buf.zero_()
+        flush_buf.view(torch.int64).sum()
+
+    for cfg in args.configs:
+        wl, m, n, col, val = load(cfg)
+        nnz = col.shape[0]
+        dt = 0 if val.dtype == np.float32 else 1
+        sv = val.itemsize
+        dcol = torch.from_numpy(col).to(dev)
+        dval = torch.from_numpy(val).to(dev)
+        x = torch.rand(n, dtype=torch.float32 if dt == 0 else torch.float64, device=dev)
+        s = torch.cuda.current_stream().cuda_stream
+        model = nnz * (sv + 4) + n * sv + m * sv  # plan bytes model (beta = 0) without metadata
+        base = {"config": wl, "nnz": nnz, "n": n, "dtype": "f32" if dt == 0 else "f64", "bytes_model": model}
+
+        def run(mode, colp, xh=None, nh=0, grid=2 * nsm, tpb=1024):
+            rc = lib.gr_launch(dt, mode, dval.data_ptr(), colp.data_ptr(), x.data_ptr(),
+                               xh.data_ptr() if xh is not None else 0, nh, nnz, out.data_ptr(), grid, tpb, s)
+            assert rc == 0, rc
+
+        for mode, name in [(0, "stream"), (1, "gather")]:
+            med, mn = timeit(lambda: run(mode, dcol), args.reps, flush)
+            print(json.dumps({**base, "kernel": name, "median_us": med * 1e3, "min_us": mn * 1e3,
+                              "model_gbs": model / (med * 1e-3) / 1e9, "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
+        cnt = np.bincount(col, minlength=n)
+        order = np.argsort(-cnt, kind="stable")
+        for K in args.hot:
+            if K * sv > 200 * 1024:
+                continue
+            hot = order[:K]
+            slot = np.full(n, -1, np.int64)
+            slot[hot] = np.arange(K)
+            enc = np.where(slot[col] >= 0, ~slot[col], col).astype(np.int32)
+            cover = float(cnt[hot].sum()) / nnz
+            denc = torch.from_numpy(enc).to(dev)
+            xh = x[torch.from_numpy(hot).to(dev)].contiguous()
+            med, mn = timeit(lambda: run(2, denc, xh, K, grid=nsm, tpb=1024), args.reps, flush)
+            print(json.dumps({**base, "kernel": f"gather_hot{K}", "hot_cover": cover, "median_us": med * 1e3,
+                              "min_us": mn * 1e3, "model_gbs": model / (med * 1e-3) / 1e9,
+                              "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
+            del denc
+        # random sectors alone: the same number of gathers, hashed indices, no index stream
+        med, mn = timeit(lambda: lib.gr_launch_hash(dt, x.data_ptr(), n, nnz, out.data_ptr(), 2 * nsm, 1024, s),
+                         args.reps, flush)
+        print(json.dumps({**base, "kernel": "hash_gather", "median_us": med * 1e3, "min_us": mn * 1e3,
+                          "gathers_per_s": nnz / (med * 1e-3), "sector_gbs": nnz * 32 / (med * 1e-3) / 1e9}), flush=True)
+        del dcol, dval, x
+
+
+if __name__ == "__main__":
+    main()
