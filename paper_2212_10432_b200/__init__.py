@@ -274,6 +274,7 @@ class Plan:
                  spmm: bool = False, graph_replay: bool = False):
         self.dtype = np.dtype(matrix.dtype) if matrix is not None else None
         self.device = device
+        self.m, self.n = matrix.shape if matrix is not None else (None, None)
         if _handle is not None:
             self._h = _vp(_handle)
             return
@@ -309,6 +310,33 @@ class Plan:
         _ck(_lib.as_plan_export(self._h, key.encode(), out.ctypes.data if out.size else None, ctypes.byref(n)))
         return out
 
+    def _check_dev(self, t, shape, name):
+        """Argument checks before the C-ABI call (A33): a torch tensor of the plan dtype, the
+        given shape, contiguous (vectors) or unit column stride (SpMM), on the plan's device.
+        A plain int is taken as a raw device pointer the caller vouches for."""
+        if isinstance(t, int):
+            return
+        if not hasattr(t, "data_ptr") or not hasattr(t, "is_cuda"):
+            raise AsError(1, f"{name}: expected a torch CUDA tensor or a raw device pointer")
+        import torch
+        want = torch.float64 if self.dtype == np.float64 else torch.float32
+        if t.dtype != want:
+            raise AsError(1, f"{name}: dtype {t.dtype} does not match the plan's {want}")
+        if not t.is_cuda or (self.device >= 0 and t.device.index != self.device):
+            raise AsError(1, f"{name}: tensor on {t.device}, plan on cuda:{self.device}")
+        if self.m is not None and tuple(t.shape) != tuple(shape):
+            raise AsError(1, f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+        if len(shape) == 1 and not t.is_contiguous():
+            raise AsError(1, f"{name}: must be contiguous")
+
+    def _check_host(self, a, length, name, writable=False):
+        if not isinstance(a, np.ndarray) or a.dtype != self.dtype or a.ndim != 1 or not a.flags.c_contiguous:
+            raise AsError(1, f"{name}: expected a contiguous 1-D numpy array of {self.dtype}")
+        if self.m is not None and a.shape[0] != length:
+            raise AsError(1, f"{name}: length {a.shape[0]}, expected {length}")
+        if writable and not a.flags.writeable:
+            raise AsError(1, f"{name}: read-only array")
+
     def _scalars(self, alpha, beta):
         if self.dtype == np.float64:
             return ctypes.c_double(alpha), ctypes.c_double(beta)
@@ -316,6 +344,8 @@ class Plan:
 
     def spmv(self, alpha, x, beta, y, stream=None):
         """y = alpha*A*x + beta*y on device tensors (asynchronous on `stream`)."""
+        self._check_dev(x, (self.n,), "x")
+        self._check_dev(y, (self.m,), "y")
         a, b = self._scalars(alpha, beta)
         _ck(_lib.as_spmv(self._h, ctypes.byref(a), _ptr(x), ctypes.byref(b), _ptr(y), _stream_handle(stream)))
 
@@ -337,12 +367,16 @@ class Plan:
         with unit column stride; plan built with spmm=True."""
         if X.dim() != 2 or Y.dim() != 2 or X.stride(1) != 1 or Y.stride(1) != 1 or X.shape[1] != Y.shape[1]:
             raise AsError(1, "X (n x k) and Y (m x k) must be 2-D row-major with matching k")
+        self._check_dev(X, (self.n, X.shape[1]), "X")
+        self._check_dev(Y, (self.m, X.shape[1]), "Y")
         a, b = self._scalars(alpha, beta)
         _ck(_lib.as_spmm(self._h, X.shape[1], ctypes.byref(a), _ptr(X), X.stride(0), ctypes.byref(b), _ptr(Y),
                          Y.stride(0), _stream_handle(stream)))
 
     def spmv_host(self, alpha, x: np.ndarray, beta, y: np.ndarray, stream=None):
         """Same with host arrays (copies inside; synchronous)."""
+        self._check_host(x, self.n, "x")
+        self._check_host(y, self.m, "y", writable=True)
         a, b = self._scalars(alpha, beta)
         _ck(_lib.as_spmv_host(self._h, ctypes.byref(a), x.ctypes.data, ctypes.byref(b), y.ctypes.data,
                               _stream_handle(stream)))

@@ -594,6 +594,9 @@ as_status_t as_spmm(as_plan_t h, int64_t k, const void* alpha, const void* X, in
     cudaGetDevice(&cur);
     if (cur != P.device) cudaSetDevice(P.device);
     const int dtc = P.dt == AS_R64F ? 1 : 0;
+    for (const DevPart& d : P.launches)  // validate every part before the first launch
+      if (d.fam == FAM_DENSE && d.b > 64)
+        fail(AS_ERR_PLAN_INFEASIBLE, "as_spmm: DENSE tiles larger than 64 are not implemented for SpMM");
     int err = 0;
     if (P.n_prepass) {  // same rule as the SpMV: a fill of all rows when it moves fewer bytes (beta == 0)
       if (b == 0.0 && (double)P.m * sv <= (double)P.n_prepass * (4 + 32))

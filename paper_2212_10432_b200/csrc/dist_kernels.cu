@@ -90,12 +90,17 @@ int launch_push(const void* src, PeerPush pp, unsigned* ctr, unsigned* target, u
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t g = std::max<int64_t>(1, std::min<int64_t>((cnt + 511) / 512, (int64_t)sms * 2));
-  *target += (unsigned)g;
+  // the CTA arrival counter is monotonic; this call's CTAs bring it to `want`.  The host
+  // target advances only once the launch is known to have been accepted, so a failed launch
+  // cannot leave it ahead of the device counter (which would stall every later epoch)
+  const unsigned want = *target + (unsigned)g;
   cudaStream_t s = (cudaStream_t)stream;
-  if (esz == 16) k_push<uint4><<<g, 512, 0, s>>>((const uint4*)src, pp, ctr, *target, epoch, rank);
-  else if (esz == 8) k_push<uint64_t><<<g, 512, 0, s>>>((const uint64_t*)src, pp, ctr, *target, epoch, rank);
-  else k_push<uint32_t><<<g, 512, 0, s>>>((const uint32_t*)src, pp, ctr, *target, epoch, rank);
-  return (int)cudaGetLastError();
+  if (esz == 16) k_push<uint4><<<g, 512, 0, s>>>((const uint4*)src, pp, ctr, want, epoch, rank);
+  else if (esz == 8) k_push<uint64_t><<<g, 512, 0, s>>>((const uint64_t*)src, pp, ctr, want, epoch, rank);
+  else k_push<uint32_t><<<g, 512, 0, s>>>((const uint32_t*)src, pp, ctr, want, epoch, rank);
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) *target = want;
+  return (int)e;
 }
 
 int launch_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch,

@@ -604,6 +604,11 @@ void Plan::upload(cudaStream_t s) {
 // units of this part in the SpMV, so its value was initialised by the pre-pass or an earlier
 // part; SpMM adds this part's whole-row partial).  Exclusive rows of a STORE part store.
 void Plan::upload_spmm(cudaStream_t s) {
+  // the SpMM DENSE kernel (k_spmm_dense_dmma) holds tiles of b <= 64; reject larger tiles at
+  // plan time so as_spmm never launches a prefix of the parts and then fails on a later one
+  for (int64_t pi : host.launch_order)
+    if (host.parts[pi].kind == "dense" && host.parts[pi].b > 64)
+      fail(AS_ERR_PLAN_INFEASIBLE, "AS_PLAN_SPMM: DENSE tiles larger than 64 are not implemented for SpMM");
   std::vector<uint8_t> atom((size_t)m, 0);
   for (int64_t pi : host.launch_order) {
     const HostPart& h = host.parts[pi];

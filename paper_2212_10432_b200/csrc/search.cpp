@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <memory>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -282,6 +284,9 @@ std::string random_graph(const Matrix& A, uint64_t seed) {
   return gen_path(r, st, true, true, true, 0);
 }
 
+// internal status of a candidate whose y failed verification (never returned by the ABI)
+constexpr as_status_t kWrongResult = (as_status_t)100;
+
 as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device, void* stream, as_plan_t* best,
                         char* best_graph, size_t* len) {
   using clk = std::chrono::steady_clock;
@@ -317,6 +322,83 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       flush = dev_alloc(flush_bytes, stream);
     }
   }
+  // Verification (every measured design must compute the right y; the returned one is
+  // re-verified): after its timed reps each candidate runs once more with
+  // alpha = 1, beta = 0.5 on a known y0, and the result is compared row by row with a host
+  // CSR reference in double within north_star's tolerance (1e-12 fp64 / 1e-5 fp32 times
+  // sum|a_ij x_j| + |beta y0_i|, plus the reference's own rounding).  A candidate that fails
+  // is logged "wrong_result" and never kept.
+  std::vector<double> xh(A.n), y0h(A.m);
+  void* dy0 = dev_alloc(std::max<size_t>(16, A.m * sv), stream);
+  {
+    std::vector<double> xd(A.n);
+    uint64_t z = cfg->seed | 1;
+    for (auto& v : xd) {
+      z ^= z << 13;
+      z ^= z >> 7;
+      z ^= z << 17;
+      v = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    }
+    for (int64_t j = 0; j < A.n; ++j) xh[j] = sv == 8 ? xd[j] : (double)(float)xd[j];
+    for (int64_t i = 0; i < A.m; ++i) y0h[i] = (double)((i * 7919) % 17 - 8) / 8.0;  // exact in fp32
+    if (sv == 8) {
+      check_cuda(cudaMemcpy(dy0, y0h.data(), A.m * 8, cudaMemcpyHostToDevice), "H2D y0");
+    } else {
+      std::vector<float> f(y0h.begin(), y0h.end());
+      check_cuda(cudaMemcpy(dy0, f.data(), A.m * 4, cudaMemcpyHostToDevice), "H2D y0");
+    }
+  }
+  const double vbeta = 0.5, tol = sv == 8 ? 1e-12 : 1e-5;
+  struct Ref {
+    std::vector<double> y, bound, slack;
+  };
+  auto make_ref = [&](const Matrix& Mx) {
+    Ref r;
+    r.y.resize(Mx.m);
+    r.bound.resize(Mx.m);
+    r.slack.resize(Mx.m);
+    parallel_for(Mx.m, [&](int64_t a, int64_t e) {
+      for (int64_t i = a; i < e; ++i) {
+        double s = 0, ab = 0;
+        for (int64_t k = Mx.row_ptr[i]; k < Mx.row_ptr[i + 1]; ++k) {
+          const double p = Mx.val[k] * xh[Mx.col[k]];
+          s += p;
+          ab += std::fabs(p);
+        }
+        r.y[i] = s + vbeta * y0h[i];
+        r.bound[i] = ab + std::fabs(vbeta * y0h[i]);
+        r.slack[i] = (double)(Mx.row_ptr[i + 1] - Mx.row_ptr[i] + 2) * 0x1p-52 * r.bound[i];
+      }
+    });
+    return r;
+  };
+  std::unique_ptr<Ref> ref_full, ref_sample;
+  std::vector<double> ybuf;
+  auto verify = [&](as_plan_s& h, const Matrix& Mx) -> bool {
+    std::unique_ptr<Ref>& R = (&Mx == &A) ? ref_full : ref_sample;
+    if (!R) R.reset(new Ref(make_ref(Mx)));
+    check_cuda(cudaMemcpyAsync(dy, dy0, Mx.m * sv, cudaMemcpyDeviceToDevice, s), "y0");
+    double vb = vbeta, va = 1.0;
+    float vbf = (float)vbeta, vaf = 1.0f;
+    if (as_spmv(&h, sv == 8 ? (const void*)&va : (const void*)&vaf, dx, sv == 8 ? (const void*)&vb : (const void*)&vbf, dy, stream) != AS_OK)
+      fail(AS_ERR_CUDA, as_last_error());
+    ybuf.resize(Mx.m);
+    if (sv == 8) {
+      check_cuda(cudaMemcpyAsync(ybuf.data(), dy, Mx.m * 8, cudaMemcpyDeviceToHost, s), "D2H y");
+      check_cuda(cudaStreamSynchronize(s), "verify");
+    } else {
+      std::vector<float> f(Mx.m);
+      check_cuda(cudaMemcpyAsync(f.data(), dy, Mx.m * 4, cudaMemcpyDeviceToHost, s), "D2H y");
+      check_cuda(cudaStreamSynchronize(s), "verify");
+      for (int64_t i = 0; i < Mx.m; ++i) ybuf[i] = f[i];
+    }
+    std::atomic<bool> ok{true};
+    parallel_for(Mx.m, [&](int64_t a, int64_t e) {
+      for (int64_t i = a; i < e && ok.load(std::memory_order_relaxed); ++i)
+        if (!(std::fabs(ybuf[i] - R->y[i]) <= tol * R->bound[i] + R->slack[i])) ok = false;
+    });
+    return ok.load();
+  };
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -350,6 +432,7 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       ts.push_back(ms);
     }
     t_med = median(ts);
+    if (!verify(h, M)) fail(kWrongResult, "wrong_result: y differs from the host reference");
     return h.P.release();
   };
   auto logline = [&](int i, const std::string& g, const char* status, double t) {
@@ -411,7 +494,11 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       set_last_error(e.msg);
       if (!canon.empty()) seen.insert(canon);
       logline(i, canon.empty() ? text : canon,
-              e.st == AS_ERR_PLAN_INFEASIBLE ? "infeasible" : e.st == AS_ERR_CUDA ? "cuda_error" : "rejected", -1);
+              e.st == AS_ERR_PLAN_INFEASIBLE  ? "infeasible"
+              : e.st == AS_ERR_CUDA           ? "cuda_error"
+              : e.st == kWrongResult ? "wrong_result"
+                                               : "rejected",
+              -1);
     }
     return {t_med, canon};
   };
@@ -581,7 +668,26 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       }
     }
   }
+  // the returned plan is re-verified on the full matrix (A30: rebuilt from its canonical text
+  // by the confirm / final stages, or the coarse-stage plan itself)
+  if (best_plan) {
+    as_plan_s h;
+    h.P.reset(best_plan);
+    bool good = false;
+    try {
+      good = verify(h, A);
+    } catch (const Error&) {
+      cudaGetLastError();
+    }
+    best_plan = h.P.release();
+    if (!good) {
+      logline(-3, best_canon, "final_wrong_result", best_t);
+      delete best_plan;
+      best_plan = nullptr;
+    }
+  }
   if (log) std::fclose(log);
+  dev_free(dy0, stream);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   dev_free(dx, stream);

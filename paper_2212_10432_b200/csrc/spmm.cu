@@ -272,13 +272,11 @@ int spmm_part_t(const DevPart& p, const SpmmPart& s, double alpha, double beta, 
     k_spmm_dia<V><<<grid_of(p.mb * k, 256), 256, 0, st>>>(p, alpha, beta, X, ldx, Y, ldy, k);
   } else if (p.fam == FAM_DENSE) {
     if (p.b > kTB) return (int)cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(k_spmm_dense_dmma<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)kDenseSmem);
-      if (e != cudaSuccess) return (int)e;
-      attr = true;
-    }
+    // the shared-memory opt-in is a per-device function attribute: set it for the device
+    // this launch runs on (idempotent and cheap; no process-wide cache to go stale or race)
+    cudaError_t e = cudaFuncSetAttribute(k_spmm_dense_dmma<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kDenseSmem);
+    if (e != cudaSuccess) return (int)e;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(p.n_tile_rows, 148 * 8));
     k_spmm_dense_dmma<V><<<g, 256, kDenseSmem, st>>>(p, alpha, beta, X, ldx, Y, ldy, k);
   } else {

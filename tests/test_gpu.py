@@ -141,6 +141,15 @@ def test_preconditions():
     hp = asp.Plan(_mat(coo), FAMILY_GRAPHS[0], device=-1)
     with pytest.raises(asp.AsError):
         hp.spmv(1.0, buf[0:8], 0.0, buf[32:40])     # host-only plan
+    # the binding checks dtype, length, contiguity and device before the C-ABI call
+    with pytest.raises(asp.AsError):
+        P.spmv(1.0, buf[0:8].float(), 0.0, buf[32:40])  # fp32 x on an fp64 plan
+    with pytest.raises(asp.AsError):
+        P.spmv(1.0, buf[0:7], 0.0, buf[32:40])          # x too short
+    with pytest.raises(asp.AsError):
+        P.spmv(1.0, buf[0:16:2], 0.0, buf[32:40])       # strided x
+    with pytest.raises(asp.AsError):
+        P.spmv(1.0, buf[0:8].cpu(), 0.0, buf[32:40])    # host tensor
 
 
 def test_spmv_host_path():
@@ -306,3 +315,25 @@ def test_search_small():
                             seed_graphs=["COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED"])
     assert G.is_legal(text), text
     run_check(coo, text, 1.0, 0.0, plan=best)
+
+
+def test_search_verifies_and_beats_seed(tmp_path):
+    """a7 pins (SURVEY §8(c) search row): the CSR-Scalar seed is timed
+    first, no candidate's y fails the search's own verification, the winner validates and
+    passes O2, and its confirmed median is no slower than the seed's (within the 1 % tie
+    band of A29)."""
+    import json
+    coo = synth.random_powerlaw(20000, 20000, 6, 3000).astype(np.float32)
+    A = _mat(coo)
+    log = str(tmp_path / "search.jsonl")
+    seed = "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED"
+    best, text = asp.search(A, device=0, seed=11, max_candidates=16, budget_seconds=60, warmup=2, reps=7,
+                            seed_graphs=[seed], log_path=log)
+    rows = [json.loads(l) for l in open(log)]
+    assert rows[0]["graph"] == str(asp.Graph(seed)) and rows[0]["median_ms"] > 0
+    assert not any(r["status"].endswith("wrong_result") for r in rows)
+    assert G.is_legal(text), text
+    run_check(coo, text, 1.5, -0.5, plan=best)
+    seed_t = rows[0]["median_ms"]
+    best_t = min(r["median_ms"] for r in rows if r["median_ms"] > 0 and r["graph"] == text)
+    assert best_t <= seed_t * 1.01, (best_t, seed_t)

@@ -371,3 +371,17 @@ def test_dist_unique_id():
         assert e.status == "AS_ERR_NCCL"
         pytest.skip("NCCL not loadable here")
     assert len(a) == asp.AS_DIST_ID_BYTES and a != asp.Dist.unique_id()
+
+
+def test_binding_checks_host_arrays():
+    """Plan.spmv_host refuses arrays of the wrong dtype / length before the C-ABI call
+    (a float32 or short y would otherwise be overrun by the device-to-host copy)."""
+    coo = synth.random_matrix(20, 16, 0.3, 3)
+    P = asp.Plan(_mat(coo), "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED", device=-1)
+    x, y = np.zeros(16), np.zeros(20)
+    for bad in [(x.astype(np.float32), y), (x, y.astype(np.float32)), (x[:15], y), (x, y[:19]), (x, y[::2])]:
+        with pytest.raises(asp.AsError):
+            P.spmv_host(1.0, bad[0], 0.0, bad[1])
+    y.flags.writeable = False
+    with pytest.raises(asp.AsError):
+        P.spmv_host(1.0, x, 0.0, y)
