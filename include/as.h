@@ -232,6 +232,10 @@ as_status_t as_set_allocator(void* (*alloc)(size_t bytes, void* stream, void* ct
 /* ---------------------------------------------------------------- e: multi-GPU helpers
  * nnz-balanced ROW_DIV cuts over `world` ranks (reading A35): cuts[world+1]. */
 as_status_t as_dist_row_cuts(as_matrix_t, int world, int64_t* cuts);
+/* The same cuts from a host row_ptr[m+1] alone (int64, non-decreasing, row_ptr[0] = 0):
+ * ranks that generate or load only their own band (C5 at 10^9 nonzeros) agree on the cuts
+ * without building the whole matrix.  AS_ERR_INVALID_ARG on NULL, m < 0, world < 1. */
+as_status_t as_dist_row_cuts_ptr(const int64_t* row_ptr, int64_t m, int world, int64_t* cuts);
 /* Column span [*lo, *hi] referenced by the matrix (a ROW_DIV band): the x rows a rank needs
  * from its peers when y becomes the next x (halo exchange).  An empty
  * matrix gives lo = 0, hi = -1. */

@@ -56,7 +56,9 @@ SCHEMA: dict[str, list[tuple[str, str, Any]]] = {
     "BMT_NNZ_BLOCK": [("nnz", "int", None)],
     "BMT_PAD": [("scope", "scope", "GLOBAL"), ("vec", "int", 0)],
     "SORT_BMTB": [],
-    "SET_RESOURCE": [("tpb", "int", 256), ("grid", "int", 0), ("stages", "int", 2)],
+    # stages / xcache: shared-memory resource choices of the implementing stage (TMA staging of
+    # CSR-stream blocks; x entries staged per CTA); they do not change what y is (R-xcache)
+    "SET_RESOURCE": [("tpb", "int", 256), ("grid", "int", 0), ("stages", "int", 2), ("xcache", "int", 0)],
     **{r: [] for r in REDUCTIONS},
 }
 ALIASES = {"WARP_SEG_RED": "WARP_SEG_ADD_RED", "THREAD_BITMAP_RED": "THREAD_BITMAP_RED_G",
@@ -316,8 +318,9 @@ def _check_params(op: Op, nid: int):
         if p["vec"] not in (0, 1, 2, 4):
             bad("vec in {0,1,2,4}")
     elif op.name == "SET_RESOURCE":
-        if p["tpb"] < 32 or p["tpb"] > 1024 or p["tpb"] % 32 or p["grid"] < 0 or p["stages"] not in (0, 2):
-            bad("tpb multiple of 32 in [32,1024], grid >= 0, stages in {0,2}")
+        if (p["tpb"] < 32 or p["tpb"] > 1024 or p["tpb"] % 32 or p["grid"] < 0 or p["stages"] not in (0, 2)
+                or not 0 <= p["xcache"] <= 65536):
+            bad("tpb multiple of 32 in [32,1024], grid >= 0, stages in {0,2}, xcache in [0,65536]")
 
 
 def validate(seq):

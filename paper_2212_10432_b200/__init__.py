@@ -95,6 +95,7 @@ _sig("as_graph_features", [_vp, _vp, _P(_sz)])
 _sig("as_fit_array_model", [_vp, _sz, _i32, _vp])
 _sig("as_surrogate_fit_predict", [_vp, _vp, _sz, _sz, _vp, _sz, _vp])
 _sig("as_dist_row_cuts", [_vp, _i32, _vp])
+_sig("as_dist_row_cuts_ptr", [_vp, _i64, _i32, _vp])
 _sig("as_matrix_col_span", [_vp, _vp, _vp])
 _ALLOC_T = ctypes.CFUNCTYPE(_vp, _sz, _vp, _vp)
 _FREE_T = ctypes.CFUNCTYPE(None, _vp, _vp, _vp)
@@ -113,7 +114,7 @@ EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create
             "as_matrix_stats", "as_matrix_row_slice", "as_matrix_export_csr", "as_matrix_destroy", "as_graph_parse",
             "as_graph_print", "as_graph_destroy", "as_plan", "as_plan_ex", "as_plan_info", "as_plan_export",
             "as_plan_keys", "as_plan_destroy", "as_spmv", "as_spmv_host", "as_search", "as_random_graph",
-            "as_dist_row_cuts", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
+            "as_dist_row_cuts", "as_dist_row_cuts_ptr", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
             "as_dist_set_cuts", "as_dist_ipc_handle", "as_dist_open_peers", "as_spmv_dist", "as_dist_check",
             "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows", "as_fit_array_model", "as_spmm", "as_plan_profile"]
 
@@ -385,6 +386,14 @@ class Plan:
         if getattr(self, "_h", None) and _lib:
             _lib.as_plan_destroy(self._h)
             self._h = None
+
+
+def row_cuts_from_ptr(row_ptr, world: int) -> np.ndarray:
+    """as_dist_row_cuts_ptr: nnz-balanced ROW_DIV cuts (reading A35) from a row_ptr alone."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cuts = np.zeros(world + 1, np.int64)
+    _ck(_lib.as_dist_row_cuts_ptr(rp.ctypes.data, rp.shape[0] - 1, world, cuts.ctypes.data))
+    return cuts
 
 
 def search(matrix: Matrix, device: int = 0, stream=None, seed: int = 1, max_candidates: int = 32,

@@ -644,6 +644,15 @@ as_status_t as_matrix_col_span(as_matrix_t M, int64_t* lo, int64_t* hi) {
   });
 }
 
+as_status_t as_dist_row_cuts_ptr(const int64_t* row_ptr, int64_t m, int world, int64_t* cuts) {
+  return guard([&] {
+    if (!row_ptr || !cuts || m < 0 || world < 1) fail(AS_ERR_INVALID_ARG, "NULL argument, m < 0 or world < 1");
+    std::vector<int64_t> rp(row_ptr, row_ptr + m + 1);
+    auto c = row_cuts(rp, world);
+    std::memcpy(cuts, c.data(), c.size() * 8);
+  });
+}
+
 as_status_t as_dist_row_cuts(as_matrix_t M, int world, int64_t* cuts) {
   return guard([&] {
     if (!M || !cuts) fail(AS_ERR_INVALID_ARG, "NULL argument");

@@ -398,6 +398,7 @@ struct Builder {
         P.tpb = (int)op.geti("tpb");
         P.grid = (int)op.geti("grid");
         P.stages = (int)op.geti("stages");
+        P.xcache = op.geti("xcache");
       } else if (nm == "THREAD_TOTAL_RED") P.red[2] = RED_TOTAL;
       else if (nm == "THREAD_BITMAP_RED_G") P.red[2] = RED_BITMAP;
       else if (nm == "WARP_TOTAL_RED") P.red[1] = RED_TOTAL;

@@ -86,6 +86,11 @@ struct DevPart {
   int tred = 0, wred = 0, bred = 0;
   int has_w = 0, has_b = 0, per_elem = 0;
   const int32_t* bmtb_child = nullptr;
+  // hot-x cache (SET_RESOURCE xcache): xh_n columns staged in shared memory per CTA, encoded
+  // as ~slot in col / pad_col; persistent grid of xh_ctas CTAs per SM
+  const int32_t* xh_cols = nullptr;
+  int64_t xh_n = 0;
+  int xh_ctas = 0;
   // BMT_PAD (slot-major interleaved)
   int pad = 0, vec = 1;
   int64_t n_grp = 0, grp_regular = 0;     // BMTs per group if regular, else 0

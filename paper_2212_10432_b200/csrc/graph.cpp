@@ -54,7 +54,8 @@ const std::vector<OpSpec>& specs() {
       {"BMT_PAD", 2, {{"scope", P_SCOPE, true, 0, "GLOBAL"}, {"vec", P_INT, true, 0, nullptr}}},
       {"SORT_BMTB", 2, {}},
       {"SET_RESOURCE", 3,
-       {{"tpb", P_INT, true, 256, nullptr}, {"grid", P_INT, true, 0, nullptr}, {"stages", P_INT, true, 2, nullptr}}},
+       {{"tpb", P_INT, true, 256, nullptr}, {"grid", P_INT, true, 0, nullptr}, {"stages", P_INT, true, 2, nullptr},
+        {"xcache", P_INT, true, 0, nullptr}}},
       {"THREAD_TOTAL_RED", 3, {}},
       {"THREAD_BITMAP_RED_G", 3, {}},
       {"WARP_TOTAL_RED", 3, {}},
@@ -385,8 +386,9 @@ void check_params(const Op& o) {
   } else if (o.name == "SET_RESOURCE") {
     int64_t tpb = o.geti("tpb");
     int64_t st = o.geti("stages");
-    if (tpb < 32 || tpb > 1024 || tpb % 32 || o.geti("grid") < 0 || (st != 0 && st != 2))
-      bad("tpb multiple of 32 in [32,1024], grid >= 0, stages in {0,2}");
+    const int64_t xc = o.geti("xcache");
+    if (tpb < 32 || tpb > 1024 || tpb % 32 || o.geti("grid") < 0 || (st != 0 && st != 2) || xc < 0 || xc > 65536)
+      bad("tpb multiple of 32 in [32,1024], grid >= 0, stages in {0,2}, xcache in [0,65536]");
   }
 }
 

@@ -122,6 +122,7 @@ struct HostPart {
   bool sort_bmtb = false;
   Red red[3] = {RED_NONE, RED_NONE, RED_NONE};  // per level (BMTB, BMW, BMT)
   int tpb = 0, grid = 0, stages = 2;  // SET_RESOURCE
+  int64_t xcache = 0;                 // SET_RESOURCE xcache: hot x entries staged in shared memory per CTA
   // DIA
   int64_t r0 = 0, mb = 0;
   std::vector<int64_t> dia_off;

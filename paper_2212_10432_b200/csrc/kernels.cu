@@ -14,6 +14,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <type_traits>
+
 #include "devpart.h"
 #include "kcommon.cuh"
 
@@ -129,6 +132,23 @@ struct XGlobal {
   const V* __restrict__ x;
   __device__ __forceinline__ double operator()(int64_t c) const { return ldx(x, c); }
 };
+// Hot-x cache (SET_RESOURCE xcache, reading R-xcache): the part's K most referenced x
+// entries are staged in shared memory once per (persistent) CTA; their columns were
+// re-encoded at plan time as ~slot (negative), so a gather reads shared memory instead of
+// moving a 32-byte L1/L2 sector.  On power-law matrices (C3) the top 32K columns carry a
+// third of the nonzeros; the rest are gathered from global memory as before.
+template <class V>
+struct XHot {
+  const V* __restrict__ x;
+  const V* sm;
+  __device__ __forceinline__ double operator()(int64_t c) const { return c < 0 ? (double)sm[~c] : ldx(x, c); }
+};
+template <class V>
+__device__ __forceinline__ void xhot_fill(const DevPart& p, const V* __restrict__ x, V* sm) {
+  for (int64_t i = threadIdx.x; i < p.xh_n; i += blockDim.x) sm[i] = __ldg(x + ldm(p.xh_cols + i));
+  __syncthreads();
+}
+
 template <class V>
 struct XRing {
   const V* ring;
@@ -373,11 +393,19 @@ __device__ __forceinline__ void nnz_thread_bmt_pe(const DevPart& p, XA xa, V* __
   else write_atom(p, y, o.row, o.acc);
 }
 
-template <class V, bool PAD, int VEC, int KB, int EM>
+template <class V, bool PAD, int VEC, int KB, int EM, bool XH>
 __global__ void __launch_bounds__(1024) k_nnz_thread_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const Units u = thread_units(p.n_bmt);
-  for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x)
-    nnz_thread_bmt_pe<V, PAD, VEC, KB, EM>(p, XGlobal<V>{x}, y, t);
+  if constexpr (XH) {
+    extern __shared__ __align__(128) unsigned char xh_smem[];
+    V* xs = (V*)xh_smem;
+    xhot_fill(p, x, xs);
+    for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x)
+      nnz_thread_bmt_pe<V, PAD, VEC, KB, EM>(p, XHot<V>{x, xs}, y, t);
+  } else {
+    for (int64_t t = u.begin, t_e = u.end; t < t_e; t += blockDim.x)
+      nnz_thread_bmt_pe<V, PAD, VEC, KB, EM>(p, XGlobal<V>{x}, y, t);
+  }
 }
 
 // =====================================================================================
@@ -629,10 +657,15 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
 // k_nnz_warp, predicated-emit form: each lane scans its BMT with bmt_scan_pe (rows closed
 // inside the BMT stored by one predicated store, no divergent writer calls), then the same
 // warp combine of (cin, cout, head flag) as above.  Same writes as k_nnz_warp.
-template <class V, int WRED, bool PAD, int VEC, int KB, int EM>
+template <class V, int WRED, bool PAD, int VEC, int KB, int EM, bool XH>
 __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const int lane = threadIdx.x & 31;
-  const XGlobal<V> xa{x};
+  extern __shared__ __align__(128) unsigned char xh_smem[];
+  if constexpr (XH) xhot_fill(p, x, (V*)xh_smem);
+  using XA = std::conditional_t<XH, XHot<V>, XGlobal<V>>;
+  XA xa;
+  if constexpr (XH) xa = XHot<V>{x, (const V*)xh_smem};
+  else xa = XGlobal<V>{x};
   for (int64_t w = warp_units(p.n_bmw).begin, w_e = warp_units(p.n_bmw).end; w < w_e; w += blockDim.x >> 5) {
     const int64_t tb0 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w) : w * p.bmts_per_bmw;
     const int64_t tb1 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w + 1) : min(tb0 + p.bmts_per_bmw, p.n_bmt);
@@ -1170,12 +1203,15 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       // timing (variant 9)
       const bool pe = p.variant != 9 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
       const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin && !p.org_model.kind;
+      const int64_t gx = std::min<int64_t>(g, (int64_t)std::max(1, p.xh_ctas) * sm_count());  // xcache: persistent
 #define AS_NT(PADV, VECV)                                                                                 \
   {                                                                                                       \
     constexpr int KBV = sizeof(V) == 4 && VECV <= 4 ? 4 : 8;                                              \
     if (!pe) k_nnz_thread<V, PADV, VECV, KBV><<<g, tt, 0, s>>>(p, x, y);                                  \
-    else if (em0) k_nnz_thread_pe<V, PADV, VECV, KBV, 0><<<g, tt, 0, s>>>(p, x, y);                       \
-    else k_nnz_thread_pe<V, PADV, VECV, KBV, 1><<<g, tt, 0, s>>>(p, x, y);                                \
+    else if (p.xh_n && em0) k_nnz_thread_pe<V, PADV, VECV, KBV, 0, true><<<gx, tt, p.smem, s>>>(p, x, y);   \
+    else if (p.xh_n) k_nnz_thread_pe<V, PADV, VECV, KBV, 1, true><<<gx, tt, p.smem, s>>>(p, x, y);          \
+    else if (em0) k_nnz_thread_pe<V, PADV, VECV, KBV, 0, false><<<g, tt, 0, s>>>(p, x, y);                 \
+    else k_nnz_thread_pe<V, PADV, VECV, KBV, 1, false><<<g, tt, 0, s>>>(p, x, y);                          \
   }
       if (!p.pad) {
         AS_NT(false, 1)
@@ -1211,11 +1247,14 @@ int launch_typed(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       // legacy form is forced (variant + 8: AS_NT_LEGACY)
       const bool pe = p.variant < 8 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
       const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin && !p.org_model.kind;
+      const int64_t gx = std::min<int64_t>(g, (int64_t)std::max(1, p.xh_ctas) * sm_count());  // xcache: persistent
       constexpr int KBW = 4;  // fp64 batches of 8 spill 100-180 bytes next to the warp-combine state
 #define AS_NWPE(WR, PADV, VECV)                                                                  \
   {                                                                                              \
-    if (em0) k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 0><<<g, tpb, 0, s>>>(p, x, y); \
-    else k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 1><<<g, tpb, 0, s>>>(p, x, y);     \
+    if (p.xh_n && em0) k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 0, true><<<gx, tpb, p.smem, s>>>(p, x, y); \
+    else if (p.xh_n) k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 1, true><<<gx, tpb, p.smem, s>>>(p, x, y);   \
+    else if (em0) k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 0, false><<<g, tpb, 0, s>>>(p, x, y);           \
+    else k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 1, false><<<g, tpb, 0, s>>>(p, x, y);                    \
   }
 #define AS_NW(WR)                                                              \
   if (pe) {                                                                    \
@@ -1333,8 +1372,58 @@ int launch_l2_flush(void* buf, size_t bytes, int pattern, void* stream) {
 }
 
 
+// xcache (R-xcache): opt the XH instantiations the launch may pick (EM 0 / 1) in to `smem`
+// bytes of dynamic shared memory; returns the CTAs per SM they reach (0 on failure)
+template <class K>
+static int xh_optin(K kern, size_t smem, int tpb) {
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, tpb, smem) != cudaSuccess) return 0;
+  return n;
+}
+template <class V, bool PAD, int VEC>
+static int xh_prep_thread(size_t smem, int tpb) {
+  constexpr int KB = sizeof(V) == 4 && VEC <= 4 ? 4 : 8;
+  return std::min(xh_optin(k_nnz_thread_pe<V, PAD, VEC, KB, 0, true>, smem, tpb),
+                  xh_optin(k_nnz_thread_pe<V, PAD, VEC, KB, 1, true>, smem, tpb));
+}
+template <class V, int WR, bool PAD, int VEC>
+static int xh_prep_warp(size_t smem, int tpb) {
+  constexpr int KB = 4 > VEC ? 4 : VEC;
+  return std::min(xh_optin(k_nnz_warp_pe<V, WR, PAD, VEC, KB, 0, true>, smem, tpb),
+                  xh_optin(k_nnz_warp_pe<V, WR, PAD, VEC, KB, 1, true>, smem, tpb));
+}
+template <class V>
+static int xh_prep(const DevPart& p, size_t smem, int tpb) {
+  if (p.fam == FAM_NNZ_THREAD) {
+    if (!p.pad) return xh_prep_thread<V, false, 1>(smem, tpb);
+    if (p.vec == 1) return xh_prep_thread<V, true, 1>(smem, tpb);
+    if (p.vec == 2) return xh_prep_thread<V, true, 2>(smem, tpb);
+    return xh_prep_thread<V, true, 4>(smem, tpb);
+  }
+  if ((p.variant & 7) == 1) {
+    if (!p.pad) return xh_prep_warp<V, 1, false, 1>(smem, tpb);
+    if (p.vec == 1) return xh_prep_warp<V, 1, true, 1>(smem, tpb);
+    if (p.vec == 2) return xh_prep_warp<V, 1, true, 2>(smem, tpb);
+    return xh_prep_warp<V, 1, true, 4>(smem, tpb);
+  }
+  if (!p.pad) return xh_prep_warp<V, 2, false, 1>(smem, tpb);
+  if (p.vec == 1) return xh_prep_warp<V, 2, true, 1>(smem, tpb);
+  if (p.vec == 2) return xh_prep_warp<V, 2, true, 2>(smem, tpb);
+  return xh_prep_warp<V, 2, true, 4>(smem, tpb);
+}
+
 int prepare_part(DevPart& p) {
   if (p.fam == FAM_COMPOSE) return prepare_compose(p);
+  if (p.xh_n > 0 && (p.fam == FAM_NNZ_THREAD || p.fam == FAM_NNZ_WARP)) {
+    const int tpb = p.tpb > 0 ? p.tpb : 256;
+    p.smem = (size_t)p.xh_n * (p.dtype == 1 ? 8 : 4);
+    const int per = p.dtype == 1 ? xh_prep<double>(p, p.smem, tpb) : xh_prep<float>(p, p.smem, tpb);
+    cudaGetLastError();
+    if (per < 1) return (int)cudaErrorInvalidConfiguration;
+    p.xh_ctas = p.grid > 0 ? std::min(p.grid, per) : per;
+    return 0;
+  }
   if (p.fam == FAM_BLOCK_OFFSET && p.variant == 1) {  // TMA-staged CSR-stream
     const size_t sv = p.dtype == 1 ? 8 : 4;
     p.smem = 2 * ((size_t)p.smem_cap * (sv + 4) + (size_t)p.smem_rcap * 4) + (size_t)p.smem_cap * 8 + 16;

@@ -85,7 +85,7 @@ const void* Plan::up_vals(const std::vector<double>& v, cudaStream_t s, size_t p
 }
 
 // BMT_PAD arrays (A18): slot-major values/columns + per-group first BMT, slot base, width.
-void Plan::upload_pad(const HostPart& h, DevPart& d, cudaStream_t s) {
+void Plan::upload_pad(const HostPart& h, DevPart& d, cudaStream_t s, const std::vector<int32_t>* pad_col) {
   const int64_t sv = dt == AS_R64F ? 8 : 4;
   d.pad = 1;
   d.vec = h.vec;
@@ -99,10 +99,55 @@ void Plan::upload_pad(const HostPart& h, DevPart& d, cudaStream_t s) {
   d.grp_first_bmt = up_i32(h.grp_first_bmt, s, "grp_first_bmt");
   d.grp_base = (const int64_t*)up(h.grp_base.data(), h.grp_base.size() * 8, s);
   d.grp_width = up_i32(h.pad_width, s, "pad_width");
-  d.pad_col = (const int32_t*)up(h.pad_col.data(), h.pad_col.size() * 4, s);
+  const std::vector<int32_t>& pc = (pad_col && !pad_col->empty()) ? *pad_col : h.pad_col;
+  d.pad_col = (const int32_t*)up(pc.data(), pc.size() * 4, s);
   cudaStreamSynchronize(s);
   d.pad_val = up_vals(h.pad_val, s);
   bytes_model += (double)(h.pad_col.size() * 4 + h.pad_val.size() * sv + d.n_grp * (reg ? 12 : 16));
+}
+
+// Hot-x cache (SET_RESOURCE xcache = K, reading R-xcache): the K columns the part
+// references most (ties: smaller column) are staged in shared memory by every persistent CTA;
+// their entries in col / pad_col are re-encoded as ~slot (slots in column order).  Only the
+// device copies change: the exported (logical) metadata keeps the original columns.
+bool Plan::encode_xcache(const HostPart& h, DevPart& d, cudaStream_t s, std::vector<int32_t>& col_enc,
+                         std::vector<int32_t>& pad_enc) {
+  const int64_t sv = dt == AS_R64F ? 8 : 4;
+  const int64_t cap = (device_max_smem_optin(device) - 1024) / sv;
+  int64_t K = std::min<int64_t>(h.xcache, cap);
+  if (K <= 0 || h.col.empty()) return false;
+  const int64_t nn = host.n;
+  std::vector<int32_t> cnt((size_t)nn, 0);
+  parallel_for((int64_t)h.col.size(), [&](int64_t a, int64_t e) {
+    for (int64_t i = a; i < e; ++i) __atomic_fetch_add(&cnt[(size_t)h.col[i]], 1, __ATOMIC_RELAXED);
+  });
+  std::vector<int32_t> cand;
+  for (int64_t c = 0; c < nn; ++c)
+    if (cnt[(size_t)c]) cand.push_back((int32_t)c);
+  K = std::min<int64_t>(K, (int64_t)cand.size());
+  if (K <= 0) return false;
+  auto hotter = [&](int32_t a, int32_t b) { return cnt[a] != cnt[b] ? cnt[a] > cnt[b] : a < b; };
+  std::nth_element(cand.begin(), cand.begin() + (K - 1), cand.end(), hotter);
+  cand.resize((size_t)K);
+  std::sort(cand.begin(), cand.end());
+  std::vector<int32_t> slot((size_t)nn, -1);
+  for (int64_t i = 0; i < K; ++i) slot[(size_t)cand[(size_t)i]] = (int32_t)i;
+  auto enc = [&](const std::vector<int32_t>& in, std::vector<int32_t>& out) {
+    out.resize(in.size());
+    parallel_for((int64_t)in.size(), [&](int64_t a, int64_t e) {
+      for (int64_t i = a; i < e; ++i) {
+        const int32_t sl = slot[(size_t)in[i]];
+        out[i] = sl >= 0 ? ~sl : in[i];
+      }
+    });
+  };
+  if (h.pad) enc(h.pad_col, pad_enc);
+  else enc(h.col, col_enc);
+  std::vector<int64_t> hot(cand.begin(), cand.end());
+  d.xh_cols = up_i32(hot, s, "xcache columns");
+  d.xh_n = K;
+  bytes_model += (double)(K * 4);
+  return true;
 }
 
 // x-window staging for k_nnz_thread (banded matrices): persistent CTAs, per (CTA, round)
@@ -335,6 +380,7 @@ void Plan::upload(cudaStream_t s) {
       }
       const Level &B = h.lv[0], &W = h.lv[1], &T = h.lv[2];
       bool need_rowptr = true, need_colval = true;
+      std::vector<int32_t> col_enc, pad_enc;  // xcache-encoded device columns (empty: as built)
       switch (h.fam) {
         case FAM_THREAD_ROW: {
           d.n_bmt = T.count();
@@ -361,7 +407,7 @@ void Plan::upload(cudaStream_t s) {
           d.n_bmt = T.count();
           d.k = T.size;
           if (h.fam == FAM_NNZ_WARP && !h.pad && (T.size == 1 || T.size == 2 || T.size == 4) && W.nnz &&
-              !B.present && W.size % (32 * T.size) == 0) {
+              !B.present && W.size % (32 * T.size) == 0 && h.xcache == 0) {
             // tile form: packed 1-bit heads + BMW first rows; BMT starts and first rows
             // are computed from them (k_warp_tile)
             d.tile = 1;
@@ -391,12 +437,13 @@ void Plan::upload(cudaStream_t s) {
           d.bm_words = h.bm_words;
           d.bitmap = (const uint32_t*)up(h.bitmap.data(), h.bitmap.size() * 4, s);
           bytes_model += (double)(h.bitmap.size() * 4);
+          if (h.xcache > 0) encode_xcache(h, d, s, col_enc, pad_enc);
           if (h.pad) {  // CSR5-like slot-major tiles (BMT_PAD over NNZ BMTs)
-            upload_pad(h, d, s);
+            upload_pad(h, d, s, &pad_enc);
             need_colval = false;
             d.pad_grp_bmw = (h.fam == FAM_NNZ_WARP && h.pad_scope == 1) ? 1 : 0;
           }
-          if (h.fam == FAM_NNZ_THREAD && h.stages == 2) try_xwin(h, d, s);
+          if (h.fam == FAM_NNZ_THREAD && h.stages == 2 && !d.xh_n) try_xwin(h, d, s);
           if (h.fam == FAM_NNZ_WARP) {
             d.variant = h.red[1] == RED_SEG ? 1 : 2;
             d.n_bmw = W.count();
@@ -569,7 +616,8 @@ void Plan::upload(cudaStream_t s) {
       }
       if (h.fam == FAM_WARP_ROW && !d.bmw_start) d.bmw_start = d.row_ptr;
       if (need_colval) {
-        d.col = (const int32_t*)up(h.col.data(), h.col.size() * 4, s);
+        const std::vector<int32_t>& cc = col_enc.empty() ? h.col : col_enc;
+        d.col = (const int32_t*)up(cc.data(), cc.size() * 4, s);
         d.val = up_vals(h.val, s);
         bytes_model += (double)(nnz * (4 + sv));
       }
@@ -582,6 +630,7 @@ void Plan::upload(cudaStream_t s) {
     // name the kernel form actually chosen (as_plan_info.kernels)
     std::string& fn = host.parts[pi].fam_name;
     if (d.xwin) fn += "_xwin";
+    if (d.xh_n) fn += "_xh";
     if (d.tile) fn += "_tile";
     if (d.fam == FAM_BLOCK_OFFSET && d.variant == 1) fn += "_tma";
     launches.push_back(d);
@@ -593,6 +642,25 @@ void Plan::upload(cudaStream_t s) {
     n_prepass = (int64_t)host.prepass.size();
   }
   if (dt == AS_R32F) mark_heavy_rows(s);
+  // xcache is implemented in the predicated-emit nnz kernels; parts that will run the
+  // branching form (fp32 ADD-mode parts with heavy rows, or the AS_NT_LEGACY A/B knob) get
+  // their columns back unencoded
+  for (size_t i = 0; i < launches.size(); ++i) {
+    DevPart& d = launches[i];
+    if (!d.xh_n) continue;
+    const bool legacy = (d.fam == FAM_NNZ_THREAD && d.variant == 9) || (d.fam == FAM_NNZ_WARP && d.variant >= 8) ||
+                        (d.dtype == 0 && d.n_heavy && d.mode == 1);
+    if (!legacy) continue;
+    const HostPart& h = host.parts[host.launch_order[i]];
+    if (d.pad) d.pad_col = (const int32_t*)up(h.pad_col.data(), h.pad_col.size() * 4, s);
+    else d.col = (const int32_t*)up(h.col.data(), h.col.size() * 4, s);
+    d.xh_n = 0;
+    d.xh_cols = nullptr;
+    d.smem = 0;
+    std::string& fn = host.parts[host.launch_order[i]].fam_name;
+    const size_t at = fn.find("_xh");
+    if (at != std::string::npos) fn.erase(at, 3);
+  }
   single_writer = host.prepass.empty() && n_heavy == 0;
   for (int64_t pi : host.launch_order)
     if (host.parts[pi].mode != 0 || !host.parts[pi].atom.empty()) single_writer = false;

@@ -53,7 +53,9 @@ struct Plan {
   const int32_t* up_i32(const std::vector<int64_t>& v, cudaStream_t s, const char* what);
   const void* up_vals(const std::vector<double>& v, cudaStream_t s, size_t pad_elems = 0);
   void upload(cudaStream_t s);
-  void upload_pad(const HostPart& h, DevPart& d, cudaStream_t s);
+  void upload_pad(const HostPart& h, DevPart& d, cudaStream_t s, const std::vector<int32_t>* pad_col = nullptr);
+  bool encode_xcache(const HostPart& h, DevPart& d, cudaStream_t s, std::vector<int32_t>& col_enc,
+                     std::vector<int32_t>& pad_enc);
   void try_xwin(const HostPart& h, DevPart& d, cudaStream_t s);
   void mark_heavy_rows(cudaStream_t s);
   const int32_t* d_heavy_rows = nullptr;  // fp32 A25 heavy rows (sorted) + fp64 scratch

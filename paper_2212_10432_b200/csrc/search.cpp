@@ -82,14 +82,21 @@ std::string join_list(const std::vector<int64_t>& v) {
 
 // mapping + implementing stage for one COMPRESSed branch
 std::string gen_kernel(Rng& r, const Stats& st) {
-  std::vector<int> fams = {0, 0, 1, 2, 3, 5};  // thread_row x2, nnz_thread, nnz_warp, warp_row, block_offset
-  if (st.avg > 24) fams = {2, 2, 3, 3, 4, 5, 0};
+  // thread_row x2, nnz_thread, nnz_warp, warp_row, block_offset, composed levels (6)
+  std::vector<int> fams = {0, 0, 1, 2, 3, 5, 6};
+  if (st.avg > 24) fams = {2, 2, 3, 3, 4, 5, 0, 6};
   if (st.maxlen > 4096) fams.push_back(4);     // block_total only helps long rows
   int f = r.pick(fams);
   std::string s = "COMPRESS; ";
-  std::string tpb = r.coin(0.5) ? ""
-                                : "SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{128, 256, 512})) +
-                                      ",grid=" + std::to_string(r.pick(std::vector<int>{0, 0, 8, 16})) + "); ";
+  // hot-x cache (R-xcache) for the nnz families on large irregular matrices: the x vector is
+  // far larger than one SM's shared memory and a few columns carry many nonzeros
+  const bool xc = (f == 1 || f == 2) && st.n >= (int64_t(1) << 20) && st.var > 16 && r.coin(0.5);
+  std::string tpb =
+      xc ? "SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{512, 1024})) + ",grid=1,stages=2,xcache=" +
+               std::to_string(r.pick(std::vector<int64_t>{8192, 16384, 24576, 32768})) + "); "
+      : r.coin(0.5) ? ""
+                    : "SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{128, 256, 512})) +
+                          ",grid=" + std::to_string(r.pick(std::vector<int>{0, 0, 8, 16})) + "); ";
   switch (f) {
     case 0: {  // CSR-scalar / ELL / SELL-P family
       int64_t rows = r.pick(std::vector<int64_t>{32, 64, 128, 256});
@@ -130,6 +137,43 @@ std::string gen_kernel(Rng& r, const Stats& st) {
     }
     case 4: {  // block per row (long rows)
       s += "BMTB_ROW_BLOCK(1); SHMEM_TOTAL_RED; ";
+      break;
+    }
+    case 6: {  // composed levels (compose.cu): random level kinds/sizes, reductions at random levels
+      const bool B = r.coin(0.6), W = r.coin(0.5), T = !W || r.coin(0.8);
+      bool b_row1 = false, w_row1 = false, t_row1 = false;
+      std::string red;
+      if (B) {
+        if (r.coin(0.5)) {
+          const int64_t rows = r.pick(std::vector<int64_t>{1, 4, 16, 64});
+          b_row1 = rows == 1;
+          s += "BMTB_ROW_BLOCK(" + std::to_string(rows) + "); ";
+        } else {
+          s += "BMTB_NNZ_BLOCK(" + std::to_string(r.pick(std::vector<int64_t>{256, 1024, 2048})) + "); ";
+        }
+      }
+      if (W) {
+        if (r.coin(0.5)) {
+          const int64_t rows = r.pick(std::vector<int64_t>{1, 2, 4});
+          w_row1 = rows == 1;
+          s += "BMW_ROW_BLOCK(" + std::to_string(rows) + "); ";
+        } else {
+          s += "BMW_NNZ_BLOCK(" + std::to_string(32 * r.pick(std::vector<int64_t>{1, 2, 4, 8})) + "); ";
+        }
+      }
+      if (T) {
+        if (r.coin(0.4)) {
+          const int64_t rows = r.pick(std::vector<int64_t>{1, 2});
+          t_row1 = rows == 1;
+          s += "BMT_ROW_BLOCK(" + std::to_string(rows) + "); ";
+        } else {
+          s += "BMT_NNZ_BLOCK(" + std::to_string(r.pick(std::vector<int64_t>{2, 4, 8, 16})) + "); ";
+        }
+        if (r.coin(0.85)) red += t_row1 && r.coin(0.5) ? "THREAD_TOTAL_RED; " : "THREAD_BITMAP_RED_G; ";
+      }
+      if (W && r.coin(0.8)) red += w_row1 && r.coin(0.5) ? "WARP_TOTAL_RED; " : r.coin(0.5) ? "WARP_SEG_ADD_RED; " : "WARP_BITMAP_RED; ";
+      if (B && r.coin(0.8)) red += b_row1 && r.coin(0.5) ? "SHMEM_TOTAL_RED; " : "SHMEM_OFFSET_RED; ";
+      s += red;
       break;
     }
     default: {  // CSR-stream
@@ -262,6 +306,7 @@ std::string mutate_graph(const Seq& g0, Rng& r) {
   if (k == "tpb") step({64, 128, 256, 512, 1024});
   else if (k == "grid") step({0, 1, 2, 4, 8, 16});
   else if (k == "stages") v.i = v.i ? 0 : 2;
+  else if (k == "xcache") step({0, 4096, 8192, 16384, 24576, 32768});
   else if (k == "vec") step({0, 1, 2, 4});
   else if (k == "max") step({4, 8, 16, 32});
   else if (k == "b") step({16, 32, 64, 128});

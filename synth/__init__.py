@@ -404,6 +404,9 @@ def _gen():
         i64, vp, u64 = ctypes.c_int64, ctypes.c_void_p, ctypes.c_uint64
         L.synth_values.argtypes = [u64, i64, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int]
         L.synth_c5.argtypes = [i64, i64, i64, u64, vp, vp, ctypes.c_int]
+        L.synth_c5_rowptr.argtypes = [i64, i64, i64, u64, vp, ctypes.c_int]
+        L.synth_c5_band.argtypes = [i64, i64, u64, vp, i64, i64, vp, ctypes.c_int]
+        L.synth_values_range.argtypes = [u64, i64, i64, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int]
         L.synth_c4.argtypes = [i64, i64, i64, i64, u64, vp, vp, vp, ctypes.c_int]
         L.synth_c3.argtypes = [ctypes.c_int, i64, ctypes.c_double, ctypes.c_double, ctypes.c_double, u64, vp, vp,
                                ctypes.c_int]
@@ -431,6 +434,30 @@ def c5_band_csr(m: int = 67_108_864, nnz: int = 1 << 30, band: int = 4096, seed:
     if rc:
         raise ValueError("C5 row-length adjustment failed (nnz not reachable)")
     return Csr(m, m, rp, col, _fast_values(seed, nnz, dtype, int_mode), "band-irreg")
+
+
+def c5_row_ptr(m: int = 67_108_864, nnz: int = 1 << 30, band: int = 4096, seed: int = 5) -> np.ndarray:
+    """row_ptr of C5 alone (row lengths + the seeded adjustment; 0.5 GB, no columns)."""
+    rp = np.empty(m + 1, np.int64)
+    if _gen().synth_c5_rowptr(m, nnz, band, seed, rp.ctypes.data, _nth()):
+        raise ValueError("C5 row-length adjustment failed (nnz not reachable)")
+    return rp
+
+
+def c5_band_rows(row_ptr: np.ndarray, r0: int, r1: int, band: int = 4096, seed: int = 5, dtype=np.float64,
+                 int_mode: bool = False) -> "Csr":
+    """Rows [r0, r1) of C5 as a CSR band with global columns -- bit-identical to the same
+    rows of c5_band_csr (counter-based per-row draws and per-nonzero values), generated
+    without the rest of the matrix (a multi-GPU rank's ROW_DIV band)."""
+    m = row_ptr.shape[0] - 1
+    a, e = int(row_ptr[r0]), int(row_ptr[r1])
+    col = np.empty(e - a, np.int32)
+    _gen().synth_c5_band(m, band, seed, np.ascontiguousarray(row_ptr, np.int64).ctypes.data, r0, r1,
+                         col.ctypes.data, _nth())
+    val = np.empty(e - a, dtype)
+    _gen().synth_values_range(seed, a, e - a, int(int_mode), int(np.dtype(dtype) == np.float32), val.ctypes.data,
+                              _nth())
+    return Csr(r1 - r0, m, (row_ptr[r0:r1 + 1] - a).astype(np.int64), col, val, "band-irreg")
 
 
 def c4_blockdense_csr(m: int = 8_388_608, b: int = 64, n_tiles: int = 24_576, nnz: int = 200_000_000,

@@ -106,10 +106,11 @@ static void sort_kv(kv_t* v, int64_t n, uint64_t kmax, int nth) {
 }
 
 /* ------------------------------------------------------------------ values */
-typedef struct { uint64_t seed; int int_mode; int f32; void* val; } val_t;
+typedef struct { uint64_t seed; int int_mode; int f32; void* val; int64_t i0; } val_t;
 static void fill_vals(void* p, int64_t a, int64_t e) {
   val_t* s = (val_t*)p;
-  for (int64_t i = a; i < e; ++i) {
+  for (int64_t k = a; k < e; ++k) {
+    const int64_t i = s->i0 + k; /* global nonzero index: the Philox counter */
     double v;
     if (s->int_mode) {
       uint32_t u = rnd32(s->seed, 3, (uint64_t)i, 0);
@@ -121,19 +122,26 @@ static void fill_vals(void* p, int64_t a, int64_t e) {
       uint64_t bits = ((uint64_t)(o[0] >> 5) << 26) | (o[1] >> 6);
       v = (double)bits * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
     }
-    if (s->f32) ((float*)s->val)[i] = (float)v;
-    else ((double*)s->val)[i] = v;
+    if (s->f32) ((float*)s->val)[k] = (float)v;
+    else ((double*)s->val)[k] = v;
   }
 }
 /* values for nnz entries: U[-1,1) (real) or {-4..4}\{0} (int_mode); f32 selects float */
 int synth_values(uint64_t seed, int64_t nnz, int int_mode, int f32, void* val, int nth) {
-  val_t s = {seed, int_mode, f32, val};
+  val_t s = {seed, int_mode, f32, val, 0};
   par(nth, nnz, fill_vals, &s);
+  return 0;
+}
+/* values of the nonzeros [i0, i0 + n) only (a rank's ROW_DIV band): identical to the
+ * corresponding slice of synth_values */
+int synth_values_range(uint64_t seed, int64_t i0, int64_t n, int int_mode, int f32, void* val, int nth) {
+  val_t s = {seed, int_mode, f32, val, i0};
+  par(nth, n, fill_vals, &s);
   return 0;
 }
 
 /* ------------------------------------------------------------------ C5 band-irregular */
-typedef struct { int64_t m, band; uint64_t seed; int64_t* L; const int64_t* rp; int32_t* col; } c5_t;
+typedef struct { int64_t m, band; uint64_t seed; int64_t* L; const int64_t* rp; int32_t* col; int64_t r0; } c5_t;
 static void c5_len(void* p, int64_t a, int64_t e) {
   c5_t* s = (c5_t*)p;
   for (int64_t i = a; i < e; ++i) {
@@ -148,7 +156,7 @@ static void c5_len(void* p, int64_t a, int64_t e) {
 static void c5_cols(void* p, int64_t a, int64_t e) {
   c5_t* s = (c5_t*)p;
   int32_t buf[4096];
-  for (int64_t i = a; i < e; ++i) {
+  for (int64_t i = s->r0 + a; i < s->r0 + e; ++i) {
     int64_t lo = i - s->band < 0 ? 0 : i - s->band, hi = i + s->band > s->m - 1 ? s->m - 1 : i + s->band;
     int64_t width = hi - lo; /* window without the diagonal */
     int64_t need = s->rp[i + 1] - s->rp[i] - 1, got = 0;
@@ -163,15 +171,16 @@ static void c5_cols(void* p, int64_t a, int64_t e) {
       if (!dup) buf[got++] = (int32_t)c;
     }
     qsort(buf, (size_t)got, sizeof(int32_t), cmp_i32);
-    memcpy(s->col + s->rp[i], buf, (size_t)got * sizeof(int32_t));
+    memcpy(s->col + (s->rp[i] - s->rp[s->r0]), buf, (size_t)got * sizeof(int32_t));
   }
 }
 static int64_t gcd64(int64_t a, int64_t b) { while (b) { int64_t t = a % b; a = b; b = t; } return a; }
 
-/* rows m, total nnz, band half-width; row_ptr[m+1] (out), col[nnz] (out) */
-int synth_c5(int64_t m, int64_t nnz, int64_t band, uint64_t seed, int64_t* row_ptr, int32_t* col, int nth) {
+/* row lengths of C5 (drawn per row, then the seeded round-robin +-1 adjustment to nnz):
+ * row_ptr[m+1] (out) */
+int synth_c5_rowptr(int64_t m, int64_t nnz, int64_t band, uint64_t seed, int64_t* row_ptr, int nth) {
   int64_t* L = (int64_t*)malloc((size_t)m * sizeof(int64_t));
-  c5_t s = {m, band, seed, L, row_ptr, col};
+  c5_t s = {m, band, seed, L, row_ptr, NULL, 0};
   par(nth, m, c5_len, &s);
   int64_t tot = 0;
   for (int64_t i = 0; i < m; ++i) tot += L[i];
@@ -191,8 +200,20 @@ int synth_c5(int64_t m, int64_t nnz, int64_t band, uint64_t seed, int64_t* row_p
   row_ptr[0] = 0;
   for (int64_t i = 0; i < m; ++i) row_ptr[i + 1] = row_ptr[i] + L[i];
   free(L);
-  par(nth, m, c5_cols, &s);
   return 0;
+}
+/* columns of rows [r0, r1) given the full row_ptr: col[row_ptr[r1] - row_ptr[r0]] (out).
+ * Per-row counter-based draws, so a band equals the same rows of the whole matrix. */
+int synth_c5_band(int64_t m, int64_t band, uint64_t seed, const int64_t* row_ptr, int64_t r0, int64_t r1,
+                  int32_t* col, int nth) {
+  c5_t s = {m, band, seed, NULL, row_ptr, col, r0};
+  par(nth, r1 - r0, c5_cols, &s);
+  return 0;
+}
+/* rows m, total nnz, band half-width; row_ptr[m+1] (out), col[nnz] (out) */
+int synth_c5(int64_t m, int64_t nnz, int64_t band, uint64_t seed, int64_t* row_ptr, int32_t* col, int nth) {
+  if (synth_c5_rowptr(m, nnz, band, seed, row_ptr, nth)) return -1;
+  return synth_c5_band(m, band, seed, row_ptr, 0, m, col, nth);
 }
 
 /* ------------------------------------------------------------------ C4 block-dense */

@@ -337,3 +337,30 @@ def test_search_verifies_and_beats_seed(tmp_path):
     seed_t = rows[0]["median_ms"]
     best_t = min(r["median_ms"] for r in rows if r["median_ms"] > 0 and r["graph"] == text)
     assert best_t <= seed_t * 1.01, (best_t, seed_t)
+
+
+XCACHE_GRAPHS = [
+    "COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=256,grid=1,xcache=512); GMEM_ATOM_RED",
+    "COMPRESS; BMT_NNZ_BLOCK(16); BMT_PAD(GLOBAL); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=512,xcache=1000); GMEM_ATOM_RED",
+    "COMPRESS; BMT_NNZ_BLOCK(5); BMT_PAD(GLOBAL,1); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=128,xcache=3000); GMEM_ATOM_RED",
+    "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,0); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; "
+    "SET_RESOURCE(tpb=1024,grid=2,xcache=4096); GMEM_ATOM_RED",
+    "COMPRESS; BMW_NNZ_BLOCK(128); BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; WARP_BITMAP_RED; "
+    "SET_RESOURCE(tpb=256,xcache=65536); GMEM_ATOM_RED",
+    "SORT; COMPRESS; BMW_NNZ_BLOCK(96); BMT_NNZ_BLOCK(3); BMT_PAD(BMW,1); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; "
+    "SET_RESOURCE(tpb=512,xcache=2048); GMEM_ATOM_RED",
+]
+
+
+@pytest.mark.parametrize("graph", XCACHE_GRAPHS)
+@pytest.mark.parametrize("dtype,int_mode", [(np.float64, True), (np.float32, True), (np.float64, False),
+                                            (np.float32, False)])
+def test_xcache_parity(graph, dtype, int_mode):
+    """R-xcache: staging the most referenced x entries in shared memory (columns re-encoded as
+    ~slot on the device) changes no result: bit-identical in integer mode, O2 otherwise, and
+    the logical (exported) columns are the original ones."""
+    coo = synth.random_powerlaw(9000, 7000, 4, 2500, int_mode=int_mode).astype(dtype)
+    P, _ = run_check(coo, graph, 1.5 if not int_mode else 2.0, -0.5, int_mode=int_mode, seed=4, keep_host=True)
+    assert "_xh" in P.info()["kernels"], P.info()["kernels"]
+    if int_mode:
+        compare_export(P, coo, graph)

@@ -65,6 +65,17 @@ def test_mtx_ingest(tmp_path):
     assert e.value.status == "AS_ERR_DUPLICATE"
 
 
+def test_row_cuts_from_ptr_match_oracle():
+    """as_dist_row_cuts_ptr (band-local ranks) gives the oracle's A35 cuts from row_ptr alone."""
+    for seed in range(4):
+        coo = synth.random_powerlaw(500 + 77 * seed, 400, seed, 150)
+        rp = np.zeros(coo.m + 1, np.int64)
+        np.add.at(rp, coo.row + 1, 1)
+        rp = np.cumsum(rp)
+        for world in (1, 2, 3, 8):
+            assert asp.row_cuts_from_ptr(rp, world).tolist() == B.row_cuts(rp, world).tolist()
+
+
 def test_row_cuts_match_oracle():
     for seed in range(5):
         coo = synth.random_powerlaw(200, 200, seed, 80)

@@ -12,7 +12,7 @@ import pytest
 
 asp = pytest.importorskip("paper_2212_10432_b200")
 
-N_OPS, N_PAR = 24, 15
+N_OPS, N_PAR = 24, 16  # parameter classes incl. SET_RESOURCE xcache
 
 
 def test_feature_layout_hand_derived():

@@ -77,3 +77,18 @@ def test_lap2d_band_weak_scaling():
     assert sum(x.nnz for x in bands) == tall.nnz == 5 * g * (g * P) - 2 * g - 2 * (g * P)
     assert np.array_equal(np.concatenate([x.col for x in bands]), tall.col)
     assert all(x.n == g * g * P for x in bands)
+
+
+def test_c5_band_rows_equal_whole_matrix():
+    """A rank's ROW_DIV band generated alone equals the same rows of the whole matrix."""
+    m, nnz = 1 << 16, 1 << 20
+    A = synth.c5_band_csr(m=m, nnz=nnz, band=512)
+    rp = synth.c5_row_ptr(m=m, nnz=nnz, band=512)
+    assert np.array_equal(rp, A.row_ptr)
+    for r0, r1 in [(0, 1000), (12345, 40000), (m - 77, m)]:
+        b = synth.c5_band_rows(rp, r0, r1, band=512)
+        a, e = int(rp[r0]), int(rp[r1])
+        assert b.m == r1 - r0 and b.n == m
+        assert np.array_equal(b.row_ptr, rp[r0:r1 + 1] - a)
+        assert np.array_equal(b.col, A.col[a:e])
+        assert np.array_equal(b.val, A.val[a:e])
