@@ -1,20 +1,32 @@
 """bench.py — SpMV GFLOP/s and HBM GB/s (% of roofline) of the searched operator graph.
 
-Default workload (N=1): BASELINE configs[1] = C2 `lap2d-2048`, the 5-point Laplacian on a
-2048x2048 grid (4,194,304 rows, 20,963,328 nnz, fp64), alpha=1, beta=0.  One step = one
-as_spmv call (the whole hot loop a5+a6; the plan a1-a4 and the search a7 run before the
-timed region, as in the paper, which times the generated SpMV program) with the
-inputs resident in HBM.  L2 is flushed (memset of 2 x L2 bytes) before every timed step,
-outside the timed events.
+Headline (N=1): BASELINE configs[2] = C3 `rmat-24`, the largest single-GPU configuration
+(Graph500 R-MAT, 16,777,216 rows, 268,435,456 nnz, fp32), alpha = 1, beta = 0, the graph
+found by as_search (seeded with the committed best design, profiles/best_graphs.json).  One
+step = one as_spmv call (the whole hot loop a5 + a6; the plan a1-a4 and the search a7 run
+before the timed region, as the paper times the generated SpMV program) with the
+inputs resident in HBM; L2 is flushed (write + read back of 2 x L2) before every timed step,
+outside the CUDA events.  ms_per_step is the MEDIAN of the timed steps (A27).
 
-Multi-GPU (torchrun, one rank per GPU): ROW_DIV bands with nnz-balanced cuts (reading A35),
-each rank plans/searches its own band; the y -> x exchange (all-gather over NCCL, or the
-halo of banded matrices) runs only with --exchange allgather|halo|nccl|peer.
-`--impl reference` times the oracle (long-double CPU SpMV) on the host instead.
+The same JSON line carries the other BASELINE configs measured in the same run under
+"configs" (C2 lap2d-2048, C4 blockdense-8m, C5 band-irreg-64m: their committed best graphs,
+same timing protocol, each with its dominant-kernel roofline), the gather roofline of the
+headline matrix (tools/gather_roofline.cu: stream every (val, col) pair once and gather
+x[col], no reduction, no y -- the floor any SpMV over these nonzeros has on this GPU),
+cpu_baseline (the oracle on the host cores), and e2e (as_spmv_host, host buffers).
+
+Multi-GPU (torchrun, one rank per GPU): default C5 `band-irreg-64m` (BASELINE configs[4])
+ROW_DIV across ranks with nnz-balanced cuts (reading A35, as_dist_row_cuts_ptr on the row
+pointer alone); every rank GENERATES ONLY ITS BAND (synth.c5_band_rows) and plans it; x is
+replicated.  value = total nnz of all ranks / the max-over-ranks SpMV step time (strong
+scaling).  The y exchange the next iterate needs is timed separately: as_spmv_dist with the
+NCCL AllGatherV (SpMV + exchange per step) and the all-gather alone.
+`--impl reference` times the oracle (long-double CPU SpMV) on the host, full config.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -34,12 +46,18 @@ METRIC = "SpMV GFLOP/s and achieved HBM GB/s (% of roofline) per matrix at 1/2/4
 C2_SEEDS = [
     "DIA_DECOM(theta=0.5,max=8) { DIA; SET_RESOURCE(tpb=128,grid=16) }",
     "DIA_DECOM(theta=0.5,max=8) { DIA; SET_RESOURCE(tpb=512,grid=4) }",
-    "DIA_DECOM(theta=0.5,max=8) { DIA; SET_RESOURCE(128) }",
     "COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED",
-    "COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL,1); THREAD_TOTAL_RED; GMEM_ATOM_RED",
     "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED",
     "COMPRESS; BMTB_ROW_BLOCK(128); SHMEM_OFFSET_RED; GMEM_ATOM_RED",
 ]
+WORKLOAD = {"c1": "uniform-1k", "c2": "lap2d-2048", "c3": "rmat-24", "c4": "blockdense-8m", "c5": "band-irreg-64m"}
+
+
+def best_graph(wl):
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "best_graphs.json")))[wl]["graph"]
+    except Exception:
+        return None
 
 
 def peaks():
@@ -90,42 +108,43 @@ class Clocks:
 
 
 def load_config(name, int_mode=False):
+    """(csr, workload name, seed graphs); the committed best graph (if any) seeds first."""
     if name == "c2":
-        return synth.c2_lap2d(2048), "lap2d-2048", C2_SEEDS
-    if name == "c1":
-        return synth.c1_uniform(int_mode=int_mode), "uniform-1k", [
+        coo, seeds = synth.c2_lap2d(2048), list(C2_SEEDS)
+    elif name == "c1":
+        coo, seeds = synth.c1_uniform(int_mode=int_mode), [
             "COMPRESS; BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; SET_RESOURCE(128); GMEM_ATOM_RED"]
-    if name == "c4":
+    elif name == "c4":
         coo, _ = synth.c4_blockdense_csr()
-        return coo, "blockdense-8m", [
+        seeds = [
             "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMTB_ROW_BLOCK(32); BMT_ROW_BLOCK(1); BMT_PAD(BMTB); THREAD_TOTAL_RED; SET_RESOURCE(64); GMEM_ATOM_RED }",
-            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMW_NNZ_BLOCK(1024); BMT_NNZ_BLOCK(32); BMT_PAD(BMW,2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=512,grid=2); GMEM_ATOM_RED }",
-            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL,2); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=512,grid=2,stages=0); GMEM_ATOM_RED }",
-            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
-            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMTB_ROW_BLOCK(64); BMT_ROW_BLOCK(1); BMT_PAD(BMTB); THREAD_TOTAL_RED; SET_RESOURCE(128); GMEM_ATOM_RED }",
-            "COMPRESS; BMTB_ROW_BLOCK(64); BMT_ROW_BLOCK(1); BMT_PAD(BMTB); THREAD_TOTAL_RED; SET_RESOURCE(128); GMEM_ATOM_RED"]
-    if name == "c3":
-        return synth.c3_rmat_csr(), "rmat-24", [
+            "DENSE_DECOM(b=64,theta=0.5) { DENSE; SET_RESOURCE(256) | COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }"]
+    elif name == "c3":
+        coo = synth.c3_rmat_csr()
+        seeds = [
+            "COMPRESS; BMW_NNZ_BLOCK(4096); BMT_NNZ_BLOCK(64); BMT_PAD(BMW,0); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=1024,grid=1,xcache=32768); GMEM_ATOM_RED",
+            "COMPRESS; BMW_NNZ_BLOCK(4096); BMT_NNZ_BLOCK(64); BMT_PAD(BMW,0); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=1024,grid=2); GMEM_ATOM_RED",
+            "COMPRESS; BMW_NNZ_BLOCK(2048); BMT_NNZ_BLOCK(64); BMT_PAD(BMW,4); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=1024,grid=1,xcache=16384); GMEM_ATOM_RED",
             "BIN(t=[32,2048]) { COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED"
             " | COMPRESS; BMTB_NNZ_BLOCK(2048); SHMEM_OFFSET_RED; GMEM_ATOM_RED"
-            " | COMPRESS; BMTB_ROW_BLOCK(1); BMW_NNZ_BLOCK(2048); WARP_TOTAL_RED; GMEM_ATOM_RED }",
-            "COMPRESS; BMW_NNZ_BLOCK(2048); BMT_NNZ_BLOCK(64); BMT_PAD(BMW,4); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=512,grid=2); GMEM_ATOM_RED",
-            "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,1); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
-            "COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=256,grid=16); GMEM_ATOM_RED"]
-    if name in ("c3s", "c4s", "c5s"):  # shape-preserving 1/4..1/16-scale instances (dev sweeps)
+            " | COMPRESS; BMTB_ROW_BLOCK(1); BMW_NNZ_BLOCK(2048); WARP_TOTAL_RED; GMEM_ATOM_RED }"]
+    elif name in ("c3s", "c4s", "c5s"):  # shape-preserving 1/4..1/16-scale instances (dev sweeps)
         c = {"c3s": lambda: synth.c3_rmat_csr(scale=22, nnz=1 << 26),
              "c4s": lambda: synth.c4_blockdense_csr(m=1 << 21, b=64, n_tiles=6144, nnz=50_000_000)[0],
              "c5s": lambda: synth.c5_band_csr(m=1 << 22, nnz=1 << 26)}[name]()
         return c, c.name + "-scaled", []
-    if name == "c5":
-        return synth.c5_band_csr(), "band-irreg-64m", [
-            "COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL,2); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=1024,grid=1,stages=0); GMEM_ATOM_RED",
-            "COMPRESS; BMW_NNZ_BLOCK(2048); BMT_NNZ_BLOCK(64); BMT_PAD(BMW,4); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=1024,grid=2); GMEM_ATOM_RED",
+    elif name == "c5":
+        coo = synth.c5_band_csr()
+        seeds = [
             "COMPRESS; BMT_NNZ_BLOCK(64); BMT_PAD(GLOBAL,4); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=1024,grid=2,stages=0); GMEM_ATOM_RED",
-            "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); BMT_PAD(BMW,2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
-            "COMPRESS; BMTB_ROW_BLOCK(256); SORT_BMTB; BMW_ROW_BLOCK(32); BMT_ROW_BLOCK(1); BMT_PAD(BMW); THREAD_TOTAL_RED; GMEM_ATOM_RED",
-            "COMPRESS; BMT_NNZ_BLOCK(32); BMT_PAD(GLOBAL,2); THREAD_BITMAP_RED_G; SET_RESOURCE(tpb=512,grid=2,stages=0); GMEM_ATOM_RED"]
-    raise SystemExit(f"unknown config {name}")
+            "COMPRESS; BMW_NNZ_BLOCK(2048); BMT_NNZ_BLOCK(64); BMT_PAD(BMW,4); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=1024,grid=2); GMEM_ATOM_RED"]
+    else:
+        raise SystemExit(f"unknown config {name}")
+    wl = WORKLOAD[name]
+    b = best_graph(wl)
+    if b:
+        seeds = [b] + [s for s in seeds if s != b]
+    return coo, wl, seeds
 
 
 def csr_of(coo):
@@ -143,34 +162,31 @@ def to_csr(obj):
     return synth.Csr(obj.m, obj.n, csr_of(obj), obj.col.astype(np.int32), obj.val, obj.name)
 
 
-def reference_arm(args, coo, wl, scaling="strong"):
-    """The oracle (long-double CSR SpMV, oracle/spmv_ref.c) on the host cores."""
+def reference_arm(args, coo, wl):
+    """The oracle (long-double CSR SpMV, oracle/spmv_ref.c) on the host cores: every step one
+    full pass over the same matrix as our arm (same config); median of the steps."""
     from oracle import spmv as S
     rp = csr_of(coo)
     x, _ = synth.vectors(coo.n, coo.m, 2, coo.val.dtype)
     cores = os.cpu_count() or 1
-    # bounded sample: the first rows covering ~1/8 of the nonzeros (C2: ~2.6M nnz) per step
-    frac_rows = max(1, coo.m // 8)
-    srp = rp[:frac_rows + 1]
-    nnz_s = int(srp[-1])
-    col, val = coo.col[:nnz_s], coo.val[:nnz_s].astype(np.float64)
-    for _ in range(max(1, args.warmup)):
-        S.spmv_csr(srp, col, val, x, nthreads=cores)
+    col, val = coo.col, coo.val.astype(np.float64)
+    for _ in range(max(1, min(args.warmup, 2))):
+        S.spmv_csr(rp, col, val, x, nthreads=cores)
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        S.spmv_csr(srp, col, val, x, nthreads=cores)
+        S.spmv_csr(rp, col, val, x, nthreads=cores)
         ts.append(time.perf_counter() - t0)
-    t = statistics.mean(ts)
-    v = 2.0 * nnz_s / t / 1e9
-    sample = f"first {frac_rows} rows ({nnz_s} nnz) of {wl} per step, long double, {cores} threads"
+    t = statistics.median(ts)
+    v = 2.0 * coo.nnz / t / 1e9
+    sample = f"{args.steps} full passes over {wl} ({coo.nnz} nnz), long double, {cores} threads"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": scaling, "vs_baseline": None, "dtype": "f64x", "data": "synthetic",
-            "config": {"workload": wl, "nnz": coo.nnz, "rows": coo.m},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64x", "data": "synthetic",
+            "config": {"workload": wl, "nnz": coo.nnz, "rows": coo.m, "same_config": True},
             "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
 def cpu_baseline(coo, wl, budget_s=10.0):
@@ -215,94 +231,89 @@ def cdev():
     return "cpu" if os.environ.get("AS_BENCH_BACKEND") == "gloo" else "cuda"
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
-    ap.add_argument("--graph", default=None, help="skip the search and time this graph")
-    ap.add_argument("--search-budget", type=float, default=20.0)
-    ap.add_argument("--search-candidates", type=int, default=24)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--exchange", default="none", choices=["none", "allgather", "halo", "nccl", "peer", "peer_halo"],
-                    help="y -> next x exchange after the SpMV (N > 1), timed separately: allgather/halo "
-                         "over torch.distributed; nccl/peer = as_spmv_dist (C-ABI: SpMV + AllGatherV, or "
-                         "SpMV + peer-memory push; peer_halo: only the rows each peer's band reads), "
-                         "timed as whole steps")
-    ap.add_argument("--profile", action="store_true", help="short run for ncu (no search/baseline/e2e)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1 on c2: weak = the Laplacian grows to 2048 x 2048N and each rank owns one "
-                         "2048 x 2048 ROW_DIV band (per-GPU work fixed); strong = C2 itself cut into N bands")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if not args.profile else args.warmup
+class Timer:
+    """CUDA-event timing on the launching stream with an L2 flush (write + read back of 2 x
+    L2, outside the events) before every timed call."""
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    def __init__(self, torch, stream, local, no_flush):
+        self.torch, self.stream, self.no_flush = torch, stream, no_flush
+        l2 = torch.cuda.get_device_properties(local).L2_cache_size
+        self.flush_buf = torch.empty(2 * l2, dtype=torch.uint8, device="cuda")
 
-    weak = world > 1 and args.config == "c2" and args.scaling == "weak"
-    if weak:
-        # weak scaling of the ROW_DIV path: global grid 2048 x 2048*world, rank r generates
-        # only its band (grid rows [2048r, 2048(r+1)), global columns)
-        g = 2048
-        coo = synth.c2_lap2d_band(g, g * world, g * rank, g * (rank + 1))
-        wl, seeds = f"lap2d-{g}x{g * world}", C2_SEEDS
-    else:
-        coo, wl, seeds = load_config(args.config)
-        coo = to_csr(coo)
-    if args.impl == "reference":
-        if rank == 0:
-            reference_arm(args, coo, wl, "weak" if args.config == "c2" and args.scaling == "weak" else "strong")
-        return
+    def flush(self):
+        if not self.no_flush:
+            self.flush_buf.zero_()
+            self.flush_buf.view(self.torch.int64).sum()
 
-    import torch
-    import paper_2212_10432_b200 as asp
+    def steps(self, fn, n):
+        torch = self.torch
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for e0, e1 in evs:
+            self.flush()
+            e0.record(self.stream)
+            fn()
+            e1.record(self.stream)
+        torch.cuda.synchronize()
+        return [e0.elapsed_time(e1) for e0, e1 in evs]
 
-    if os.environ.get("AS_BENCH_BACKEND") == "gloo":
-        local = 0
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        # AS_BENCH_BACKEND=gloo: control plane over gloo so that N ranks can share one GPU
-        # (single-GPU validation of the N > 1 code path; the exchange kinds need nccl)
-        if os.environ.get("AS_BENCH_BACKEND") == "gloo":
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    if weak:
-        A = asp.Matrix.from_csr(coo.m, coo.n, coo.row_ptr, coo.col, coo.val)
-        cuts = np.arange(world + 1, dtype=np.int64) * coo.m
-        m_global = coo.m * world
-    else:
-        A_full = asp.Matrix.from_csr(coo.m, coo.n, coo.row_ptr, coo.col, coo.val)
-        cuts = A_full.row_cuts(world)
-        m_global = coo.m
-    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
-    A = A if weak else (A_full if world == 1 else A_full.row_slice(r0, r1))
-    nnz_local = A.nnz
-    stream = torch.cuda.current_stream()
+def dominant_of(P, dx, dy, timer, npass):
+    """Per-launch device times (as_plan_profile, CUDA events between the launches, L2 flushed
+    before each pass) and per-launch algorithmic bytes; the dominant launch."""
+    acc = None
+    for _ in range(npass):
+        timer.flush()
+        prof = P.profile(dx, dy, reps=1, stream=timer.stream)
+        acc = [[n, ms, by] for n, ms, by in prof] if acc is None else [[a[0], a[1] + p_[1], a[2]] for a, p_ in zip(acc, prof)]
+    per = [(n, ms / npass, by) for n, ms, by in acc]
+    name, dms, dby = max(per, key=lambda e: e[1])
+    return {"kernel": name, "ms": dms, "bytes": dby, "launches": [{"kernel": n, "ms": ms, "bytes": by} for n, ms, by in per]}
 
+
+def gather_roofline(torch, coo, dx, timer, reps):
+    """tools/gather_roofline.cu on this matrix's own (val, col) arrays in CSR order: stream
+    every pair once and gather x[col] (no reduction, no y).  Returns the median time."""
+    here = os.path.join(ROOT, "tools")
+    so = os.path.join(here, "libgather_roofline.so")
+    src = os.path.join(here, "gather_roofline.cu")
+    if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                               "-shared", "-Xcompiler", "-fPIC", "-o", so, src])
+    lib = ctypes.CDLL(so)
+    lib.gr_launch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                              ctypes.c_int, ctypes.c_void_p]
+    dcol = torch.from_numpy(np.ascontiguousarray(coo.col, np.int32)).cuda()
+    dval = torch.from_numpy(np.ascontiguousarray(coo.val)).cuda()
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    dt = 0 if coo.val.dtype == np.float32 else 1
+    s = timer.stream.cuda_stream
+
+    def run():
+        rc = lib.gr_launch(dt, 1, dval.data_ptr(), dcol.data_ptr(), dx.data_ptr(), None, 0, coo.nnz, out.data_ptr(),
+                           2 * nsm, 1024, s)
+        assert rc == 0, rc
+    for _ in range(3):
+        run()
+    ms = statistics.median(timer.steps(run, reps))
+    del dcol, dval
+    return ms
+
+
+def run_config(args, torch, asp, name, A, coo, wl, seeds, graph, search, local, timer, with_e2e, budget):
+    """Plan (search or fixed graph), then time args.steps steps (median) and profile the
+    dominant launch.  Returns (result dict, plan, dx, dy)."""
+    stream = timer.stream
     t_plan = time.perf_counter()
-    if args.config == "c1" and not args.graph:
-        # BASELINE configs[0] names a single graph (COMPRESS + BMT_NNZ_BLOCK(4) + thread reduction)
-        args.graph = seeds[0]
-    if args.graph:
-        P = asp.Plan(A, args.graph, device=local)
-        graph = str(asp.Graph(args.graph))
-        searched = False
-    elif args.profile:
-        P = asp.Plan(A, seeds[0], device=local)
-        graph = str(asp.Graph(seeds[0]))
+    if graph:
+        P = asp.Plan(A, graph, device=local)
+        graph = str(asp.Graph(graph))
         searched = False
     else:
         P, graph = asp.search(A, device=local, seed=1, max_candidates=args.search_candidates,
-                              budget_seconds=args.search_budget, warmup=3, reps=10, seed_graphs=seeds,
-                              log_path=os.path.join(ROOT, "gpurun_out", f"search_{wl}_r{rank}.jsonl")
+                              budget_seconds=budget, warmup=3, reps=10, seed_graphs=seeds,
+                              log_path=os.path.join(ROOT, "gpurun_out", f"search_{wl}.jsonl")
                               if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else None)
         searched = True
     plan_s = time.perf_counter() - t_plan
@@ -310,162 +321,44 @@ def main():
     dt = coo.val.dtype
     x, _ = synth.vectors(coo.n, coo.m, 2, dt)
     dx = torch.from_numpy(x).cuda()
-    m_local = r1 - r0
-    dy = torch.zeros(m_local, dtype=torch.float64 if dt == np.float64 else torch.float32, device="cuda")
-    l2 = torch.cuda.get_device_properties(local).L2_cache_size
-    flush = torch.empty(2 * l2, dtype=torch.uint8, device="cuda")
+    dy = torch.zeros(coo.m, dtype=torch.float64 if dt == np.float64 else torch.float32, device="cuda")
 
     def step():
         P.spmv(1.0, dx, 0.0, dy, stream)
-
-    def flush_l2():
-        # write 2x L2 (the flush), then read it back so the dirty lines are written back to
-        # HBM before the timed region rather than during it
-        flush.zero_()
-        flush.view(torch.int64).sum()
-
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with Clocks(local) as clk:
-        torch.cuda.synchronize()
-        for e0, e1 in evs:
-            if not args.no_flush:
-                flush_l2()
-            e0.record(stream)
-            step()
-            e1.record(stream)
-        torch.cuda.synchronize()
-        gather_ms = None
-        if args.exchange in ("nccl", "peer", "peer_halo") and dist:
-            # as_spmv_dist: band SpMV into y_full + the exchange inside the library
-            from paper_2212_10432_b200 import dist as D
-            d = D.init_dist(rank, world, local, cuts, nccl=args.exchange == "nccl")
-            y_full = torch.zeros(m_global, dtype=dy.dtype, device="cuda")
-            kind = "peer" if args.exchange == "peer_halo" else args.exchange
-            if kind == "peer":
-                D.register_peers(d, y_full)
-            if args.exchange == "peer_halo":
-                d.set_windows(D.gather_spans(A.col_span()))
-            for _ in range(3):
-                d.spmv(P, 1.0, dx, 0.0, y_full, kind, stream)
-            torch.cuda.synchronize()
-            dist.barrier()
-            gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(args.steps)]
-            for g0, g1 in gev:
-                if not args.no_flush:
-                    flush_l2()
-                g0.record(stream)
-                d.spmv(P, 1.0, dx, 0.0, y_full, kind, stream)
-                g1.record(stream)
-            torch.cuda.synchronize()
-            d.check()
-            gather_ms = statistics.mean(g0.elapsed_time(g1) for g0, g1 in gev)
-            dist.barrier()
-            d.close()
-        elif args.exchange != "none" and dist:
-            # y -> next x: all-gather (uneven bands, NCCL broadcasts) or halo (P2P of the
-            # band's column span only, NEXT-1), timed separately from the SpMV
-            from paper_2212_10432_b200 import dist as D
-            x_next = torch.zeros(m_global, dtype=dy.dtype, device="cuda")
-            moves = D.halo_plan(D.gather_spans(A.col_span()), cuts) if args.exchange == "halo" else None
-            dist.barrier()
-            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            g0.record(stream)
-            if args.exchange == "halo":
-                D.halo_exchange(dy, x_next, cuts, moves)
-            else:
-                D.allgather_rows(dy, x_next, cuts)
-            g1.record(stream)
-            torch.cuda.synchronize()
-            gather_ms = g0.elapsed_time(g1)
-    if gather_ms is not None:
-        gm = torch.tensor([gather_ms], device=cdev(), dtype=torch.float64)
-        dist.all_reduce(gm, op=dist.ReduceOp.MAX)
-        gather_ms = float(gm.item())
-    ms = [e0.elapsed_time(e1) for e0, e1 in evs]
-    t_ms = statistics.mean(ms)
-    if dist:
-        tt = torch.tensor([t_ms], device=cdev(), dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
-        tot = torch.tensor([float(nnz_local)], device=cdev(), dtype=torch.float64)
-        dist.all_reduce(tot)
-        nnz_total = int(tot.item())
-    else:
-        nnz_total = nnz_local
-    gflops = 2.0 * nnz_total / (t_ms * 1e-3) / 1e9
+        ms = timer.steps(step, args.steps)
+    t_ms = statistics.median(ms)
     hbm, hbm_kind = peaks()
+    dom = dominant_of(P, dx, dy, timer, max(3, args.steps // 3))
+    dom["share_of_step"] = dom["ms"] / t_ms if t_ms else None
+    achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9 if dom["ms"] > 0 else 0.0
     achieved_step = info["bytes_model"] / (t_ms * 1e-3) / 1e9
     launches = int(info["n_launches"])
-    # dominant kernel: per-launch device times (as_plan_profile, CUDA events between the
-    # launches, L2 flushed before each pass) and per-launch algorithmic bytes
-    dominant = None
-    if not args.profile:
-        acc = None
-        for _ in range(max(3, args.steps // 3)):
-            if not args.no_flush:
-                flush_l2()
-            prof = P.profile(dx, dy, reps=1, stream=stream)
-            acc = [[n, ms, by] for n, ms, by in prof] if acc is None else [[a[0], a[1] + p_[1], a[2]] for a, p_ in zip(acc, prof)]
-        npass = max(3, args.steps // 3)
-        per = [(n, ms / npass, by) for n, ms, by in acc]
-        name, dms, dby = max(per, key=lambda e: e[1])
-        dominant = {"kernel": name, "ms": dms, "bytes": dby, "share_of_step": dms / t_ms if t_ms else None,
-                    "launches": [{"kernel": n, "ms": ms, "bytes": by} for n, ms, by in per]}
-    achieved_gbs = (dominant["bytes"] / (dominant["ms"] * 1e-3) / 1e9) if dominant and dominant["ms"] > 0 else achieved_step
-
-    # e2e through the C-ABI with host buffers (pinned), copies inside the timed region.  Two
-    # plans: the searched one (copies, kernels, copies back to back) and the same graph under
-    # ROW_DIV into E2E_BANDS bands, which as_spmv_host pipelines (chunked H2D of x and D2H of
-    # y on copy streams overlapping the band kernels); the faster is reported.
-    e2e = None
-    if not args.profile:
-        xh = torch.from_numpy(x).pin_memory()
-        yh = torch.zeros(m_local, dtype=dy.dtype).pin_memory()
-        xn, yn = xh.numpy(), yh.numpy()
-        cands = [(graph, P)]
-        if "ROW_DIV" not in graph and m_local >= 8 * E2E_BANDS:
-            cut = ",".join(str(m_local * i // E2E_BANDS) for i in range(1, E2E_BANDS))
-            g_pipe = f"ROW_DIV(cuts=[{cut}]) {{ {graph} }}"
-            try:
-                cands.append((g_pipe, asp.Plan(A, g_pipe, device=local)))
-            except asp.AsError:
-                pass
-        res = []
-        for g_e, P_e in cands:
-            for _ in range(2):
-                P_e.spmv_host(1.0, xn, 0.0, yn, stream)
-            e2e_ms = []
-            for _ in range(max(3, args.steps // 3)):
-                if not args.no_flush:
-                    flush_l2()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                P_e.spmv_host(1.0, xn, 0.0, yn, stream)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                e2e_ms.append(e0.elapsed_time(e1))
-            res.append((statistics.mean(e2e_ms), g_e, int(P_e.info()["n_launches"])))
-        tm, g_e, l_e = min(res)
-        if dist:
-            tt = torch.tensor([tm], device=cdev(), dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            tm = float(tt.item())
-        sv = dx.element_size()
-        e2e = {"value": 2.0 * nnz_total / (tm * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": tm,
-               "h2d_bytes_per_step": int(coo.n * sv), "d2h_bytes_per_step": int(m_local * sv),
-               "graph": g_e, "launches_per_step": l_e,
-               "candidates_ms": {("pipelined" if i else "searched"): r[0] for i, r in enumerate(res)}}
-
-    # warm steady state: back-to-back calls in one event window, no
-    # flush -- for C2 the working set is a small multiple of L2
-    warm = None
-    if not args.profile:
+    r = {"workload": wl, "rows": coo.m, "nnz": coo.nnz, "dtype": "f64" if dt == np.float64 else "f32",
+         "graph": graph, "searched": searched, "plan_and_search_s": round(plan_s, 2), "kernels": info["kernels"],
+         "ms_per_step": t_ms, "ms_min": min(ms), "ms_mean": statistics.mean(ms), "steps": args.steps,
+         "gflops": 2.0 * coo.nnz / (t_ms * 1e-3) / 1e9, "bytes_model": info["bytes_model"],
+         "bytes_floor": info["bytes_floor"], "launches": launches, "clocks": clk.summary(),
+         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                      "peak_kind": hbm_kind, "frac_of_8tbs": achieved / 8000.0, "achieved_step": achieved_step,
+                      "frac_step": achieved_step / hbm, "dominant": dom}}
+    # traffic: the committed ncu capture of this workload's dominant kernel, when it is the
+    # same kernel form (profiles/traffic_<workload>.json)
+    prof = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
+    r["roofline"]["traffic"] = None
+    if os.path.exists(prof):
+        try:
+            tj = json.load(open(prof))
+            if tj.get("kernels") == info["kernels"]:
+                r["roofline"]["traffic"] = tj["dram_bytes_per_launch"]
+                r["roofline"]["traffic_src"] = tj.get("src")
+        except Exception:
+            pass
+    if with_e2e:
+        r["e2e"] = e2e_of(args, torch, asp, P, A, coo, graph, local, timer)
         nw = 100 if t_ms < 1.0 else 20
         w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -475,84 +368,288 @@ def main():
         w1.record(stream)
         torch.cuda.synchronize()
         wm = w0.elapsed_time(w1) / nw
-        warm = {"ms_per_step": wm, "gflops": 2.0 * nnz_local / (wm * 1e-3) / 1e9, "calls": nw}
+        r["warm"] = {"ms_per_step": wm, "gflops": 2.0 * coo.nnz / (wm * 1e-3) / 1e9, "calls": nw}
+    return r, P, dx, dy
 
-    # CUDA-graph replay of the same plan (AS_PLAN_GRAPH): the launch-latency floor of small
-    # matrices ("C1 also reports CUDA-Graph replay time"); small workloads only
-    graph_replay = None
-    if not args.profile and nnz_local < 50_000_000:
-        Pg = asp.Plan(A, graph, device=local, graph_replay=True)
-        for _ in range(3):
-            Pg.spmv(1.0, dx, 0.0, dy, stream)
-        gts = []
-        for _ in range(args.steps):
-            if not args.no_flush:
-                flush_l2()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            Pg.spmv(1.0, dx, 0.0, dy, stream)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            gts.append(e0.elapsed_time(e1))
-        graph_replay = {"ms_per_step": statistics.mean(gts), "gflops": 2.0 * nnz_local / (statistics.mean(gts) * 1e-3) / 1e9}
-        del Pg
 
-    if rank != 0:
-        if dist:
-            dist.destroy_process_group()
-        return
-    traffic = None
-    # weak-scaled C2 bands run the same per-rank kernel as C2 itself
-    prof = os.path.join(ROOT, "profiles", f"traffic_{'lap2d-2048' if weak else wl}.json")
-    if os.path.exists(prof):
+def e2e_of(args, torch, asp, P, A, coo, graph, local, timer):
+    """e2e through the C-ABI with pinned host buffers, copies inside the timed region: the
+    searched plan (copies, kernels, copies back to back) and the same graph under ROW_DIV into
+    E2E_BANDS bands, which as_spmv_host pipelines; the faster is reported."""
+    x, _ = synth.vectors(coo.n, coo.m, 2, coo.val.dtype)
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.zeros(coo.m, dtype=torch.float64 if coo.val.dtype == np.float64 else torch.float32).pin_memory()
+    xn, yn = xh.numpy(), yh.numpy()
+    cands = [(graph, P)]
+    if "ROW_DIV" not in graph and coo.m >= 8 * E2E_BANDS:
+        cut = ",".join(str(coo.m * i // E2E_BANDS) for i in range(1, E2E_BANDS))
+        g_pipe = f"ROW_DIV(cuts=[{cut}]) {{ {graph} }}"
         try:
-            tj = json.load(open(prof))
-            if tj.get("kernels") == info["kernels"]:
-                traffic = tj["dram_bytes_per_launch"]
-        except Exception:
+            cands.append((g_pipe, asp.Plan(A, g_pipe, device=local)))
+        except asp.AsError:
             pass
+    res = []
+    for g_e, P_e in cands:
+        for _ in range(2):
+            P_e.spmv_host(1.0, xn, 0.0, yn, timer.stream)
+        ms = timer.steps(lambda: P_e.spmv_host(1.0, xn, 0.0, yn, timer.stream), max(3, args.steps // 3))
+        res.append((statistics.median(ms), g_e, int(P_e.info()["n_launches"])))
+    tm, g_e, l_e = min(res)
+    sv = xn.itemsize
+    return {"value": 2.0 * coo.nnz / (tm * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": tm,
+            "h2d_bytes_per_step": int(coo.n * sv), "d2h_bytes_per_step": int(coo.m * sv), "graph": g_e,
+            "launches_per_step": l_e, "candidates_ms": {("pipelined" if i else "searched"): r[0] for i, r in enumerate(res)}}
+
+
+def single_gpu(args, torch, asp):
+    t0 = time.perf_counter()
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream()
+    timer = Timer(torch, stream, 0, args.no_flush)
+    name = args.config or "c3"
+    coo, wl, seeds = load_config(name)
+    coo = to_csr(coo)
+    A = asp.Matrix.from_csr(coo.m, coo.n, coo.row_ptr, coo.col, coo.val)
+    graph = args.graph or (seeds[0] if name == "c1" else None)
+    if args.no_search and not graph:
+        graph = seeds[0]
+    head, P, dx, dy = run_config(args, torch, asp, name, A, coo, wl, seeds, graph, not graph, 0, timer, True,
+                                 args.search_budget)
+    # the gather roofline of this matrix (tools/gather_roofline.cu, timed live)
+    gr = None
+    if not args.no_gather and name in ("c3", "c4", "c5", "c3s", "c5s"):
+        try:
+            gms = gather_roofline(torch, coo, dx, timer, max(5, args.steps // 2))
+            dk = head["roofline"]["dominant"]
+            gr = {"ms": gms, "achieved_gbs": head["bytes_model"] / (gms * 1e-3) / 1e9,
+                  "frac_step": gms / head["ms_per_step"], "frac_dominant": gms / dk["ms"] if dk["ms"] else None,
+                  "note": "time to stream every (val, col) pair once and gather x[col] (no reduction, no y), "
+                          "CSR order, same x, L2 flushed: frac = gather time / SpMV time"}
+        except Exception as e:  # the measurement tool is optional; the SpMV numbers stand
+            gr = {"error": str(e)[:200]}
+    head["roofline"]["gather"] = gr
+    cpu = None if args.no_cpu_baseline else cpu_baseline(coo, wl)
+    launches = head["launches"] * args.steps
+    del P, dx, dy, A, coo
+    torch.cuda.empty_cache()
+    extras = []
+    for cfg in [c for c in args.extra.split(",") if c and c != name]:
+        if time.perf_counter() - t0 > args.max_seconds:
+            extras.append({"workload": WORKLOAD.get(cfg, cfg), "skipped": "time budget"})
+            continue
+        try:
+            c2, wl2, seeds2 = load_config(cfg)
+            c2 = to_csr(c2)
+            A2 = asp.Matrix.from_csr(c2.m, c2.n, c2.row_ptr, c2.col, c2.val)
+            r2, P2, dx2, dy2 = run_config(args, torch, asp, cfg, A2, c2, wl2, seeds2, seeds2[0], False, 0, timer,
+                                          False, 0)
+            extras.append(r2)
+            del P2, dx2, dy2, A2, c2
+        except Exception as e:
+            extras.append({"workload": WORKLOAD.get(cfg, cfg), "error": str(e)[:300]})
+        torch.cuda.empty_cache()
+    hr = head["roofline"]
     line = {
-        "metric": METRIC, "value": gflops, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
-        "scaling": "weak" if (weak or world == 1) and args.config == "c2" and args.scaling == "weak" else "strong",
-        "vs_baseline": None, "dtype": "f64" if dt == np.float64 else "f32", "data": "synthetic",
-        "config": {"workload": wl, "rows": m_global, "nnz": nnz_total, "graph": graph, "searched": searched,
-                   "alpha": 1.0, "beta": 0.0, "l2": "flushed before every step" if not args.no_flush else "not flushed",
-                   "parallelism": f"row_div{world}", "plan_and_search_s": round(plan_s, 2),
-                   "kernels": info["kernels"], "bytes_model": info["bytes_model"], "bytes_floor": info["bytes_floor"]},
-        "hbm_gbs_model": achieved_gbs,
-        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved_gbs / hbm, "traffic": traffic, "peak_kind": hbm_kind,
-                     "frac_of_8tbs": achieved_gbs / 8000.0,
-                     # measured DRAM bytes of the dominant kernel (ncu, committed) over the same
-                     # time: the model counts x and y in full although part of them stays in
-                     # L2, and a read-dominated stream can beat the copy peak, so frac may
-                     # exceed 1 where frac_dram does not
-                     "achieved_dram": (traffic / (t_ms * 1e-3) / 1e9) if traffic else None,
-                     "frac_dram": (traffic / (t_ms * 1e-3) / 1e9 / hbm) if traffic else None,
-                     "achieved_step": achieved_step, "frac_step": achieved_step / hbm,
-                     "dominant": dominant,
-                     "note": "achieved = algorithmic bytes of the dominant kernel / its mean launch duration "
-                             "(CUDA events between launches, as_plan_profile); achieved_step = the plan's "
-                             "bytes model / the step time" + (" (single launch)" if launches == 1 else
-                                                              f" ({launches} launches)")},
-        "gpu_launches": launches * args.steps,
-        "clocks": clk.summary(),
-        "e2e": e2e,
+        "metric": METRIC, "value": head["gflops"], "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": head["dtype"], "data": "synthetic",
+        "config": {"workload": wl, "rows": head["rows"], "nnz": head["nnz"], "graph": head["graph"],
+                   "searched": head["searched"], "alpha": 1.0, "beta": 0.0,
+                   "l2": "flushed before every step (inputs 2.4 GB > L2 as well)" if not args.no_flush else "not flushed",
+                   "timing": f"median of {args.steps} steps, CUDA events on the launch stream",
+                   "parallelism": "row_div1", "plan_and_search_s": head["plan_and_search_s"],
+                   "kernels": head["kernels"], "bytes_model": head["bytes_model"], "bytes_floor": head["bytes_floor"]},
+        "hbm_gbs_model": hr["achieved"],
+        "roofline": {k: hr[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
+        "roofline_detail": {k: v for k, v in hr.items() if k not in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
+        "gpu_launches": launches,
+        "clocks": head["clocks"],
+        "e2e": head["e2e"],
+        "warm": head.get("warm"),
+        "configs": extras,
     }
-    if graph_replay is not None:
-        line["graph_replay"] = graph_replay
-    if warm is not None:
-        line["warm"] = warm
-    if gather_ms is not None:
-        line["exchange"] = {"kind": args.exchange, "ms": gather_ms,
-                            "timed": "spmv + exchange per step (as_spmv_dist)" if args.exchange in ("nccl", "peer", "peer_halo")
-                            else "exchange only"}
-    if not args.no_cpu_baseline and not args.profile and world == 1:
-        line["cpu_baseline"] = cpu_baseline(coo, wl)
-    print(json.dumps(line))
-    if dist:
-        dist.destroy_process_group()
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def multi_gpu(args, torch, asp, world, rank, local):
+    """ROW_DIV across ranks: rank-local band generation (C5) or bands of a shared config."""
+    import torch.distributed as dist
+    if os.environ.get("AS_BENCH_BACKEND") == "gloo":
+        local = 0
+    torch.cuda.set_device(local)
+    if os.environ.get("AS_BENCH_BACKEND") == "gloo":
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    timer = Timer(torch, stream, local, args.no_flush)
+    name = args.config or "c5"
+    small = os.environ.get("AS_BENCH_C5_SCALE")  # tests: a shape-preserving small C5
+    if name == "c5":
+        m, nnz = (1 << 26, 1 << 30) if not small else (1 << int(small), 1 << (int(small) + 4))
+        rp = synth.c5_row_ptr(m=m, nnz=nnz)
+        cuts = asp.row_cuts_from_ptr(rp, world)
+        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+        band = synth.c5_band_rows(rp, r0, r1)
+        wl = WORKLOAD["c5"] + (f"-2^{small}" if small else "")
+        seeds = [best_graph(WORKLOAD["c5"])] if best_graph(WORKLOAD["c5"]) else []
+        m_global, n_global = m, m
+        scaling = "strong"
+    else:
+        coo, wl, seeds = load_config(name)
+        coo = to_csr(coo)
+        cuts = asp.row_cuts_from_ptr(coo.row_ptr, world)
+        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+        a, e = int(coo.row_ptr[r0]), int(coo.row_ptr[r1])
+        band = synth.Csr(r1 - r0, coo.n, coo.row_ptr[r0:r1 + 1] - a, coo.col[a:e], coo.val[a:e], coo.name)
+        m_global, n_global = coo.m, coo.n
+        scaling = "strong"
+    A = asp.Matrix.from_csr(band.m, band.n, band.row_ptr, band.col, band.val)
+    graph = args.graph or (seeds[0] if seeds else None)
+    t_plan = time.perf_counter()
+    if graph and (args.no_search or not args.search_budget):
+        P = asp.Plan(A, graph, device=local)
+        graph = str(asp.Graph(graph))
+    else:
+        P, graph = asp.search(A, device=local, seed=1 + rank, max_candidates=args.search_candidates,
+                              budget_seconds=args.search_budget, warmup=3, reps=10, seed_graphs=[graph] if graph else [])
+    plan_s = time.perf_counter() - t_plan
+    info = P.info()
+    dt = band.val.dtype
+    tdt = torch.float64 if dt == np.float64 else torch.float32
+    # replicated x (every rank holds the whole vector, north_star); deterministic per index
+    x = torch.from_numpy(synth.vectors(n_global, 1, 2, dt)[0]).cuda()
+    dy = torch.zeros(band.m, dtype=tdt, device="cuda")
+
+    def step():
+        P.spmv(1.0, x, 0.0, dy, stream)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    with Clocks(local) as clk:
+        ms = timer.steps(step, args.steps)
+    t_ms = statistics.median(ms)
+    tt = torch.tensor([t_ms], device=cdev(), dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max = float(tt.item())
+    tot = torch.tensor([float(band.nnz), float(info["bytes_model"])], device=cdev(), dtype=torch.float64)
+    dist.all_reduce(tot)
+    nnz_total, bytes_total = int(tot[0].item()), float(tot[1].item())
+    # y exchange for the next iterate, timed separately (SURVEY §8(e)): the all-gather alone
+    # (uneven bands: one NCCL broadcast per rank), and as_spmv_dist (SpMV + NCCL AllGatherV
+    # inside the library) per step; a watchdog keeps a failing exchange from hiding the line
+    exch = {}
+    done = threading.Event()
+
+    def watchdog():
+        if not done.wait(args.exchange_timeout):
+            if rank == 0:
+                exch["error"] = "exchange timed out"
+                emit()
+            os._exit(0)
+    line_box = {}
+
+    def emit():
+        line = line_box["line"]
+        line["exchange"] = exch
+        print(json.dumps(line), flush=True)
+    hbm, hbm_kind = peaks()
+    line_box["line"] = {
+        "metric": METRIC, "value": 2.0 * nnz_total / (t_max * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64" if dt == np.float64 else "f32", "data": "synthetic",
+        "config": {"workload": wl, "rows": m_global, "nnz": nnz_total, "graph": graph, "parallelism": f"row_div{world}",
+                   "band_generation": "rank-local" if name == "c5" else "sliced", "plan_and_search_s": round(plan_s, 2),
+                   "kernels": info["kernels"], "l2": "flushed before every step" if not args.no_flush else "not flushed",
+                   "timing": f"median of {args.steps} steps per rank, max over ranks"},
+        "roofline": {"bound": "hbm", "achieved": bytes_total / (t_max * 1e-3) / 1e9 / world, "peak": hbm,
+                     "unit": "GB/s", "frac": bytes_total / (t_max * 1e-3) / 1e9 / world / hbm, "traffic": None,
+                     "peak_kind": hbm_kind, "note": "per-GPU: sum of the ranks' plan bytes models / max step / N"},
+        "gpu_launches": int(info["n_launches"]) * args.steps,
+        "clocks": clk.summary(),
+        "e2e": None,
+    }
+    if args.exchange != "none":
+        threading.Thread(target=watchdog, daemon=True).start()
+        try:
+            from paper_2212_10432_b200 import dist as D
+            y_full = torch.zeros(m_global, dtype=tdt, device="cuda")
+            dist.barrier()
+            ag = timer.steps(lambda: D.allgather_rows(dy, y_full, cuts), max(3, args.steps // 3))
+            t_ag = torch.tensor([statistics.median(ag)], device=cdev(), dtype=torch.float64)
+            dist.all_reduce(t_ag, op=dist.ReduceOp.MAX)
+            exch["allgather_ms"] = float(t_ag.item())
+            exch["allgather_bytes_per_rank"] = int((m_global - band.m) * dy.element_size())
+            if args.exchange in ("nccl", "peer", "peer_halo") and cdev() == "cuda":
+                d = D.init_dist(rank, world, local, cuts, nccl=args.exchange == "nccl")
+                kind = "peer" if args.exchange == "peer_halo" else args.exchange
+                if kind == "peer":
+                    D.register_peers(d, y_full)
+                if args.exchange == "peer_halo":
+                    d.set_windows(D.gather_spans(A.col_span()))
+                for _ in range(3):
+                    d.spmv(P, 1.0, x, 0.0, y_full, kind, stream)
+                torch.cuda.synchronize()
+                dist.barrier()
+                sd = timer.steps(lambda: d.spmv(P, 1.0, x, 0.0, y_full, kind, stream), args.steps)
+                d.check()
+                t_sd = torch.tensor([statistics.median(sd)], device=cdev(), dtype=torch.float64)
+                dist.all_reduce(t_sd, op=dist.ReduceOp.MAX)
+                exch["kind"] = args.exchange
+                exch["spmv_plus_exchange_ms"] = float(t_sd.item())
+                exch["spmv_plus_exchange_gflops"] = 2.0 * nnz_total / (float(t_sd.item()) * 1e-3) / 1e9
+                d.close()
+        except Exception as e:
+            exch["error"] = str(e)[:300]
+        done.set()
+    if rank == 0:
+        emit()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, help="c1..c5 (default: c3 at N=1, c5 at N>1)")
+    ap.add_argument("--graph", default=None, help="skip the search and time this graph")
+    ap.add_argument("--no-search", action="store_true", help="time the committed best graph")
+    ap.add_argument("--search-budget", type=float, default=60.0)
+    ap.add_argument("--search-candidates", type=int, default=24)
+    ap.add_argument("--extra", default="c2,c4,c5", help="other configs timed in the same run (N=1)")
+    ap.add_argument("--max-seconds", type=float, default=900.0, help="skip remaining extras after this")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gather", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["none", "allgather", "nccl", "peer", "peer_halo"],
+                    help="N > 1: y exchange timed after the SpMV (allgather alone, plus as_spmv_dist "
+                         "SpMV + exchange for nccl / peer / peer_halo)")
+    ap.add_argument("--exchange-timeout", type=float, default=300.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:  # the oracle on the host; under torchrun only rank 0 runs it
+            coo, wl, _ = load_config(args.config or ("c3" if world == 1 else "c5"))
+            reference_arm(args, to_csr(coo), wl)
+        return
+
+    import torch
+    import paper_2212_10432_b200 as asp
+    if world > 1:
+        multi_gpu(args, torch, asp, world, rank, local)
+    else:
+        single_gpu(args, torch, asp)
 
 
 if __name__ == "__main__":

@@ -358,6 +358,8 @@ def _compress_and_map(csr, st, rest, dtype):
             pcol.append(gcol)
             pval.append(gval)
         arrays["pad.width"] = np.asarray(widths, np.int64)
+        # padded slot offset of every group (nt * W slots each), plus the total
+        arrays["pad.base"] = np.concatenate([[0], np.cumsum([p.shape[0] for p in pcol])]).astype(np.int64)
         arrays["pad.col"] = np.concatenate(pcol) if pcol else np.zeros(0, np.int64)
         arrays["pad.val"] = np.concatenate(pval) if pval else np.zeros(0, dtype)
 

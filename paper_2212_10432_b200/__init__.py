@@ -298,6 +298,14 @@ class Plan:
     def keys(self):
         return _string(_lib.as_plan_keys, self._h).split(";")
 
+    def device_keys(self):
+        """Keys of the device readback ("dev.p<i>.<name>", as_plan_export)."""
+        n = _sz(0)
+        _ck(_lib.as_plan_export(self._h, b"dev.keys", None, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(max(1, n.value))
+        _ck(_lib.as_plan_export(self._h, b"dev.keys", buf, ctypes.byref(n)))
+        return [k for k in buf.raw[:n.value].decode().split(";") if k]
+
     def export(self, key: str) -> np.ndarray:
         n = _sz(0)
         _ck(_lib.as_plan_export(self._h, key.encode(), None, ctypes.byref(n)))

@@ -327,6 +327,28 @@ as_status_t as_plan_info(as_plan_t P, as_plan_info_t* out) {
 as_status_t as_plan_export(as_plan_t P, const char* key, void* host_dst, size_t* bytes) {
   return guard([&] {
     if (!P || !key || !bytes) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    if (std::strncmp(key, "dev.", 4) == 0) {  // device readback (readback.cpp)
+      if (P->P->device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan has no device arrays");
+      auto arrs = device_arrays(*P->P);
+      std::vector<uint8_t> val;
+      bool found = false;
+      if (std::strcmp(key, "dev.keys") == 0) {
+        std::string s;
+        for (auto& kv : arrs) s += (s.empty() ? "" : ";") + kv.first;
+        val.assign(s.begin(), s.end());
+        found = true;
+      }
+      for (auto& kv : arrs)
+        if (kv.first == key) {
+          val = std::move(kv.second);
+          found = true;
+        }
+      if (!found) fail(AS_ERR_NOT_FOUND, std::string("no export key ") + key);
+      if (host_dst && *bytes < val.size()) fail(AS_ERR_INVALID_ARG, "destination too small");
+      if (host_dst && !val.empty()) std::memcpy(host_dst, val.data(), val.size());
+      *bytes = val.size();
+      return;
+    }
     if (!P->P->host_kept) fail(AS_ERR_INVALID_ARG, "plan built without AS_PLAN_KEEP_HOST");
     size_t need = 0;
     if (!export_key(P->P->host, key, nullptr, &need)) fail(AS_ERR_NOT_FOUND, std::string("no export key ") + key);

@@ -739,6 +739,9 @@ std::map<std::string, std::pair<std::vector<uint8_t>, int>> export_all(const Hos
       if (!p.bitmap.empty() || (p.red[2] == RED_BITMAP && p.lv[2].nnz)) put(out, pre + "bmt.bitmap", p.bitmap);
       if (p.pad) {
         put(out, pre + "pad.width", p.pad_width);
+        std::vector<int64_t> pb = p.grp_base;  // padded slot offset of every group + total slots
+        pb.push_back((int64_t)p.pad_col.size());
+        put(out, pre + "pad.base", pb);
         put(out, pre + "pad.col", i64(p.pad_col));
         put_vals(out, pre + "pad.val", p.pad_val, hp.dt);
       }

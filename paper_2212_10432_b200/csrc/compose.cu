@@ -329,8 +329,8 @@ int launch_pad(const DevPart& p, const V* x, V* y, cudaStream_t s, int64_t g, in
 }
 
 template <class V, bool PAD, int WR, int BR>
-cudaError_t smem_optin(size_t bytes) {
-  return cudaFuncSetAttribute(k_compose<V, PAD, WR, BR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+cudaError_t optin_one(size_t bytes) {
+  return as::smem_optin(k_compose<V, PAD, WR, BR>, bytes);
 }
 template <class V>
 cudaError_t optin_all(size_t bytes) {
@@ -338,14 +338,14 @@ cudaError_t optin_all(size_t bytes) {
   auto f = [&](cudaError_t r) {
     if (r != cudaSuccess) e = r;
   };
-  f(smem_optin<V, false, RED_NONE, 2>(bytes));
-  f(smem_optin<V, false, RED_TOTAL, 2>(bytes));
-  f(smem_optin<V, false, RED_SEG, 2>(bytes));
-  f(smem_optin<V, false, RED_BITMAP, 2>(bytes));
-  f(smem_optin<V, true, RED_NONE, 2>(bytes));
-  f(smem_optin<V, true, RED_TOTAL, 2>(bytes));
-  f(smem_optin<V, true, RED_SEG, 2>(bytes));
-  f(smem_optin<V, true, RED_BITMAP, 2>(bytes));
+  f(optin_one<V, false, RED_NONE, 2>(bytes));
+  f(optin_one<V, false, RED_TOTAL, 2>(bytes));
+  f(optin_one<V, false, RED_SEG, 2>(bytes));
+  f(optin_one<V, false, RED_BITMAP, 2>(bytes));
+  f(optin_one<V, true, RED_NONE, 2>(bytes));
+  f(optin_one<V, true, RED_TOTAL, 2>(bytes));
+  f(optin_one<V, true, RED_SEG, 2>(bytes));
+  f(optin_one<V, true, RED_BITMAP, 2>(bytes));
   return e;
 }
 

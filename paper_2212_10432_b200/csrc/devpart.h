@@ -84,7 +84,7 @@ struct DevPart {
   // uploaded as NNZ_BLOCK(1) BMTs), BMTB -> child block range (BMWs, else BMTs), and whether
   // no level reduces below GMEM (every nonzero written on its own)
   int tred = 0, wred = 0, bred = 0;
-  int has_w = 0, has_b = 0, per_elem = 0;
+  int has_w = 0, has_b = 0, per_elem = 0, t_synth = 0;
   const int32_t* bmtb_child = nullptr;
   // hot-x cache (SET_RESOURCE xcache): xh_n columns staged in shared memory per CTA, encoded
   // as ~slot in col / pad_col; persistent grid of xh_ctas CTAs per SM

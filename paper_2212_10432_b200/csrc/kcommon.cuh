@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "devpart.h"
+#include "optin.h"
 
 namespace as {
 namespace {
@@ -357,4 +358,5 @@ __device__ __forceinline__ void warp_combine(int lane, bool hh, double cin, doub
 }
 
 }  // namespace
+
 }  // namespace as

@@ -1376,7 +1376,7 @@ int launch_l2_flush(void* buf, size_t bytes, int pattern, void* stream) {
 // bytes of dynamic shared memory; returns the CTAs per SM they reach (0 on failure)
 template <class K>
 static int xh_optin(K kern, size_t smem, int tpb) {
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  if (smem_optin(kern, smem) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, tpb, smem) != cudaSuccess) return 0;
   return n;
@@ -1427,10 +1427,8 @@ int prepare_part(DevPart& p) {
   if (p.fam == FAM_BLOCK_OFFSET && p.variant == 1) {  // TMA-staged CSR-stream
     const size_t sv = p.dtype == 1 ? 8 : 4;
     p.smem = 2 * ((size_t)p.smem_cap * (sv + 4) + (size_t)p.smem_rcap * 4) + (size_t)p.smem_cap * 8 + 16;
-    cudaError_t e = p.dtype == 1 ? cudaFuncSetAttribute(k_block_offset_tma<double>,
-                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem)
-                                 : cudaFuncSetAttribute(k_block_offset_tma<float>,
-                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    cudaError_t e = p.dtype == 1 ? smem_optin(k_block_offset_tma<double>, p.smem)
+                                 : smem_optin(k_block_offset_tma<float>, p.smem);
     if (e != cudaSuccess) return (int)e;
     int per_sm = 0;
     const int tpb = p.tpb > 0 ? p.tpb : 256;
@@ -1446,8 +1444,8 @@ int prepare_part(DevPart& p) {
     p.smem = (size_t)p.max_block_nnz * sizeof(double);
     if (p.smem > 48 * 1024) {
       cudaError_t e = p.dtype == 1
-                          ? cudaFuncSetAttribute(k_block_offset<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem)
-                          : cudaFuncSetAttribute(k_block_offset<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+                          ? smem_optin(k_block_offset<double>, p.smem)
+                          : smem_optin(k_block_offset<float>, p.smem);
       return (int)e;
     }
   }
@@ -1459,7 +1457,7 @@ int prepare_part(DevPart& p) {
 template <class V>
 static int xw_occ_t(int pad, int vec, int tpb, size_t smem) {
   auto occ = [&](auto kern) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    if (smem_optin(kern, smem) != cudaSuccess) return 0;
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, tpb, smem) != cudaSuccess) return 0;
     return n;

@@ -533,6 +533,7 @@ void Plan::upload(cudaStream_t s) {
           const std::vector<int64_t>* ts = &T.start;
           const std::vector<int64_t>* tf = &T.first_row;
           if (!T.present) {
+            d.t_synth = 1;
             tstart.resize((size_t)nnz + 1);
             tfirst.resize((size_t)nnz);
             for (int64_t e = 0; e <= nnz; ++e) tstart[(size_t)e] = e;
@@ -634,6 +635,7 @@ void Plan::upload(cudaStream_t s) {
     if (d.tile) fn += "_tile";
     if (d.fam == FAM_BLOCK_OFFSET && d.variant == 1) fn += "_tma";
     launches.push_back(d);
+    launch_part.push_back(pi);
     spans.push_back(part_span(h, host.n));
     launch_bytes.push_back(bytes_model - bytes_before);
   }

@@ -14,6 +14,7 @@ struct Plan {
   HostPlan host;                 // logical metadata (kept for host-only plans / AS_PLAN_KEEP_HOST)
   bool host_kept = false;
   std::vector<DevPart> launches; // in launch order
+  std::vector<int64_t> launch_part;  // part index (DFS order) of every launch
   const int32_t* d_prepass = nullptr;
   int64_t n_prepass = 0;
   std::vector<void*> allocs;
@@ -63,6 +64,10 @@ struct Plan {
   int64_t n_heavy = 0;
   void compute_model();
 };
+
+// "dev.<key>" exports: the device arrays read back and decoded to the logical layout
+// (readback.cpp); keys "dev.p<part>.<name>"
+std::vector<std::pair<std::string, std::vector<uint8_t>>> device_arrays(const Plan& P);
 
 // Enqueue one SpMV of the plan on `stream` (pre-pass, parts, epilogue); with n_peers > 0
 // every part's final STORE of a row in [peer_lo[i], peer_hi[i]) also goes to peer_y[i]

@@ -480,10 +480,13 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
     if (!verify(h, M)) fail(kWrongResult, "wrong_result: y differs from the host reference");
     return h.P.release();
   };
+  double pred_ms = -1;  // cost-model prediction of the candidate being evaluated (model stage)
   auto logline = [&](int i, const std::string& g, const char* status, double t) {
     if (!log) return;
-    std::fprintf(log, "{\"i\": %d, \"graph\": \"%s\", \"status\": \"%s\", \"median_ms\": %.6f}\n", i,
+    std::fprintf(log, "{\"i\": %d, \"graph\": \"%s\", \"status\": \"%s\", \"median_ms\": %.6f", i,
                  json_escape(g).c_str(), status, t);
+    if (pred_ms > 0) std::fprintf(log, ", \"pred_ms\": %.6f", pred_ms);  // surrogate accuracy
+    std::fprintf(log, ", \"elapsed_s\": %.3f}\n", std::chrono::duration<double>(clk::now() - t_start).count());
     std::fflush(log);
   };
 
@@ -610,7 +613,9 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return pred[a] < pred[b]; });
       for (size_t k = 0; k < std::min<size_t>(4, order.size()) && ran < cap; ++k) {
         if (cfg->budget_seconds > 0 && elapsed() > 0.8 * cfg->budget_seconds) break;
+        pred_ms = std::exp(pred[order[k]]);
         evaluate(2000 + ran, pool[order[k]], sampled ? "sample_model" : "model");
+        pred_ms = -1;
         ++ran;
       }
     }
@@ -729,6 +734,27 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       logline(-3, best_canon, "final_wrong_result", best_t);
       delete best_plan;
       best_plan = nullptr;
+      // fall back to the next fastest distinct candidates, re-planned on the full matrix
+      // (run() verifies each before it is accepted)
+      std::vector<Cand> order = ranked;
+      std::sort(order.begin(), order.end(), [](const Cand& a, const Cand& b) { return a.t < b.t; });
+      std::set<std::string> tried_final = {best_canon};
+      for (auto& c : order) {
+        if (best_plan || tried_final.size() > 4) break;
+        if (c.t <= 0 || tried_final.count(c.canon)) continue;
+        tried_final.insert(c.canon);
+        std::string canon;
+        double t_med = -1;
+        try {
+          best_plan = run(A, c.canon, canon, t_med);
+          best_t = t_med;
+          best_canon = canon;
+          logline(-4, canon, "fallback", t_med);
+        } catch (const Error& e) {
+          if (e.st == AS_ERR_CUDA) cudaGetLastError();
+          logline(-4, c.canon, "fallback_rejected", -1);
+        }
+      }
     }
   }
   if (log) std::fclose(log);

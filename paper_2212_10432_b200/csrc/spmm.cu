@@ -18,6 +18,7 @@
 #include <algorithm>
 
 #include "devpart.h"
+#include "optin.h"
 
 namespace as {
 namespace {
@@ -274,8 +275,7 @@ int spmm_part_t(const DevPart& p, const SpmmPart& s, double alpha, double beta, 
     if (p.b > kTB) return (int)cudaErrorInvalidValue;
     // the shared-memory opt-in is a per-device function attribute: set it for the device
     // this launch runs on (idempotent and cheap; no process-wide cache to go stale or race)
-    cudaError_t e = cudaFuncSetAttribute(k_spmm_dense_dmma<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kDenseSmem);
+    cudaError_t e = smem_optin(k_spmm_dense_dmma<V>, kDenseSmem);
     if (e != cudaSuccess) return (int)e;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(p.n_tile_rows, 148 * 8));
     k_spmm_dense_dmma<V><<<g, 256, kDenseSmem, st>>>(p, alpha, beta, X, ldx, Y, ldy, k);

@@ -364,3 +364,50 @@ def test_xcache_parity(graph, dtype, int_mode):
     assert "_xh" in P.info()["kernels"], P.info()["kernels"]
     if int_mode:
         compare_export(P, coo, graph)
+
+
+@pytest.mark.parametrize("graph", FAMILY_GRAPHS + COMPOSE_GRAPHS + XCACHE_GRAPHS)
+def test_device_readback_matches_oracle(graph):
+    """The uploaded device format, read back from device memory ("dev." export keys: implicit
+    arrays and fitted models evaluated, the xcache column encoding undone) equals the oracle's
+    logical Matrix Metadata Set byte for byte -- a check of the arrays the kernels read, not
+    of the host copy they were built from."""
+    coo = synth.random_powerlaw(3000, 2600, 2, 900, int_mode=True)
+    try:
+        P = asp.Plan(_mat(coo), graph, device=0)
+    except asp.AsError as e:
+        assert_infeasible_justified(coo, graph, e)
+        return
+    csr = B.Csr(coo.m, coo.n, coo.row, coo.col, coo.val)
+    parts, w = B.build(csr, G.parse(graph), coo.val.dtype)
+    ref = B.export(parts, w)
+    keys = P.device_keys()
+    assert keys, graph
+    for i, p in enumerate(parts):
+        if p.kind == "csr" and (p.excl_rows.shape[0] or p.atom_rows.shape[0]):
+            have = {k.split(".", 2)[2] for k in keys if k.startswith(f"dev.p{i}.")}
+            assert "col" in have or "pad.col" in have, (graph, i, have)
+    for k in keys:
+        lk = k[len("dev."):]
+        assert lk in ref, (graph, k)
+        got, want = P.export(k), ref[lk]
+        assert got.shape == want.shape and np.array_equal(got.astype(want.dtype), want), (graph, k)
+
+
+def test_smem_optin_not_lowered_by_later_plans():
+    """The dynamic shared-memory opt-in is a per-function attribute shared by all plans: a
+    plan built later with a smaller need must not break an earlier plan's launches (the
+    search builds and keeps plans in any order)."""
+    coo = synth.random_powerlaw(9000, 7000, 4, 2500, int_mode=True).astype(np.float32)
+    big = "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=512,grid=1,xcache=20000); GMEM_ATOM_RED"
+    small = big.replace("xcache=20000", "xcache=2000")
+    P_big = asp.Plan(_mat(coo), big, device=0)
+    P_small = asp.Plan(_mat(coo), small, device=0)
+    run_check(coo, big, 2.0, -0.5, int_mode=True, seed=1, plan=P_big)
+    run_check(coo, small, 2.0, -0.5, int_mode=True, seed=1, plan=P_small)
+    cs_big = "COMPRESS; BMTB_NNZ_BLOCK(6000); SHMEM_OFFSET_RED; SET_RESOURCE(tpb=256,stages=0); GMEM_ATOM_RED"
+    cs_small = cs_big.replace("6000", "64")
+    Q_big = asp.Plan(_mat(coo), cs_big, device=0)
+    Q_small = asp.Plan(_mat(coo), cs_small, device=0)
+    run_check(coo, cs_big, 1.0, 0.0, int_mode=True, seed=2, plan=Q_big)
+    run_check(coo, cs_small, 1.0, 0.0, int_mode=True, seed=2, plan=Q_small)
