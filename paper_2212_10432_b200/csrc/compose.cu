@@ -59,7 +59,7 @@ __device__ __forceinline__ PadPos pad_pos_rt(const DevPart& p, int64_t t) {
     t0 = ldm(p.grp_first_bmt + g);
     t1 = ldm(p.grp_first_bmt + g + 1);
   }
-  return {ldm(p.grp_base + g) + (t - t0) * p.vec, (t1 - t0) * p.vec};
+  return {grp_base_at(p, g) + (t - t0) * p.vec, (t1 - t0) * p.vec};
 }
 
 // One BMT's serial pass: summary of its boundary segments; rows closing strictly inside
@@ -168,7 +168,7 @@ template <class V, bool PAD>
 __device__ __forceinline__ PadPos c_pad(const DevPart& p, int64_t t, int64_t w, int64_t tb0, int64_t tb1) {
   PadPos pp{0, 0};
   if constexpr (PAD) {
-    if (p.pad_grp_bmw) pp = PadPos{ldm(p.grp_base + w) + (t - tb0) * p.vec, (tb1 - tb0) * p.vec};
+    if (p.pad_grp_bmw) pp = PadPos{grp_base_at(p, w) + (t - tb0) * p.vec, (tb1 - tb0) * p.vec};
     else if (p.n_grp == 1) pp = PadPos{t * p.vec, p.n_bmt * p.vec};
     else pp = pad_pos_rt(p, t);
   }
@@ -193,8 +193,8 @@ __device__ __forceinline__ void thread_bmt(const DevPart& p, const V* __restrict
 template <class V, bool PAD, int WR, int BR>
 __device__ __forceinline__ void warp_bmw(const DevPart& p, const V* __restrict__ x, Sink<V, BR>& sk, int64_t w,
                                          int lane) {
-  const int64_t tb0 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w) : w * p.bmts_per_bmw;
-  const int64_t tb1 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w + 1) : min(tb0 + p.bmts_per_bmw, p.n_bmt);
+  const int64_t tb0 = bmw_bmt_at(p, w);
+  const int64_t tb1 = bmw_bmt_at(p, w + 1);
   if (tb1 <= tb0) return;
   const int64_t wa = c_bmt_start(p, tb0), we = c_bmt_start(p, tb1);
   if constexpr (WR == RED_NONE) {

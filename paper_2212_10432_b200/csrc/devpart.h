@@ -3,6 +3,7 @@
 // is linear by construction and is computed instead of loaded (reading A17, the paper's
 // Model-Driven Format Compression example "row_offset = 64*bid").
 #pragma once
+#include <cstddef>
 #include <cstdint>
 
 namespace as {
@@ -55,16 +56,22 @@ struct DevPart {
   int64_t k = 0;                          // BMT_NNZ size
   int64_t s = 0;                          // BMT_ROW size
   const int32_t* bmt_start = nullptr;     // NNZ BMTs: NULL -> t*k
-  const int32_t* bmt_row_ptr = nullptr;   // ROW BMTs: NULL -> min(t*s, m_p)
+  const int32_t* bmt_row_ptr = nullptr;   // ROW BMTs: NULL -> brp_model(t) if fitted, else min(t*s, m_p)
+  IdxModel brp_model;
   const int32_t* bmt_first_row = nullptr;  // NULL -> fr_model(t) (NNZ BMTs, model-driven compression)
   IdxModel fr_model;
   const uint32_t* bitmap = nullptr;
   int bm_words = 0;
+  // short-array fusion ("combining multiple short-data-type arrays"): first_row and
+  // the bitmap words of a BMT interleaved in one array of fr_stride = bm_stride int32 words
+  // per BMT ({first_row, bm0, bm1, ...}), so one sector serves all of a BMT's metadata
+  int bm_stride = 0, fr_stride = 1;
   const uint32_t* bits = nullptr;         // tile form: packed head bits, 1 per nonzero
   int tile = 0;                           // NNZ_WARP tile kernel (k in {1,2,4})
   // BMW level
   int64_t n_bmw = 0;
-  const int32_t* bmw_bmt_ptr = nullptr;   // NNZ_WARP: BMT range per BMW; NULL -> bmts_per_bmw
+  const int32_t* bmw_bmt_ptr = nullptr;   // NNZ_WARP: BMT range per BMW; NULL -> bwp_model(w) if fitted, else w*bmts_per_bmw
+  IdxModel bwp_model;
   int64_t bmts_per_bmw = 0;
   const int32_t* bmw_start = nullptr;     // WARP_ROW: nz start per BMW
   const int32_t* bmw_first_row = nullptr; // WARP_ROW: NULL -> w
@@ -96,8 +103,9 @@ struct DevPart {
   int64_t n_grp = 0, grp_regular = 0;     // BMTs per group if regular, else 0
   int pad_grp_bmw = 0;                    // pad groups are exactly the BMWs (scope=BMW)
   const int32_t* grp_first_bmt = nullptr; // n_grp + 1
-  const int64_t* grp_base = nullptr;      // n_grp slot offsets
-  const int32_t* grp_width = nullptr;     // n_grp
+  const int64_t* grp_base = nullptr;      // n_grp slot offsets; NULL -> pb_model(g)
+  const int32_t* grp_width = nullptr;     // n_grp; NULL -> pw_model(g) (Model-Driven Format Compression)
+  IdxModel pb_model, pw_model;
   const int32_t* pad_col = nullptr;
   const void* pad_val = nullptr;
   // DIA

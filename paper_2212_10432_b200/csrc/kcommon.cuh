@@ -98,7 +98,24 @@ __device__ __forceinline__ int64_t out_row(const DevPart& p, int64_t r) {
 }
 // first (compacted) row of NNZ BMT t: stored array, or its fitted model
 __device__ __forceinline__ int64_t bmt_row0(const DevPart& p, int64_t t) {
-  return p.bmt_first_row ? (int64_t)ldm(p.bmt_first_row + t) : idx_eval(p.fr_model, t);
+  return p.bmt_first_row ? (int64_t)ldm(p.bmt_first_row + t * p.fr_stride) : idx_eval(p.fr_model, t);
+}
+// bitmap words of BMT t (stride: bm_words, or the fused metadata stride)
+__device__ __forceinline__ const uint32_t* bmt_bits(const DevPart& p, int64_t t) { return p.bitmap + t * p.bm_stride; }
+// per-block arrays that Model-Driven Format Compression may have replaced by a fitted model
+__device__ __forceinline__ int64_t grp_base_at(const DevPart& p, int64_t g) {
+  return p.grp_base ? ldm(p.grp_base + g) : idx_eval(p.pb_model, g);
+}
+__device__ __forceinline__ int64_t grp_width_at(const DevPart& p, int64_t g) {
+  return p.grp_width ? (int64_t)ldm(p.grp_width + g) : idx_eval(p.pw_model, g);
+}
+__device__ __forceinline__ int64_t bmw_bmt_at(const DevPart& p, int64_t w) {
+  if (p.bmw_bmt_ptr) return ldm(p.bmw_bmt_ptr + w);
+  return p.bwp_model.kind ? idx_eval(p.bwp_model, w) : min(w * p.bmts_per_bmw, p.n_bmt);
+}
+__device__ __forceinline__ int64_t bmt_rowp_at(const DevPart& p, int64_t t) {
+  if (p.bmt_row_ptr) return ldm(p.bmt_row_ptr + t);
+  return p.brp_model.kind ? idx_eval(p.brp_model, t) : min(t * p.s, p.m_p);
 }
 // fp32 plans: scratch slot of a heavy row (A25), or -1.  A 1-bit-per-row filter (L1/L2
 // resident) answers the common case; only heavy rows pay the binary search.
@@ -285,7 +302,7 @@ __device__ __forceinline__ PadPos pad_pos(const DevPart& p, int64_t t) {
     t0 = ldm(p.grp_first_bmt + g);
     t1 = ldm(p.grp_first_bmt + g + 1);
   }
-  return {ldm(p.grp_base + g) + (t - t0) * VEC, (t1 - t0) * VEC};
+  return {grp_base_at(p, g) + (t - t0) * VEC, (t1 - t0) * VEC};
 }
 
 // Warp-level combine of per-lane partials (one round of 32 consecutive BMTs).

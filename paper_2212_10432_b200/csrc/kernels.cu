@@ -34,8 +34,8 @@ template <class V>
 __global__ void __launch_bounds__(1024) k_thread_row(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const V* val = (const V*)p.val;
   for (int64_t t = thread_units(p.n_bmt).begin, t_e = thread_units(p.n_bmt).end; t < t_e; t += blockDim.x) {
-    int64_t r0 = p.bmt_row_ptr ? ldm(p.bmt_row_ptr + t) : t * p.s;
-    int64_t r1 = p.bmt_row_ptr ? ldm(p.bmt_row_ptr + t + 1) : min((t + 1) * p.s, p.m_p);
+    int64_t r0 = bmt_rowp_at(p, t);
+    int64_t r1 = bmt_rowp_at(p, t + 1);
     for (int64_t r = r0; r < r1; ++r) {
       int64_t a = ldm(p.row_ptr + r), e = ldm(p.row_ptr + r + 1);
       double acc0 = 0.0, acc1 = 0.0;
@@ -74,11 +74,11 @@ __global__ void __launch_bounds__(1024) k_thread_row_pad(DevPart p, const V* __r
       t1 = ldm(p.grp_first_bmt + g + 1);
     }
     const int64_t nt = t1 - t0, lt = t - t0;
-    const int64_t W = ldm(p.grp_width + g);
-    const int64_t base = ldm(p.grp_base + g) + lt * VEC;
+    const int64_t W = grp_width_at(p, g);
+    const int64_t base = grp_base_at(p, g) + lt * VEC;
     const int64_t stride = nt * VEC;
-    int64_t r0 = p.bmt_row_ptr ? ldm(p.bmt_row_ptr + t) : t * p.s;
-    int64_t r1 = p.bmt_row_ptr ? ldm(p.bmt_row_ptr + t + 1) : min((t + 1) * p.s, p.m_p);
+    int64_t r0 = bmt_rowp_at(p, t);
+    int64_t r1 = bmt_rowp_at(p, t + 1);
     if (r1 - r0 == 1) {
       // whole BMT is one row: read all W slots (pads have value 0, valid col)
       double acc[VEC];
@@ -143,9 +143,25 @@ struct XHot {
   const V* sm;
   __device__ __forceinline__ double operator()(int64_t c) const { return c < 0 ? (double)sm[~c] : ldx(x, c); }
 };
+// All CTAs fill at kernel start, so the fill's latency is exposed once per CTA: 8 column
+// indices, then 8 gathers, are in flight per thread (a one-load-at-a-time loop cost ~25 us
+// of start-up for 24K entries)
 template <class V>
 __device__ __forceinline__ void xhot_fill(const DevPart& p, const V* __restrict__ x, V* sm) {
-  for (int64_t i = threadIdx.x; i < p.xh_n; i += blockDim.x) sm[i] = __ldg(x + ldm(p.xh_cols + i));
+  constexpr int U = 8;
+  const int64_t n = p.xh_n, T = blockDim.x;
+  int64_t i = threadIdx.x;
+  for (; i + (U - 1) * T < n; i += U * T) {
+    int32_t c[U];
+    V v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = ldm(p.xh_cols + i + u * T);
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldg(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) sm[i + u * T] = v[u];
+  }
+  for (; i < n; i += T) sm[i] = __ldg(x + ldm(p.xh_cols + i));
   __syncthreads();
 }
 
@@ -239,12 +255,12 @@ __device__ __forceinline__ void nnz_thread_bmt(const DevPart& p, XA xa, V* __res
   bool inside;
   PadPos pp{0, 0};
   if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
-  bmt_pass<V, PAD, VEC, KB>(p, xa, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, acc, inside,
+  bmt_pass<V, PAD, VEC, KB>(p, xa, bmt_bits(p, t), pp, a, (int)(e - a), row, acc, inside,
                             [&](int64_t r, double s, bool in) {
                               if (in) write_excl(p, y, r, s);
                               else write_atom(p, y, r, s);
                             });
-  bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
+  bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(bmt_bits(p, t + 1)) & 1u);
   if (inside && ends) write_excl(p, y, row, acc);
   else write_atom(p, y, row, acc);
 }
@@ -353,7 +369,7 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   const int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
   const int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
   const int len = (int)(e - a);
-  const uint32_t* bm = p.bitmap + t * p.bm_words;
+  const uint32_t* bm = bmt_bits(p, t);
   const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;  // batch base
   const int32_t* pc = PAD ? p.pad_col + pp.base : p.col + a;
   ScanPE o;
@@ -388,7 +404,7 @@ __device__ __forceinline__ void nnz_thread_bmt_pe(const DevPart& p, XA xa, V* __
   // first segment closed inside the BMT but begun before it: straddler
   if (!o.s0 && o.inside) write_atom(p, y, bmt_row0(p, t), o.first);
   // open last segment: exclusive iff it began at a head here and the next BMT starts a row
-  const bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(p.bitmap + (t + 1) * p.bm_words) & 1u);
+  const bool ends = (t + 1 >= p.n_bmt) ? true : (ldm(bmt_bits(p, t + 1)) & 1u);
   if (o.inside && ends) write_excl(p, y, o.row, o.acc);
   else write_atom(p, y, o.row, o.acc);
 }
@@ -584,8 +600,8 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = gthreads() >> 5;
   for (int64_t w = warp_units(p.n_bmw).begin, w_e = warp_units(p.n_bmw).end; w < w_e; w += blockDim.x >> 5) {
-    int64_t tb0 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w) : w * p.bmts_per_bmw;
-    int64_t tb1 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w + 1) : min(tb0 + p.bmts_per_bmw, p.n_bmt);
+    int64_t tb0 = bmw_bmt_at(p, w);
+    int64_t tb1 = bmw_bmt_at(p, w + 1);
     double carry = 0.0;
     bool carry_inside = false;  // open segment's row started at a head inside this BMW
     bool carry_live = false;    // an open segment exists (false only before the first element)
@@ -608,11 +624,11 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
         bool first_open = true;
         PadPos pp{0, 0};
         if constexpr (PAD) {
-          if (p.pad_grp_bmw) pp = PadPos{ldm(p.grp_base + w) + (t - tb0) * VEC, (tb1 - tb0) * VEC};
+          if (p.pad_grp_bmw) pp = PadPos{grp_base_at(p, w) + (t - tb0) * VEC, (tb1 - tb0) * VEC};
           else if (p.n_grp == 1) pp = PadPos{t * VEC, p.n_bmt * VEC};
           else pp = pad_pos<VEC>(p, t);
         }
-        bmt_pass<V, PAD, VEC, 8>(p, XGlobal<V>{x}, p.bitmap + t * p.bm_words, pp, a, (int)(e - a), row, cur, in,
+        bmt_pass<V, PAD, VEC, 8>(p, XGlobal<V>{x}, bmt_bits(p, t), pp, a, (int)(e - a), row, cur, in,
                               [&](int64_t r, double s, bool inside) {
           if (!inside && first_open) {  // continuation of a row begun in an earlier lane
             cin = s;
@@ -622,7 +638,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
           }
           first_open = false;
         });
-        b0 = ldm(p.bitmap + t * p.bm_words) & 1u;
+        b0 = ldm(bmt_bits(p, t)) & 1u;
         hh = in;
         if (hh) cout = cur;
         else cin = cur;
@@ -647,7 +663,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
     }
     if (lane == 0 && carry_live) {
       // final open segment: the row of the BMW's last element
-      bool ends = (tb1 >= p.n_bmt) ? true : (ldm(p.bitmap + tb1 * p.bm_words) & 1u);
+      bool ends = (tb1 >= p.n_bmt) ? true : (ldm(bmt_bits(p, tb1)) & 1u);
       if (carry_inside && ends) write_excl(p, y, carry_row, carry);
       else write_atom(p, y, carry_row, carry);
     }
@@ -667,8 +683,8 @@ __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __rest
   if constexpr (XH) xa = XHot<V>{x, (const V*)xh_smem};
   else xa = XGlobal<V>{x};
   for (int64_t w = warp_units(p.n_bmw).begin, w_e = warp_units(p.n_bmw).end; w < w_e; w += blockDim.x >> 5) {
-    const int64_t tb0 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w) : w * p.bmts_per_bmw;
-    const int64_t tb1 = p.bmw_bmt_ptr ? ldm(p.bmw_bmt_ptr + w + 1) : min(tb0 + p.bmts_per_bmw, p.n_bmt);
+    const int64_t tb0 = bmw_bmt_at(p, w);
+    const int64_t tb1 = bmw_bmt_at(p, w + 1);
     double carry = 0.0;
     bool carry_inside = false;  // open segment's row started at a head inside this BMW
     bool carry_live = false;    // an open segment exists (false only before the first element)
@@ -684,7 +700,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __rest
       if (active) {
         PadPos pp{0, 0};
         if constexpr (PAD) {
-          if (p.pad_grp_bmw) pp = PadPos{ldm(p.grp_base + w) + (t - tb0) * VEC, (tb1 - tb0) * VEC};
+          if (p.pad_grp_bmw) pp = PadPos{grp_base_at(p, w) + (t - tb0) * VEC, (tb1 - tb0) * VEC};
           else if (p.n_grp == 1) pp = PadPos{t * VEC, p.n_bmt * VEC};
           else pp = pad_pos<VEC>(p, t);
         }
@@ -720,7 +736,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __rest
     }
     if (lane == 0 && carry_live) {
       // final open segment: the row of the BMW's last element
-      const bool ends = (tb1 >= p.n_bmt) ? true : (ldm(p.bitmap + tb1 * p.bm_words) & 1u);
+      const bool ends = (tb1 >= p.n_bmt) ? true : (ldm(bmt_bits(p, tb1)) & 1u);
       if (carry_inside && ends) write_excl(p, y, carry_row, carry);
       else write_atom(p, y, carry_row, carry);
     }

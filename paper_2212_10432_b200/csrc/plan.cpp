@@ -97,8 +97,23 @@ void Plan::upload_pad(const HostPart& h, DevPart& d, cudaStream_t s, const std::
     if (h.grp_first_bmt[g] != g * per) reg = false;
   d.grp_regular = reg ? per : 0;
   d.grp_first_bmt = up_i32(h.grp_first_bmt, s, "grp_first_bmt");
-  d.grp_base = (const int64_t*)up(h.grp_base.data(), h.grp_base.size() * 8, s);
-  d.grp_width = up_i32(h.pad_width, s, "pad_width");
+  // Model-Driven Format Compression (NEXT-2) of the per-group slot base and pad_width (the
+  // paper's bmt_sizes_of_bmtb): regular groups give linear / step models
+  const bool mdc = !std::getenv("AS_NO_MDC");
+  int64_t saved = 0;
+  if (mdc && fit_array_model(h.grp_base, kMaxPatches, &d.pb_model)) {
+    ++modeled_arrays;
+    saved += (int64_t)h.grp_base.size() * 8;
+  } else {
+    d.grp_base = (const int64_t*)up(h.grp_base.data(), h.grp_base.size() * 8, s);
+  }
+  if (mdc && fit_array_model(h.pad_width, kMaxPatches, &d.pw_model)) {
+    ++modeled_arrays;
+    saved += (int64_t)h.pad_width.size() * 4;
+  } else {
+    d.grp_width = up_i32(h.pad_width, s, "pad_width");
+  }
+  bytes_model -= (double)saved;
   const std::vector<int32_t>& pc = (pad_col && !pad_col->empty()) ? *pad_col : h.pad_col;
   d.pad_col = (const int32_t*)up(pc.data(), pc.size() * 4, s);
   cudaStreamSynchronize(s);
@@ -325,6 +340,7 @@ static Plan::Span part_span(const HostPart& h, int64_t n) {
 void Plan::upload(cudaStream_t s) {
   const int64_t sv = dt == AS_R64F ? 8 : 4;
   const bool mdc = !std::getenv("AS_NO_MDC");  // Model-Driven Format Compression (A/B knob)
+  const bool fuse = !std::getenv("AS_NO_FUSE");  // short-array fusion (A/B knob)
   int max_smem = device_max_smem_optin(device);
   for (int64_t pi : host.launch_order) {
     const HostPart& h = host.parts[pi];
@@ -388,8 +404,12 @@ void Plan::upload(cudaStream_t s) {
           if (!is_affine(T.first_row, T.size, 0)) {
             std::vector<int64_t> brp = T.first_row;
             brp.push_back(mp);
-            d.bmt_row_ptr = up_i32(brp, s, "bmt_row_ptr");
-            bytes_model += (double)(brp.size() * 4);
+            if (mdc && fit_array_model(brp, kMaxPatches, &d.brp_model)) {
+              ++modeled_arrays;  // ROW-block row offsets as a model (NEXT-2)
+            } else {
+              d.bmt_row_ptr = up_i32(brp, s, "bmt_row_ptr");
+              bytes_model += (double)(brp.size() * 4);
+            }
           }
           if (h.pad) {
             upload_pad(h, d, s);
@@ -428,15 +448,36 @@ void Plan::upload(cudaStream_t s) {
             d.bmt_start = up_i32(T.start, s, "bmt_start");
             bytes_model += (double)(T.start.size() * 4);
           }
+          d.bm_words = h.bm_words;
+          d.bm_stride = h.bm_words;
           if (mdc && fit_array_model(T.first_row, kMaxPatches, &d.fr_model)) {
             ++modeled_arrays;  // Model-Driven Format Compression (NEXT-2): computed, not loaded
+            d.bitmap = (const uint32_t*)up(h.bitmap.data(), h.bitmap.size() * 4, s);
+            bytes_model += (double)(h.bitmap.size() * 4);
+          } else if (fuse && h.bm_words >= 1 && h.bm_words <= 3) {
+            // short-array fusion: {first_row, bm0[, bm1[, bm2]]} per BMT, padded to a
+            // power-of-two stride of int32 words
+            const int S = h.bm_words + 1 <= 2 ? 2 : 4;
+            const int64_t nb = T.count();
+            std::vector<int32_t> fused((size_t)(nb * S), 0);
+            for (int64_t t = 0; t < nb; ++t) {
+              if (T.first_row[t] > INT32_MAX) fail(AS_ERR_PLAN_INFEASIBLE, "bmt_first_row exceeds int32 (reading A36)");
+              fused[(size_t)(t * S)] = (int32_t)T.first_row[t];
+              for (int w = 0; w < h.bm_words; ++w) fused[(size_t)(t * S + 1 + w)] = (int32_t)h.bitmap[(size_t)(t * h.bm_words + w)];
+            }
+            const int32_t* f = (const int32_t*)up(fused.data(), fused.size() * 4, s);
+            cudaStreamSynchronize(s);
+            d.bmt_first_row = f;
+            d.bitmap = (const uint32_t*)(f + 1);
+            d.fr_stride = d.bm_stride = S;
+            ++fused_arrays;
+            bytes_model += (double)(fused.size() * 4);
           } else {
             d.bmt_first_row = up_i32(T.first_row, s, "bmt_first_row");
             bytes_model += (double)(T.first_row.size() * 4);
+            d.bitmap = (const uint32_t*)up(h.bitmap.data(), h.bitmap.size() * 4, s);
+            bytes_model += (double)(h.bitmap.size() * 4);
           }
-          d.bm_words = h.bm_words;
-          d.bitmap = (const uint32_t*)up(h.bitmap.data(), h.bitmap.size() * 4, s);
-          bytes_model += (double)(h.bitmap.size() * 4);
           if (h.xcache > 0) encode_xcache(h, d, s, col_enc, pad_enc);
           if (h.pad) {  // CSR5-like slot-major tiles (BMT_PAD over NNZ BMTs)
             upload_pad(h, d, s, &pad_enc);
@@ -458,6 +499,8 @@ void Plan::upload(cudaStream_t s) {
             int64_t per = W.count() ? ptr[1] - ptr[0] : 0;
             if (per > 0 && is_affine(ptr, per, 0, T.count())) {
               d.bmts_per_bmw = per;
+            } else if (mdc && fit_array_model(ptr, kMaxPatches, &d.bwp_model)) {
+              ++modeled_arrays;  // BMT range per BMW as a model (NEXT-2)
             } else {
               d.bmw_bmt_ptr = up_i32(ptr, s, "bmw_bmt_ptr");
               bytes_model += (double)(ptr.size() * 4);
@@ -575,6 +618,8 @@ void Plan::upload(cudaStream_t s) {
             const int64_t per = W.count() ? ptr[1] - ptr[0] : 0;
             if (per > 0 && is_affine(ptr, per, 0, nt)) {
               d.bmts_per_bmw = per;
+            } else if (mdc && fit_array_model(ptr, kMaxPatches, &d.bwp_model)) {
+              ++modeled_arrays;
             } else {
               d.bmw_bmt_ptr = up_i32(ptr, s, "bmw_bmt_ptr");
               bytes_model += (double)(ptr.size() * 4);

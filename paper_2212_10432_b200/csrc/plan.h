@@ -35,6 +35,7 @@ struct Plan {
   // no atomic rows, no fp32 heavy-row epilogue): as_spmv_dist may fuse peer stores
   bool single_writer = false;
   int modeled_arrays = 0;  // index arrays replaced by fitted models (NEXT-2)
+  int fused_arrays = 0;    // per-BMT metadata arrays fused into one (short-array fusion, NEXT-2)
   bool spmm = false;              // AS_PLAN_SPMM: SpMM arrays of the CSR-family parts uploaded
   bool graph_mode = false;        // AS_PLAN_GRAPH: as_spmv replays a captured CUDA graph
   cudaGraphExec_t gexec = nullptr;

@@ -85,22 +85,35 @@ void part_arrays(const Plan& P, const DevPart& d, int64_t part, std::vector<std:
       for (int64_t t = 0; t <= d.n_bmt; ++t) st.push_back(std::min(t * d.k, d.nnz_p));
     put_i("bmt.nz_ptr", st);
     std::vector<int64_t> fr((size_t)d.n_bmt);
-    if (d.bmt_first_row) fr = widen(d2h<int32_t>(d.bmt_first_row, d.n_bmt));
-    else
+    if (d.bmt_first_row) {  // plain, or fused with the bitmap words (stride fr_stride)
+      std::vector<int32_t> raw = d2h<int32_t>(d.bmt_first_row, d.n_bmt * d.fr_stride);
+      for (int64_t t = 0; t < d.n_bmt; ++t) fr[(size_t)t] = raw[(size_t)(t * d.fr_stride)];
+    } else {
       for (int64_t t = 0; t < d.n_bmt; ++t) fr[(size_t)t] = model_at(d.fr_model, t);
+    }
     put_i("bmt.first_row", fr);
   }
-  if (d.bitmap && d.bm_words) put_raw("bmt.bitmap", bytes(d2h<uint32_t>(d.bitmap, d.n_bmt * d.bm_words)));
+  if (d.bitmap && d.bm_words) {
+    std::vector<uint32_t> raw = d2h<uint32_t>(d.bitmap, d.n_bmt * d.bm_stride), bm((size_t)(d.n_bmt * d.bm_words));
+    for (int64_t t = 0; t < d.n_bmt; ++t)
+      for (int w = 0; w < d.bm_words; ++w) bm[(size_t)(t * d.bm_words + w)] = raw[(size_t)(t * d.bm_stride + w)];
+    put_raw("bmt.bitmap", bytes(bm));
+  }
   if (d.fam == FAM_THREAD_ROW) {
     std::vector<int64_t> fr((size_t)d.n_bmt);
     if (d.bmt_row_ptr) fr = widen(d2h<int32_t>(d.bmt_row_ptr, d.n_bmt));
     else
-      for (int64_t t = 0; t < d.n_bmt; ++t) fr[(size_t)t] = t * d.s;
+      for (int64_t t = 0; t < d.n_bmt; ++t) fr[(size_t)t] = d.brp_model.kind ? model_at(d.brp_model, t) : t * d.s;
     put_i("bmt.first_row", fr);
   }
   if (d.pad) {
-    std::vector<int64_t> w = widen(d2h<int32_t>(d.grp_width, d.n_grp));
-    std::vector<int64_t> base = d2h<int64_t>(d.grp_base, d.n_grp);
+    std::vector<int64_t> w((size_t)d.n_grp), base((size_t)d.n_grp);
+    if (d.grp_width) w = widen(d2h<int32_t>(d.grp_width, d.n_grp));
+    else
+      for (int64_t g = 0; g < d.n_grp; ++g) w[(size_t)g] = model_at(d.pw_model, g);
+    if (d.grp_base) base = d2h<int64_t>(d.grp_base, d.n_grp);
+    else
+      for (int64_t g = 0; g < d.n_grp; ++g) base[(size_t)g] = model_at(d.pb_model, g);
     std::vector<int64_t> gf = widen(d2h<int32_t>(d.grp_first_bmt, d.n_grp + 1));
     const int64_t total = d.n_grp ? base.back() + (gf[(size_t)d.n_grp] - gf[(size_t)d.n_grp - 1]) * w.back() : 0;
     base.push_back(total);
