@@ -303,6 +303,7 @@ void as_graph_destroy(as_graph_t G) { delete G; }
 
 as_status_t as_plan_ex(as_matrix_t M, as_graph_t G, int device, void* stream, int flags, as_plan_t* out) {
   return guard([&] {
+    NvtxRange nv("as_plan");
     if (!M || !G || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
     Plan* P = make_plan(M->A, G->g, G->canon, device, stream, flags);
     auto* h = new as_plan_s();
@@ -376,6 +377,7 @@ void as_plan_destroy(as_plan_t P) { delete P; }
 
 as_status_t as_spmv(as_plan_t h, const void* alpha, const void* x, const void* beta, void* y, void* stream) {
   return guard([&] {
+    NvtxRange nv("as_spmv");
     if (!h || !alpha || !beta) fail(AS_ERR_INVALID_ARG, "NULL argument");
     Plan& P = *h->P;
     if (P.device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan cannot run as_spmv");
@@ -429,6 +431,7 @@ as_status_t as_spmv(as_plan_t h, const void* alpha, const void* x, const void* b
 as_status_t as_spmv_host(as_plan_t h, const void* alpha, const void* x_host, const void* beta, void* y_host,
                          void* stream) {
   return guard([&] {
+    NvtxRange nv("as_spmv_host");
     if (!h || !alpha || !beta) fail(AS_ERR_INVALID_ARG, "NULL argument");
     Plan& P = *h->P;
     if (P.device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan");
@@ -597,6 +600,7 @@ as_status_t as_plan_profile(as_plan_t h, const void* x, void* y, int reps, void*
 as_status_t as_spmm(as_plan_t h, int64_t k, const void* alpha, const void* X, int64_t ldx, const void* beta, void* Y,
                     int64_t ldy, void* stream) {
   return guard([&] {
+    NvtxRange nv("as_spmm");
     if (!h || !alpha || !beta) fail(AS_ERR_INVALID_ARG, "NULL argument");
     Plan& P = *h->P;
     if (P.device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan cannot run as_spmm");
@@ -637,6 +641,7 @@ as_status_t as_search(as_matrix_t M, const as_search_cfg_t* cfg, int device, voi
                       char* best_graph, size_t* len) {
   as_status_t st = AS_OK;
   as_status_t g = guard([&] {
+    NvtxRange nv("as_search");
     if (!M || !cfg || !best) fail(AS_ERR_INVALID_ARG, "NULL argument");
     st = search_impl(M->A, cfg, device, stream, best, best_graph, len);
   });

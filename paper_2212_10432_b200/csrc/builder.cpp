@@ -58,6 +58,7 @@ void trace(const char* phase) {
   static auto last = std::chrono::steady_clock::now();
   auto now = std::chrono::steady_clock::now();
   if (on) std::fprintf(stderr, "[as_plan] %-24s %8.3f s\n", phase, std::chrono::duration<double>(now - last).count());
+  nvtxMarkA(phase);  // builder phase boundary on the NVTX timeline
   last = now;
 }
 

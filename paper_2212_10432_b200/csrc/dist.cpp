@@ -243,6 +243,7 @@ as_status_t as_dist_open_peers(as_dist_t D, void* y_full, const void* handles) {
 as_status_t as_spmv_dist(as_dist_t D, as_plan_t local, const void* alpha, const void* x_full, const void* beta,
                          void* y_full, int exchange, void* stream) {
   return guard([&] {
+    NvtxRange nv("as_spmv_dist");
     if (!D || !local || !y_full) fail(AS_ERR_INVALID_ARG, "NULL argument");
     if (D->cuts.empty()) fail(AS_ERR_INVALID_ARG, "as_dist_set_cuts first");
     Plan& P = *local->P;

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/as.h"
 #include "devpart.h"
@@ -158,6 +159,15 @@ std::vector<std::string> export_keys(const HostPlan& hp);
 std::string random_graph(const Matrix& A, uint64_t seed);
 
 // ------------------------------------------------------------------ small utilities
+// NVTX range over a scope (SURVEY §5 tracing): header-only NVTX3, a no-op unless a tool
+// (nsys / ncu --nvtx) injects itself.  Names: "as_plan", "as_spmv", "as_search", ...
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 template <class F>
 void parallel_for(int64_t n, F f, int64_t grain = 1 << 16);
 

@@ -1,0 +1,6 @@
+// NNZ_WARP launch group of the SpMV kernel family, value type double (see klaunch.h).
+#include "kernels_impl.cuh"
+
+namespace as {
+AS_KERNELS_INSTANTIATE_NNZ_WARP(double)
+}  // namespace as

@@ -13,6 +13,8 @@
 //   k_gather_hash : x[hash(i) % n], no col stream         -> random-sector L2 rate alone
 //   k_gather_hot  : as k_gather, columns < 0 read a shared-memory copy of the hot x entries
 //                   (~col), the rest x[col]               -> the hot-x cache's ceiling
+//   mode 3        : columns relabeled by descending reference count (x permuted to match),
+//                   col < K read the shared-memory prefix -> what a column relabeling buys
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -93,13 +95,13 @@ struct Vec<double> {
 
 constexpr int UNR = 4;
 
-template <class V, int MODE>  // MODE 0 stream, 1 gather, 2 gather with hot smem
+template <class V, int MODE>  // MODE 0 stream, 1 gather, 2 gather with hot smem (~slot), 3 hot = col < nh (relabeled)
 __global__ void __launch_bounds__(1024) k_gather(const V* __restrict__ val, const int32_t* __restrict__ col,
                                                  const V* __restrict__ x, const V* __restrict__ xh, int nh,
                                                  int64_t nnz, double* out) {
   extern __shared__ __align__(16) unsigned char smem[];
   V* sh = (V*)smem;
-  if (MODE == 2) {
+  if (MODE >= 2) {
     for (int i = threadIdx.x; i < nh; i += blockDim.x) sh[i] = xh[i];
     __syncthreads();
   }
@@ -118,7 +120,8 @@ __global__ void __launch_bounds__(1024) k_gather(const V* __restrict__ val, cons
     for (int q = 0; q < UNR * W; ++q) {
       if (MODE == 0) xv[q] = (double)c[q];
       else if (MODE == 1) xv[q] = ldx(x, c[q]);
-      else xv[q] = c[q] < 0 ? (double)sh[~c[q]] : ldx(x, c[q]);
+      else if (MODE == 2) xv[q] = c[q] < 0 ? (double)sh[~c[q]] : ldx(x, c[q]);
+      else xv[q] = c[q] < nh ? (double)sh[c[q]] : ldx(x, c[q]);
     }
 #pragma unroll
     for (int q = 0; q < UNR * W; ++q) acc += v[q] * xv[q];
@@ -129,7 +132,10 @@ __global__ void __launch_bounds__(1024) k_gather(const V* __restrict__ val, cons
     Vec<V>::ld(val + i * W, col + i * W, v, c);
 #pragma unroll
     for (int q = 0; q < W; ++q) {
-      double xv = MODE == 0 ? (double)c[q] : MODE == 1 ? ldx(x, c[q]) : (c[q] < 0 ? (double)sh[~c[q]] : ldx(x, c[q]));
+      double xv = MODE == 0   ? (double)c[q]
+                  : MODE == 1 ? ldx(x, c[q])
+                  : MODE == 2 ? (c[q] < 0 ? (double)sh[~c[q]] : ldx(x, c[q]))
+                              : (c[q] < nh ? (double)sh[c[q]] : ldx(x, c[q]));
       acc += v[q] * xv;
     }
   }
@@ -164,7 +170,7 @@ extern "C" {
 int gr_launch(int dtype, int mode, const void* val, const int32_t* col, const void* x, const void* xh, int nh,
               int64_t nnz, double* out, int grid, int tpb, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  size_t sm = mode == 2 ? (size_t)nh * (dtype ? 8 : 4) : 0;
+  size_t sm = mode >= 2 ? (size_t)nh * (dtype ? 8 : 4) : 0;
 #define L(V, M)                                                                                           \
   do {                                                                                                    \
     if (sm > 48 * 1024) cudaFuncSetAttribute(k_gather<V, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -174,11 +180,13 @@ int gr_launch(int dtype, int mode, const void* val, const int32_t* col, const vo
   if (dtype == 0) {
     if (mode == 0) L(float, 0);
     else if (mode == 1) L(float, 1);
-    else L(float, 2);
+    else if (mode == 2) L(float, 2);
+    else L(float, 3);
   } else {
     if (mode == 0) L(double, 0);
     else if (mode == 1) L(double, 1);
-    else L(double, 2);
+    else if (mode == 2) L(double, 2);
+    else L(double, 3);
   }
 #undef L
   return (int)cudaGetLastError();

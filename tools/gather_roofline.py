@@ -80,6 +80,8 @@ def main():
     ap.add_argument("--configs", nargs="+", default=["c3", "c4"])
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--hot", nargs="+", type=int, default=[8192, 16384, 32768, 49152])
+    ap.add_argument("--relabel", action="store_true",
+                    help="also time the gathers with columns relabeled by descending reference count")
     args = ap.parse_args()
     import torch
     lib = build()
@@ -130,6 +132,30 @@ def main():
                               "min_us": mn * 1e3, "model_gbs": model / (med * 1e-3) / 1e9,
                               "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
             del denc
+        if args.relabel:
+            # column relabeling: rank[c] = position of c in the descending-count order; x permuted to match
+            rank = np.empty(n, np.int64)
+            rank[order] = np.arange(n)
+            rcol = torch.from_numpy(rank[col].astype(np.int32)).to(dev)
+            xr = x[torch.from_numpy(order).to(dev)].contiguous()
+            xsave = x
+
+            def runr(mode, nh, grid, tpb):
+                rc = lib.gr_launch(dt, mode, dval.data_ptr(), rcol.data_ptr(), xr.data_ptr(), xr.data_ptr(), nh, nnz,
+                                   out.data_ptr(), grid, tpb, s)
+                assert rc == 0, rc
+            for (mode, K, grid, tpb) in [(1, 0, 2 * nsm, 1024), (1, 0, nsm, 1024), (1, 0, 4 * nsm, 512)] + \
+                    [(3, K, nsm, 1024) for K in args.hot if K * sv <= 200 * 1024]:
+                med, mn = timeit(lambda: runr(mode, K, grid, tpb), args.reps, flush)
+                cover = float(cnt[order[:K]].sum()) / nnz
+                print(json.dumps({**base, "kernel": f"relabel_gather_hot{K}_g{grid}_t{tpb}", "hot_cover": cover,
+                                  "median_us": med * 1e3, "min_us": mn * 1e3, "model_gbs": model / (med * 1e-3) / 1e9,
+                                  "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
+            # cost of permuting x per call (x'[i] = x[order[i]])
+            dorder = torch.from_numpy(order).to(dev)
+            med, mn = timeit(lambda: torch.index_select(xsave, 0, dorder, out=xr), args.reps, flush)
+            print(json.dumps({**base, "kernel": "permute_x_index_select", "median_us": med * 1e3}), flush=True)
+            del rcol, xr, dorder
         # random sectors alone: the same number of gathers, hashed indices, no index stream
         med, mn = timeit(lambda: lib.gr_launch_hash(dt, x.data_ptr(), n, nnz, out.data_ptr(), 2 * nsm, 1024, s),
                          args.reps, flush)
