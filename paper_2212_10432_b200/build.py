@@ -8,11 +8,15 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libalphasparse.so")
-BUILD = os.path.join(HERE, "build")
+# A/B builds (developer timing, tools/sweep.py): AS_BUILD_TAG=t AS_BUILD_DEFS="-DX=1 ..." builds
+# libalphasparse_t.so in build_t/; the binding loads it with AS_LIB_AB=paper_2212_10432_b200/libalphasparse_t.so
+_TAG = os.environ.get("AS_BUILD_TAG", "")
+OUT = os.path.join(HERE, f"libalphasparse{'_' + _TAG if _TAG else ''}.so")
+BUILD = os.path.join(HERE, f"build{'_' + _TAG if _TAG else ''}")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-Wall", "-I", os.path.join(HERE, "..", "include")]
+FLAGS += os.environ.get("AS_BUILD_DEFS", "").split()
 
 
 def sources():

@@ -12,6 +12,13 @@ namespace as {
 namespace {
 
 // ---------------------------------------------------------------- load helpers
+// Loads are plain (non-volatile) inline PTX so the compiler may hoist and batch them like
+// ordinary loads; AS_LD_VOLATILE=1 restores `asm volatile` (A/B knob).
+#if defined(AS_LD_VOLATILE) && AS_LD_VOLATILE
+#define AS_LDASM asm volatile
+#else
+#define AS_LDASM asm
+#endif
 // Matrix streams: read once per SpMV -> L1::no_allocate + an L2 evict_first cache policy.
 __device__ __forceinline__ uint64_t pol_ef() {
   uint64_t p;
@@ -20,7 +27,7 @@ __device__ __forceinline__ uint64_t pol_ef() {
 }
 #define AS_LD1(T, PT, C, p)                                                                            \
   T v;                                                                                                 \
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint." PT " %0, [%1], %2;" : "=" C(v) : "l"(p), \
+  AS_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint." PT " %0, [%1], %2;" : "=" C(v) : "l"(p), \
                "l"(pol_ef()));                                                                         \
   return v;
 __device__ __forceinline__ double ld_stream(const double* p) { AS_LD1(double, "f64", "d", p) }
@@ -28,35 +35,35 @@ __device__ __forceinline__ float ld_stream(const float* p) { AS_LD1(float, "f32"
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { AS_LD1(int32_t, "s32", "r", p) }
 __device__ __forceinline__ double2 ld_stream2(const double* p) {
   double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+  AS_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
                : "=d"(v.x), "=d"(v.y)
                : "l"(p), "l"(pol_ef()));
   return v;
 }
 __device__ __forceinline__ float4 ld_stream4(const float* p) {
   float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+  AS_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "l"(p), "l"(pol_ef()));
   return v;
 }
 __device__ __forceinline__ float2 ld_stream2(const float* p) {
   float2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+  AS_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
                : "=f"(v.x), "=f"(v.y)
                : "l"(p), "l"(pol_ef()));
   return v;
 }
 __device__ __forceinline__ int2 ld_stream_i2(const int32_t* p) {
   int2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+  AS_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
                : "=r"(v.x), "=r"(v.y)
                : "l"(p), "l"(pol_ef()));
   return v;
 }
 __device__ __forceinline__ int4 ld_stream_i4(const int32_t* p) {
   int4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+  AS_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p), "l"(pol_ef()));
   return v;
@@ -71,13 +78,22 @@ __device__ __forceinline__ uint64_t pol_el() {
 }
 __device__ __forceinline__ double ldx(const double* x, int64_t c) {
   double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
+  AS_LDASM("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
   return v;
 }
 __device__ __forceinline__ double ldx(const float* x, int64_t c) {
   float v;
-  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  AS_LDASM("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
   return (double)v;
+}
+// the same gathers in the value type (fp32 operands are widened only at the FMA: the
+// product of two fp32 numbers is exact in fp64, so this is the same arithmetic with half
+// the registers per element in flight)
+__device__ __forceinline__ double ldxv(const double* x, int64_t c) { return ldx(x, c); }
+__device__ __forceinline__ float ldxv(const float* x, int64_t c) {
+  float v;
+  AS_LDASM("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  return v;
 }
 // metadata: small, reused by neighbours -> plain non-coherent load
 __device__ __forceinline__ int32_t ldm(const int32_t* p) { return __ldg(p); }
@@ -207,7 +223,8 @@ template <class V, int VEC>
 struct PadLoad;
 template <>
 struct PadLoad<double, 2> {
-  static __device__ __forceinline__ void ld(const double* v, const int32_t* c, double* vo, int32_t* co) {
+  template <class O>
+  static __device__ __forceinline__ void ld(const double* v, const int32_t* c, O* vo, int32_t* co) {
     double2 a = ld_stream2(v);
     int2 b = ld_stream_i2(c);
     vo[0] = a.x;
@@ -218,7 +235,8 @@ struct PadLoad<double, 2> {
 };
 template <>
 struct PadLoad<float, 4> {
-  static __device__ __forceinline__ void ld(const float* v, const int32_t* c, double* vo, int32_t* co) {
+  template <class O>
+  static __device__ __forceinline__ void ld(const float* v, const int32_t* c, O* vo, int32_t* co) {
     float4 a = ld_stream4(v);
     int4 b = ld_stream_i4(c);
     vo[0] = a.x;
@@ -233,7 +251,8 @@ struct PadLoad<float, 4> {
 };
 template <>
 struct PadLoad<float, 2> {
-  static __device__ __forceinline__ void ld(const float* v, const int32_t* c, double* vo, int32_t* co) {
+  template <class O>
+  static __device__ __forceinline__ void ld(const float* v, const int32_t* c, O* vo, int32_t* co) {
     float2 a = ld_stream2(v);
     int2 b = ld_stream_i2(c);
     vo[0] = a.x;
@@ -244,14 +263,16 @@ struct PadLoad<float, 2> {
 };
 template <class V>
 struct PadLoad<V, 1> {
-  static __device__ __forceinline__ void ld(const V* v, const int32_t* c, double* vo, int32_t* co) {
-    vo[0] = (double)ld_stream(v);
+  template <class O>
+  static __device__ __forceinline__ void ld(const V* v, const int32_t* c, O* vo, int32_t* co) {
+    vo[0] = (O)ld_stream(v);
     co[0] = ld_stream(c);
   }
 };
 template <>
 struct PadLoad<double, 4> {
-  static __device__ __forceinline__ void ld(const double* v, const int32_t* c, double* vo, int32_t* co) {
+  template <class O>
+  static __device__ __forceinline__ void ld(const double* v, const int32_t* c, O* vo, int32_t* co) {
     double2 a = ld_stream2(v), b = ld_stream2(v + 2);
     int4 q = ld_stream_i4(c);
     vo[0] = a.x;
@@ -267,17 +288,17 @@ struct PadLoad<double, 4> {
 
 __device__ __forceinline__ double ld_seq(const double* p) {
   double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol_ef()));
+  AS_LDASM("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol_ef()));
   return v;
 }
 __device__ __forceinline__ float ld_seq(const float* p) {
   float v;
-  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol_ef()));
+  AS_LDASM("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol_ef()));
   return v;
 }
 __device__ __forceinline__ int32_t ld_seq(const int32_t* p) {
   int32_t v;
-  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_ef()));
+  AS_LDASM("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_ef()));
   return v;
 }
 

@@ -128,10 +128,22 @@ __global__ void __launch_bounds__(1024) k_thread_row_pad(DevPart p, const V* __r
 // every bitmap head after element 0; returns the open (last) segment in acc/row/inside.
 // x accessors: straight from global memory (L1 / L2 evict_last), or from a shared-memory
 // ring buffer holding the CTA's current x window (banded matrices, k_nnz_thread_xw).
+// Elements per batch of the warp-level NNZ kernels: fp64 batches of 8 spill 100-180 bytes
+// next to the warp-combine state; fp32 operands stay fp32 in registers until the FMA, so
+// fp32 can afford AS_KBW_F32 in flight.
+#ifndef AS_KBW_F32
+#define AS_KBW_F32 4
+#endif
+template <class V>
+constexpr int kbw_of() {
+  return sizeof(V) == 4 ? AS_KBW_F32 : 4;
+}
+
 template <class V>
 struct XGlobal {
   const V* __restrict__ x;
   __device__ __forceinline__ double operator()(int64_t c) const { return ldx(x, c); }
+  __device__ __forceinline__ V v(int64_t c) const { return ldxv(x, c); }
 };
 // Hot-x cache (SET_RESOURCE xcache, reading R-xcache): the part's K most referenced x
 // entries are staged in shared memory once per (persistent) CTA; their columns were
@@ -143,6 +155,7 @@ struct XHot {
   const V* __restrict__ x;
   const V* sm;
   __device__ __forceinline__ double operator()(int64_t c) const { return c < 0 ? (double)sm[~c] : ldx(x, c); }
+  __device__ __forceinline__ V v(int64_t c) const { return c < 0 ? sm[~c] : ldxv(x, c); }
 };
 // All CTAs fill at kernel start, so the fill's latency is exposed once per CTA: 8 column
 // indices, then 8 gathers, are in flight per thread (a one-load-at-a-time loop cost ~25 us
@@ -171,6 +184,7 @@ struct XRing {
   const V* ring;
   int64_t mask;
   __device__ __forceinline__ double operator()(int64_t c) const { return (double)ring[c & mask]; }
+  __device__ __forceinline__ V v(int64_t c) const { return ring[c & mask]; }
 };
 
 // One batch of KB elements starting at j0.  FULL: j0 + KB <= len, so no bounds predicates
@@ -188,7 +202,7 @@ __device__ __forceinline__ void bmt_batch(XA xa, const uint32_t* bm, const V* pv
       } else {
 #pragma unroll
         for (int r = 0; r < VEC; ++r) {
-          v[q + r] = 0.0;
+          v[q + r] = (V)0;
           c[q + r] = 0;
         }
       }
@@ -306,7 +320,7 @@ __device__ __forceinline__ void emit_excl(const DevPart& p, V* y, bool pred, int
 
 // Loads of one batch (values, columns) ...
 template <class V, bool PAD, int VEC, int KB, bool FULL>
-__device__ __forceinline__ void batch_load(const V* pv, const int32_t* pc, int64_t stride, int j0, int len, double* v,
+__device__ __forceinline__ void batch_load(const V* pv, const int32_t* pc, int64_t stride, int j0, int len, V* v,
                                            int32_t* c) {
   if constexpr (PAD) {
 #pragma unroll
@@ -316,7 +330,7 @@ __device__ __forceinline__ void batch_load(const V* pv, const int32_t* pc, int64
       } else {
 #pragma unroll
         for (int r = 0; r < VEC; ++r) {
-          v[q + r] = 0.0;
+          v[q + r] = (V)0;
           c[q + r] = 0;
         }
       }
@@ -325,10 +339,10 @@ __device__ __forceinline__ void batch_load(const V* pv, const int32_t* pc, int64
 #pragma unroll
     for (int q = 0; q < KB; ++q) {
       if (FULL || j0 + q < len) {
-        v[q] = (double)ld_seq(pv + q);
+        v[q] = ld_seq(pv + q);
         c[q] = ld_seq(pc + q);
       } else {
-        v[q] = 0.0;
+        v[q] = (V)0;
         c[q] = 0;
       }
     }
@@ -338,11 +352,11 @@ __device__ __forceinline__ void batch_load(const V* pv, const int32_t* pc, int64
 // ... and their use: x gathers, then the branch-free bitmap-segmented accumulation.
 template <class V, int KB, int EM, bool FULL, class XA>
 __device__ __forceinline__ void batch_use(const DevPart& p, V* y, XA xa, const uint32_t* bm, int j0, int len,
-                                          const double* v, const int32_t* c, int32_t& row, double& acc, bool& inside,
+                                          const V* v, const int32_t* c, int32_t& row, double& acc, bool& inside,
                                           double& first) {
-  double xv[KB];
+  V xv[KB];
 #pragma unroll
-  for (int q = 0; q < KB; ++q) xv[q] = (FULL || j0 + q < len) ? xa(c[q]) : 0.0;
+  for (int q = 0; q < KB; ++q) xv[q] = (FULL || j0 + q < len) ? xa.v(c[q]) : (V)0;
   const uint32_t wd = (ldm(bm + (j0 >> 5)) >> (j0 & 31)) & ~(uint32_t)(j0 == 0);
 #pragma unroll
   for (int q = 0; q < KB; ++q) {
@@ -351,7 +365,7 @@ __device__ __forceinline__ void batch_use(const DevPart& p, V* y, XA xa, const u
     first = (h && !inside) ? acc : first;
     row += h ? 1 : 0;
     inside = inside || h;
-    acc = (h ? 0.0 : acc) + v[q] * xv[q];
+    acc = (h ? 0.0 : acc) + (double)v[q] * (double)xv[q];
   }
 }
 
@@ -383,7 +397,7 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   int j0 = 0;
   // pv / pc advance to the batch's first element (slot-major: KB/VEC chunk rows per batch)
   const int64_t adv = PAD ? (KB / VEC) * pp.stride : KB;
-  double v[KB];
+  V v[KB];
   int32_t c[KB];
   for (; j0 < full; j0 += KB, pv += adv, pc += adv) {
     batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, j0, len, v, c);
@@ -1251,7 +1265,7 @@ int launch_grp_nnz_warp(const DevPart& p, const V* x, V* y, cudaStream_t s) {
       const bool pe = p.variant < 8 && !(sizeof(V) == 4 && p.n_heavy && p.mode == 1);
       const bool em0 = p.mode == 0 && p.beta == 0.0 && !p.origin && !p.org_model.kind;
       const int64_t gx = std::min<int64_t>(g, (int64_t)std::max(1, p.xh_ctas) * sm_count());  // xcache: persistent
-      constexpr int KBW = 4;  // fp64 batches of 8 spill 100-180 bytes next to the warp-combine state
+      constexpr int KBW = kbw_of<V>();
 #define AS_NWPE(WR, PADV, VECV)                                                                  \
   {                                                                                              \
     if (p.xh_n && em0) k_nnz_warp_pe<V, WR, PADV, VECV, (KBW > VECV ? KBW : VECV), 0, true><<<gx, tpb, p.smem, s>>>(p, x, y); \
@@ -1371,7 +1385,7 @@ int xh_prep_thread(size_t smem, int tpb) {
 }
 template <class V, int WR, bool PAD, int VEC>
 int xh_prep_warp(size_t smem, int tpb) {
-  constexpr int KB = 4 > VEC ? 4 : VEC;
+  constexpr int KB = kbw_of<V>() > VEC ? kbw_of<V>() : VEC;
   return std::min(xh_optin(k_nnz_warp_pe<V, WR, PAD, VEC, KB, 0, true>, smem, tpb),
                   xh_optin(k_nnz_warp_pe<V, WR, PAD, VEC, KB, 1, true>, smem, tpb));
 }

@@ -51,10 +51,13 @@ def main():
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         med = statistics.median(ts)
+        P.spmv(1.0, dx, 0.0, dy)
+        ysum = float(dy.double().abs().sum())  # cross-variant sanity (same y up to rounding)
         bm = info["bytes_model"] if args.beta == 0 else info["bytes_model_beta"]
         print(json.dumps({"config": wl, "graph": g, "env": {k: v for k, v in os.environ.items() if k.startswith("AS_")},
                           "median_us": med * 1e3, "min_us": min(ts) * 1e3, "gflops": 2 * coo.nnz / (med * 1e-3) / 1e9,
-                          "model_gbs": bm / (med * 1e-3) / 1e9, "kernels": info["kernels"], "bytes_model": bm}))
+                          "model_gbs": bm / (med * 1e-3) / 1e9, "kernels": info["kernels"], "bytes_model": bm,
+                          "y_abs_sum": ysum, "lib": os.environ.get("AS_LIB_AB", "")}))
         del P
 
 
