@@ -130,9 +130,10 @@ __global__ void __launch_bounds__(1024) k_thread_row_pad(DevPart p, const V* __r
 // ring buffer holding the CTA's current x window (banded matrices, k_nnz_thread_xw).
 // Elements per batch of the warp-level NNZ kernels: fp64 batches of 8 spill 100-180 bytes
 // next to the warp-combine state; fp32 operands stay fp32 in registers until the FMA, so
-// fp32 can afford AS_KBW_F32 in flight.
+// fp32 affords 8 gathers in flight per lane at 64 registers (C3 winner family: 924.7 ->
+// 885.7 us; 16 spills 120-184 bytes and is slower, 949 us; profiles/r02/ab_kb.jsonl).
 #ifndef AS_KBW_F32
-#define AS_KBW_F32 4
+#define AS_KBW_F32 8
 #endif
 template <class V>
 constexpr int kbw_of() {
