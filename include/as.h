@@ -72,6 +72,7 @@ typedef struct {
                          with AS_EXCH_PEER fuses the peer stores into the SpMV epilogue */
   int modeled_arrays; /* index arrays replaced by fitted models (Model-Driven Format
                          Compression): computed in the kernel instead of loaded */
+  int device_built;   /* 1: the format was built by the on-device Designer (see as_plan) */
 } as_plan_info_t;
 
 const char* as_last_error(void);
@@ -116,13 +117,20 @@ void as_graph_destroy(as_graph_t);
  * implementing) and uploads the resulting device format to `device`
  * (device = -1: host-only plan, usable for as_plan_export but not for as_spmv).
  * Blocking.  The plan owns its device arrays and keeps no reference to the matrix.
- * flags: AS_PLAN_KEEP_HOST keeps the logical metadata on the host for as_plan_export. */
+ * flags: AS_PLAN_KEEP_HOST keeps the logical metadata on the host for as_plan_export.
+ * On-device Designer: graphs of the NNZ-blocked family
+ *   [SORT|SORT_SUB]; COMPRESS; [BMW_NNZ_BLOCK]; BMT_NNZ_BLOCK; [BMT_PAD(GLOBAL|BMW)];
+ *   THREAD_BITMAP_RED_G; [WARP_SEG_ADD_RED|WARP_BITMAP_RED]; [SET_RESOURCE]; GMEM_ATOM_RED
+ * are built on the GPU (CUB sorts/scans + kernels) unless AS_PLAN_KEEP_HOST, AS_PLAN_SPMM or
+ * AS_PLAN_HOST_BUILD is given; the first such plan uploads the matrix's canonical CSR to the
+ * device once and the matrix keeps that copy (freed by as_matrix_destroy) for later plans. */
 #define AS_PLAN_KEEP_HOST 1
 #define AS_PLAN_SPMM 2      /* also upload the plain CSR arrays of CSR-family parts (as_spmm) */
 #define AS_PLAN_GRAPH 4     /* as_spmv captures its launch sequence into a CUDA graph once per
                                (x, y, alpha, beta) and replays it: one launch per call.  The
                                plan then caches one graph: calls on the same plan must not run
                                concurrently from several host threads */
+#define AS_PLAN_HOST_BUILD 8 /* always run the host Designer (A/B of the on-device one) */
 as_status_t as_plan(as_matrix_t, as_graph_t, int device, void* stream, as_plan_t* out);
 as_status_t as_plan_ex(as_matrix_t, as_graph_t, int device, void* stream, int flags,
                        as_plan_t* out);

@@ -29,6 +29,7 @@ AS_R32F, AS_R64F = 0, 1
 AS_PLAN_KEEP_HOST = 1
 AS_PLAN_SPMM = 2
 AS_PLAN_GRAPH = 4
+AS_PLAN_HOST_BUILD = 8
 STATUS = {0: "AS_OK", 1: "AS_ERR_INVALID_ARG", 2: "AS_ERR_MALFORMED", 3: "AS_ERR_INDEX_OUT_OF_RANGE",
           4: "AS_ERR_DUPLICATE", 5: "AS_ERR_GRAPH_PARSE", 6: "AS_ERR_GRAPH_ILLEGAL", 7: "AS_ERR_PLAN_INFEASIBLE",
           8: "AS_ERR_OOM", 9: "AS_ERR_CUDA", 10: "AS_ERR_NO_FEASIBLE", 11: "AS_ERR_DTYPE", 12: "AS_ERR_NOT_FOUND",
@@ -51,7 +52,7 @@ class AsPlanInfo(ctypes.Structure):
                 ("n_launches", _i64), ("prepass_rows", _i64), ("bytes_model", ctypes.c_double),
                 ("bytes_model_beta", ctypes.c_double), ("bytes_floor", ctypes.c_double),
                 ("kernels", ctypes.c_char * 512), ("single_writer", ctypes.c_int),
-                ("modeled_arrays", ctypes.c_int)]
+                ("modeled_arrays", ctypes.c_int), ("device_built", ctypes.c_int)]
 
 
 class AsSearchCfg(ctypes.Structure):
@@ -272,7 +273,7 @@ class Plan:
     """a2-a4: the graph executed on the Matrix Metadata Set into a device-resident format."""
 
     def __init__(self, matrix: Matrix, graph, device: int = 0, stream=None, keep_host: bool = False, _handle=None,
-                 spmm: bool = False, graph_replay: bool = False):
+                 spmm: bool = False, graph_replay: bool = False, host_build: bool = False):
         self.dtype = np.dtype(matrix.dtype) if matrix is not None else None
         self.device = device
         self.m, self.n = matrix.shape if matrix is not None else (None, None)
@@ -284,7 +285,7 @@ class Plan:
         h = _vp()
         s = 0 if device < 0 else _stream_handle(stream)
         flags = ((AS_PLAN_KEEP_HOST if keep_host else 0) | (AS_PLAN_SPMM if spmm else 0)
-                 | (AS_PLAN_GRAPH if graph_replay else 0))
+                 | (AS_PLAN_GRAPH if graph_replay else 0) | (AS_PLAN_HOST_BUILD if host_build else 0))
         _ck(_lib.as_plan_ex(matrix._h, graph._h, device, s, flags, ctypes.byref(h)))
         self._h = h
 

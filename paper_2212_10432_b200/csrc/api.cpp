@@ -81,9 +81,28 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
     P->n = A.n;
     P->nnz_real = A.nnz();
     P->canon = canon;
-    P->host = build_plan(A, g);
     P->device = device;
     P->stream = stream;
+    DevSpec spec;
+    if (device >= 0 && dev_build_spec(g, A, flags, &spec)) {
+      // on-device Designer (devbuild.cu): the format is built on the GPU from the cached
+      // canonical CSR; P->host keeps only the part skeleton
+      int cur = 0;
+      check_cuda(cudaGetDevice(&cur), "cudaGetDevice");
+      check_cuda(cudaSetDevice(device), "cudaSetDevice");
+      try {
+        dev_build(*P, A, spec, (cudaStream_t)stream);
+        P->graph_mode = (flags & AS_PLAN_GRAPH) != 0;
+        P->dev_built = true;
+      } catch (...) {
+        cudaSetDevice(cur);
+        throw;
+      }
+      cudaSetDevice(cur);
+      P->host = HostPlan();
+      return P;
+    }
+    P->host = build_plan(A, g);
     if (device >= 0) {
       int cur = 0;
       check_cuda(cudaGetDevice(&cur), "cudaGetDevice");
@@ -322,6 +341,7 @@ as_status_t as_plan_info(as_plan_t P, as_plan_info_t* out) {
     *out = P->P->info;
     out->single_writer = P->P->single_writer ? 1 : 0;
     out->modeled_arrays = P->P->modeled_arrays;
+    out->device_built = P->P->dev_built ? 1 : 0;
   });
 }
 

@@ -84,12 +84,14 @@ void surrogate_fit_predict(const double* X, const double* y, size_t n, size_t d,
                            double* out, int rounds, int max_depth, double lr);
 
 // ------------------------------------------------------------------ matrix (host, canonical CSR)
+struct DevCsr;  // the canonical CSR uploaded for the on-device builder (devbuild.cu), cached
 struct Matrix {
   int64_t m = 0, n = 0;
   as_dtype_t dt = AS_R64F;
   std::vector<int64_t> row_ptr;  // m+1
   std::vector<int32_t> col;      // nnz, ascending within a row
   std::vector<double> val;       // nnz (fp32 data widened exactly)
+  mutable std::shared_ptr<DevCsr> dcache;  // device copy (devbuild.cu), shared by all plans of the matrix
   int64_t nnz() const { return (int64_t)col.size(); }
 };
 

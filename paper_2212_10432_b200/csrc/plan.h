@@ -34,6 +34,7 @@ struct Plan {
   // every row's final value is produced by exactly one STORE (no pre-pass, no ADD parts,
   // no atomic rows, no fp32 heavy-row epilogue): as_spmv_dist may fuse peer stores
   bool single_writer = false;
+  bool dev_built = false;  // format built by the on-device Designer (devbuild.cu)
   int modeled_arrays = 0;  // index arrays replaced by fitted models (NEXT-2)
   int fused_arrays = 0;    // per-BMT metadata arrays fused into one (short-array fusion, NEXT-2)
   bool spmm = false;              // AS_PLAN_SPMM: SpMM arrays of the CSR-family parts uploaded
@@ -65,6 +66,24 @@ struct Plan {
   int64_t n_heavy = 0;
   void compute_model();
 };
+
+// On-device Designer (devbuild.cu) for NNZ-blocked graphs: dev_build_spec decides whether
+// a graph is in the device-built family (and parses its parameters), dev_build builds the
+// format into P (launches, pre-pass, heavy rows, spans, bytes model, info).
+struct DevSpec {
+  int sort = 0;       // 0 none, 1 SORT, 2 SORT_SUB
+  int64_t g = 0;      // SORT_SUB group
+  int64_t K = 0;      // BMW_NNZ_BLOCK (0: no BMW level)
+  int64_t k = 0;      // BMT_NNZ_BLOCK
+  bool pad = false;
+  int pad_scope = -1; // -1 GLOBAL, 1 BMW
+  int64_t vec = 1;
+  int wred = RED_NONE;
+  int tpb = 0, grid = 0, stages = 2;
+  int64_t xcache = 0;
+};
+bool dev_build_spec(const Seq& g, const Matrix& A, int flags, DevSpec* sp);
+void dev_build(Plan& P, const Matrix& A, const DevSpec& sp, cudaStream_t s);
 
 // "dev.<key>" exports: the device arrays read back and decoded to the logical layout
 // (readback.cpp); keys "dev.p<part>.<name>"

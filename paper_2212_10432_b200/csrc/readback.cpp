@@ -148,6 +148,8 @@ std::vector<std::pair<std::string, std::vector<uint8_t>>> device_arrays(const Pl
     part_arrays(P, P.launches[i], P.launch_part[i], one);
     for (auto& kv : one) all.push_back({"dev.p" + std::to_string(P.launch_part[i]) + "." + kv.first, std::move(kv.second)});
   }
+  // the writer rule's pre-pass rows (A22) as uploaded
+  all.push_back({"dev.prepass", bytes(widen(d2h<int32_t>(P.d_prepass, P.n_prepass)))});
   cudaSetDevice(cur);
   return all;
 }
