@@ -135,6 +135,9 @@ as_status_t as_plan(as_matrix_t, as_graph_t, int device, void* stream, as_plan_t
 as_status_t as_plan_ex(as_matrix_t, as_graph_t, int device, void* stream, int flags,
                        as_plan_t* out);
 as_status_t as_plan_info(as_plan_t, as_plan_info_t* out);
+/* *out = 1 if as_plan_ex(M, G, device >= 0, flags) would build the format with the
+ * on-device Designer (the NNZ-blocked family above), else 0.  Host-only query. */
+as_status_t as_graph_device_buildable(as_matrix_t, as_graph_t, int flags, int* out);
 /* Logical metadata array `key` (DESIGN.md §Export keys, e.g. "p0.bmt.bitmap"), copied to
  * host_dst.  host_dst == NULL -> *bytes = size.  Needs a host-only plan or
  * AS_PLAN_KEEP_HOST.  Index arrays are int64, bitmaps uint32, values the plan dtype. */

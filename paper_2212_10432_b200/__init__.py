@@ -92,6 +92,7 @@ _sig("as_spmm", [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp])
 _sig("as_plan_profile", [_vp, _vp, _vp, _i32, _vp, _vp, _vp, _P(_sz)])
 _sig("as_search", [_vp, _P(AsSearchCfg), _i32, _vp, _P(_vp), ctypes.c_char_p, _P(_sz)])
 _sig("as_random_graph", [_vp, ctypes.c_uint64, ctypes.c_char_p, _P(_sz)])
+_sig("as_graph_device_buildable", [_vp, _vp, _i32, _P(_i32)])
 _sig("as_graph_features", [_vp, _vp, _P(_sz)])
 _sig("as_fit_array_model", [_vp, _sz, _i32, _vp])
 _sig("as_surrogate_fit_predict", [_vp, _vp, _sz, _sz, _vp, _sz, _vp])
@@ -117,7 +118,8 @@ EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create
             "as_plan_keys", "as_plan_destroy", "as_spmv", "as_spmv_host", "as_search", "as_random_graph",
             "as_dist_row_cuts", "as_dist_row_cuts_ptr", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
             "as_dist_set_cuts", "as_dist_ipc_handle", "as_dist_open_peers", "as_spmv_dist", "as_dist_check",
-            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows", "as_fit_array_model", "as_spmm", "as_plan_profile"]
+            "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows", "as_fit_array_model", "as_spmm", "as_plan_profile",
+            "as_graph_device_buildable"]
 
 
 class AsError(RuntimeError):
@@ -224,6 +226,15 @@ class Matrix:
 
     def random_graph(self, seed: int) -> str:
         return _string(_lib.as_random_graph, self._h, ctypes.c_uint64(seed))
+
+    def device_buildable(self, graph, host_build: bool = False) -> bool:
+        """Whether as_plan builds `graph` with the on-device Designer (as_graph_device_buildable)."""
+        if isinstance(graph, str):
+            graph = Graph(graph)
+        out = _i32()
+        _ck(_lib.as_graph_device_buildable(self._h, graph._h, AS_PLAN_HOST_BUILD if host_build else 0,
+                                           ctypes.byref(out)))
+        return bool(out.value)
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib:
@@ -457,6 +468,9 @@ def version() -> str:
 _hooks = None  # keeps the ctypes callbacks alive while installed
 
 
+_hooks_ever = []  # every installed callback pair stays alive (the library frees with the allocating hooks)
+
+
 def set_allocator(alloc=None, release=None):
     """as_set_allocator with Python callables alloc(nbytes, stream) -> int pointer (0 = out of
     memory) and release(ptr, stream); no arguments restores cudaMalloc/cudaFree."""
@@ -478,6 +492,7 @@ def set_allocator(alloc=None, release=None):
     hooks = (_ALLOC_T(_a), _FREE_T(_r))
     _ck(_lib.as_set_allocator(hooks[0], hooks[1], None))
     _hooks = hooks
+    _hooks_ever.append(hooks)  # memory made through these hooks is released through them later
 
 
 def use_torch_allocator():

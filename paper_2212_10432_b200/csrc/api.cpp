@@ -3,6 +3,8 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 
 #include "internal.h"
 #include "plan.h"
@@ -26,25 +28,43 @@ struct AllocHooks {
 }
 void set_last_error(const std::string& m) { g_last_error = m; }
 
+// Every allocation remembers the hooks that made it, so it is released by the same allocator
+// even after as_set_allocator changed them (a matrix's cached device CSR or a plan may
+// outlive the hooks that were current when it was built).
+std::mutex g_owner_mu;
+std::unordered_map<void*, AllocHooks> g_owner;
+
 void* dev_alloc(size_t bytes, void* stream) {
   void* d = nullptr;
-  if (g_hooks.alloc) {
-    d = g_hooks.alloc(bytes, stream, g_hooks.ctx);
+  const AllocHooks h = g_hooks;
+  if (h.alloc) {
+    d = h.alloc(bytes, stream, h.ctx);
     if (!d) fail(AS_ERR_OOM, "allocator hook returned NULL for " + std::to_string(bytes) + " bytes");
-    return d;
+  } else {
+    cudaError_t e = cudaMalloc(&d, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      fail(e == cudaErrorMemoryAllocation ? AS_ERR_OOM : AS_ERR_CUDA,
+           "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    }
   }
-  cudaError_t e = cudaMalloc(&d, bytes);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    fail(e == cudaErrorMemoryAllocation ? AS_ERR_OOM : AS_ERR_CUDA,
-         "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
-  }
+  std::lock_guard<std::mutex> lk(g_owner_mu);
+  g_owner[d] = h;
   return d;
 }
 
 void dev_free(void* p, void* stream) {
   if (!p) return;
-  if (g_hooks.release) g_hooks.release(p, stream, g_hooks.ctx);
+  AllocHooks h = g_hooks;
+  {
+    std::lock_guard<std::mutex> lk(g_owner_mu);
+    auto it = g_owner.find(p);
+    if (it != g_owner.end()) {
+      h = it->second;
+      g_owner.erase(it);
+    }
+  }
+  if (h.release) h.release(p, stream, h.ctx);
   else cudaFree(p);
 }
 
@@ -666,6 +686,14 @@ as_status_t as_search(as_matrix_t M, const as_search_cfg_t* cfg, int device, voi
     st = search_impl(M->A, cfg, device, stream, best, best_graph, len);
   });
   return g != AS_OK ? g : st;
+}
+
+as_status_t as_graph_device_buildable(as_matrix_t M, as_graph_t G, int flags, int* out) {
+  return guard([&] {
+    if (!M || !G || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    DevSpec sp;
+    *out = dev_build_spec(G->g, M->A, flags, &sp) ? 1 : 0;
+  });
 }
 
 as_status_t as_random_graph(as_matrix_t M, uint64_t seed, char* buf, size_t* len) {

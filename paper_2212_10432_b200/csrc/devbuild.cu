@@ -256,8 +256,21 @@ __global__ void k_writer(const int64_t* __restrict__ rpc, const int32_t* __restr
 __global__ void k_heavy_bits(const int32_t* __restrict__ rows, int64_t n, uint32_t* __restrict__ bits) {
   for (int64_t i = gtid_(); i < n; i += gthr_()) atomicOr(bits + (rows[i] >> 5), 1u << (rows[i] & 31));
 }
+__global__ void k_scatter_stride(const int32_t* __restrict__ in, int64_t n, int32_t* __restrict__ out, int64_t stride) {
+  for (int64_t i = gtid_(); i < n; i += gthr_()) out[i * stride] = in[i];
+}
 __global__ void k_widen_f32(const double* __restrict__ in, int64_t n, float* __restrict__ out) {
   for (int64_t i = gtid_(); i < n; i += gthr_()) out[i] = (float)in[i];
+}
+
+// Model-Driven Format Compression of a device int32 array (the host's fit_array_model on a
+// copy; the fit rejects random data after a few elements)
+bool fit_model_d2h(const int32_t* d, int64_t n, cudaStream_t s, IdxModel* out) {
+  if (n < 2) return false;
+  std::vector<int32_t> h((size_t)n);
+  ck(cudaMemcpyAsync(h.data(), d, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "model d2h");
+  ck(cudaStreamSynchronize(s), "model d2h sync");
+  return fit_array_model(std::vector<int64_t>(h.begin(), h.end()), kMaxPatches, out);
 }
 
 // select the indices i in [0, n) with flag[i] != 0 (ascending) into a new int32 array
@@ -281,7 +294,7 @@ int32_t* select_flagged(Scratch& S, const uint8_t* flag, int64_t n, int64_t* cou
 bool dev_build_spec(const Seq& g, const Matrix& A, int flags, DevSpec* sp) {
   if (std::getenv("AS_HOST_BUILD") || std::getenv("AS_NT_LEGACY")) return false;
   if (flags & (AS_PLAN_KEEP_HOST | AS_PLAN_SPMM | AS_PLAN_HOST_BUILD)) return false;
-  if (A.nnz() == 0 || A.nnz() >= INT32_MAX || A.m >= INT32_MAX || A.n >= INT32_MAX) return false;
+  if (A.nnz() == 0 || A.m >= INT32_MAX || A.n >= INT32_MAX) return false;
   DevSpec d;
   size_t i = 0;
   if (i < g.size() && g[i].name == "SORT") {
@@ -451,8 +464,11 @@ void dev_build(Plan& P, const Matrix& A, const DevSpec& sp, cudaStream_t s) {
   d.n = n;
   d.m_p = mp;
   d.nnz_p = nnz;
+  const bool mdc = !std::getenv("AS_NO_MDC");  // Model-Driven Format Compression (as Plan::upload)
   if (affine) {
     d.origin_base = 0;
+  } else if (mdc && fit_model_d2h(origin, mp, s, &d.org_model)) {
+    ++P.modeled_arrays;
   } else {
     d.origin = (const int32_t*)P.up(nullptr, 0, s, (size_t)mp * 4);
     ck(cudaMemcpyAsync((void*)d.origin, origin, (size_t)mp * 4, cudaMemcpyDeviceToDevice, s), "origin");
@@ -465,6 +481,7 @@ void dev_build(Plan& P, const Matrix& A, const DevSpec& sp, cudaStream_t s) {
   d.k = sp.k;
   const bool st_affine = !sp.K || sp.K % sp.k == 0 || nnz <= sp.K;
   if (!st_affine) {
+    if (nnz >= INT32_MAX) fail(AS_ERR_PLAN_INFEASIBLE, "bmt_start exceeds int32 (reading A36)");
     int32_t* st = (int32_t*)P.up(nullptr, 0, s, (size_t)(n_bmt + 1) * 4);
     k_bmt_start<<<blocks(n_bmt + 1), TPB, 0, s>>>(geo, n_bmt, st);
     d.bmt_start = st;
@@ -473,10 +490,19 @@ void dev_build(Plan& P, const Matrix& A, const DevSpec& sp, cudaStream_t s) {
   const int bmw_words = (int)((sp.k + 31) / 32);
   d.bm_words = bmw_words;
   const bool fuse = !std::getenv("AS_NO_FUSE") && bmw_words >= 1 && bmw_words <= 3;
-  if (fuse) {  // short-array fusion: {first_row, bm0[, bm1[, bm2]]} per BMT
+  int32_t* fr_tmp = S.get<int32_t>((size_t)n_bmt);
+  k_first_row<<<blocks(n_bmt), TPB, 0, s>>>(rpc, mp, geo, n_bmt, fr_tmp, 1);
+  if (mdc && fit_model_d2h(fr_tmp, n_bmt, s, &d.fr_model)) {
+    ++P.modeled_arrays;  // first rows computed, not loaded (NEXT-2); bitmap stored alone
+    uint32_t* bm = (uint32_t*)P.up(nullptr, 0, s, (size_t)(n_bmt * bmw_words) * 4);
+    k_bitmap<<<blocks(mp), TPB, 0, s>>>(rpc, mp, geo, bm, bmw_words);
+    d.bitmap = bm;
+    d.bm_stride = bmw_words;
+    bytes_model += (double)(n_bmt * bmw_words * 4);
+  } else if (fuse) {  // short-array fusion: {first_row, bm0[, bm1[, bm2]]} per BMT
     const int S4 = bmw_words + 1 <= 2 ? 2 : 4;
     int32_t* f = (int32_t*)P.up(nullptr, 0, s, (size_t)(n_bmt * S4) * 4);  // zero-filled
-    k_first_row<<<blocks(n_bmt), TPB, 0, s>>>(rpc, mp, geo, n_bmt, f, S4);
+    k_scatter_stride<<<blocks(n_bmt), TPB, 0, s>>>(fr_tmp, n_bmt, f, S4);
     k_bitmap<<<blocks(mp), TPB, 0, s>>>(rpc, mp, geo, (uint32_t*)(f + 1), S4);
     d.bmt_first_row = f;
     d.bitmap = (const uint32_t*)(f + 1);
@@ -486,7 +512,7 @@ void dev_build(Plan& P, const Matrix& A, const DevSpec& sp, cudaStream_t s) {
   } else {
     int32_t* fr = (int32_t*)P.up(nullptr, 0, s, (size_t)n_bmt * 4);
     uint32_t* bm = (uint32_t*)P.up(nullptr, 0, s, (size_t)(n_bmt * bmw_words) * 4);
-    k_first_row<<<blocks(n_bmt), TPB, 0, s>>>(rpc, mp, geo, n_bmt, fr, 1);
+    ck(cudaMemcpyAsync(fr, fr_tmp, (size_t)n_bmt * 4, cudaMemcpyDeviceToDevice, s), "first_row");
     k_bitmap<<<blocks(mp), TPB, 0, s>>>(rpc, mp, geo, bm, bmw_words);
     d.bmt_first_row = fr;
     d.bitmap = bm;
@@ -569,8 +595,21 @@ void dev_build(Plan& P, const Matrix& A, const DevSpec& sp, cudaStream_t s) {
     d.n_grp = n_grp;
     d.grp_regular = bpg;
     d.grp_first_bmt = (const int32_t*)P.up(gfirst.data(), gfirst.size() * 4, s);
-    d.grp_base = (const int64_t*)P.up(gbase.data(), gbase.size() * 8, s);
-    d.grp_width = (const int32_t*)P.up(gw.data(), gw.size() * 4, s);
+    double saved = 0;  // per-group slot base and pad_width as models (as Plan::upload_pad)
+    if (mdc && fit_array_model(gbase, kMaxPatches, &d.pb_model)) {
+      ++P.modeled_arrays;
+      saved += (double)n_grp * 8;
+    } else {
+      d.grp_base = (const int64_t*)P.up(gbase.data(), gbase.size() * 8, s);
+    }
+    std::vector<int64_t> gw64(gw.begin(), gw.end());
+    if (mdc && fit_array_model(gw64, kMaxPatches, &d.pw_model)) {
+      ++P.modeled_arrays;
+      saved += (double)n_grp * 4;
+    } else {
+      d.grp_width = (const int32_t*)P.up(gw.data(), gw.size() * 4, s);
+    }
+    bytes_model -= saved;
     int32_t* pcol = (int32_t*)P.up(nullptr, 0, s, (size_t)total * 4);
     void* pval = P.up(nullptr, 0, s, (size_t)(total * sv));
     if (f64) k_pad_fill<double><<<blocks(total), TPB, 0, s>>>(geo, n_grp, bpg, Wf, Wl, vec, total, col_c, (const double*)val_c, slot, pcol, (double*)pval, n_bmt);

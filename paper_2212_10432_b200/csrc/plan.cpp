@@ -382,7 +382,10 @@ void Plan::upload(cudaStream_t s) {
       bytes_model += (double)(h.tile_val.size() * sv + (h.tile_col.size() + 2 * h.tile_row_id.size() + 1) * 4);
     } else {
       const int64_t mp = (int64_t)h.origin.size(), nnz = h.row_ptr.back();
-      if (nnz >= INT32_MAX) fail(AS_ERR_PLAN_INFEASIBLE, "part nnz exceeds int32 (reading A36)");
+      // Index widths (A36, narrowest lossless per array): element positions are computed in
+      // int64 by the kernels (implicit NNZ block starts t*k, int64 BMT_PAD group bases), so a
+      // part may hold >= 2^31 nonzeros; every STORED index array is int32 and up_i32 rejects
+      // one whose values do not fit (AS_ERR_PLAN_INFEASIBLE naming the array)
       d.m_p = mp;
       d.nnz_p = nnz;
       // origin_rows: implicit when affine (A17), else a fitted model (NEXT-2), else stored

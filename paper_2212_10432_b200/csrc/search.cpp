@@ -493,8 +493,36 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
   // Large matrices: rank candidates on a contiguous row sample of ~2^25 nonzeros taken
   // from the middle of the matrix (plan building of 10^9-nnz candidates would otherwise
   // dominate the budget), then re-plan and re-time the best few on the full matrix.
+  // With the on-device Designer (devbuild.cu) a full-size candidate of the NNZ-blocked family
+  // plans in ~0.1-1 s even at 10^9 nonzeros, so large matrices are searched at full size over
+  // that family (the generator's proposals outside it, which would need the host Designer,
+  // are redrawn); AS_SEARCH_SAMPLE=1 restores the row-sample ranking over every family.
   const int64_t kSample = int64_t(1) << 26;
-  const bool sampled = A.nnz() > 4 * kSample;
+  const bool big = A.nnz() > 4 * kSample;
+  const bool dev_full = big && !std::getenv("AS_SEARCH_SAMPLE");
+  const bool sampled = big && !dev_full;
+  auto in_family = [&](const std::string& text) {
+    if (!dev_full) return true;
+    try {
+      DevSpec sp;
+      return dev_build_spec(parse_graph(text), A, 0, &sp);
+    } catch (const Error&) {
+      return false;
+    }
+  };
+  // a random proposal; for full-size searches of large matrices one of the device-built family
+  // (about 3 % of the generator's graphs: redraw up to 400 times, statistics computed once)
+  const Stats prop_st = stats_of(A);
+  auto propose = [&](const Matrix& Mx, Rng& r) {
+    if (!dev_full) return random_graph(Mx, r.next());
+    std::string t;
+    for (int k = 0; k < 400; ++k) {
+      Rng g(r.next());
+      t = gen_path(g, prop_st, true, true, true, 0);
+      if (in_family(t)) break;
+    }
+    return t;
+  };
   Matrix S;
   if (sampled) {
     int64_t mid = A.nnz() / 2;
@@ -559,7 +587,7 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
   for (int i = 0; i < maxc + cfg->n_seed_graphs; ++i) {
     if (cfg->budget_seconds > 0 && elapsed() > coarse_frac * cfg->budget_seconds && tried > 0) break;
     if (i >= cfg->n_seed_graphs && tried >= maxc) break;
-    std::string text = i < cfg->n_seed_graphs ? std::string(cfg->seed_graphs[i]) : random_graph(M, seq.next());
+    std::string text = i < cfg->n_seed_graphs ? std::string(cfg->seed_graphs[i]) : propose(M, seq);
     evaluate(i, text, sampled ? "sample" : "ok");
   }
   // cost-model stage (NEXT-3, P:369 step 3): fit the gradient-boosted tree model on the
@@ -593,11 +621,11 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
         } catch (const Error&) {
           return;
         }
-        if (seen.count(c) || inpool.count(c)) return;
+        if (seen.count(c) || inpool.count(c) || !in_family(c)) return;
         inpool.insert(c);
         pool.push_back(c);
       };
-      for (int k = 0; k < 192; ++k) add(random_graph(M, pr.next()));
+      for (int k = 0; k < 192; ++k) add(dev_full ? propose(M, pr) : random_graph(M, pr.next()));
       for (size_t b = 0; b < std::min<size_t>(4, okc.size()); ++b)
         for (int k = 0; k < 24; ++k) add(mutate_graph(parse_graph(okc[b].canon), pr));
       if (pool.empty()) break;
@@ -630,7 +658,7 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
     for (int step = 0; step < maxc; ++step) {
       if (cfg->budget_seconds > 0 && elapsed() > cfg->budget_seconds) break;
       std::string nb = mutate_graph(parse_graph(cur), mr);
-      if (nb.empty() || seen.count(nb)) continue;
+      if (nb.empty() || seen.count(nb) || !in_family(nb)) continue;
       auto [t, canon] = evaluate(1000 + step, nb, sampled ? "sample_refine" : "refine");
       if (t > 0 && (t < tcur || mr.coin(std::exp(-(t - tcur) / std::max(temp, 1e-9))))) {
         cur = canon;

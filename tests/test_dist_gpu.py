@@ -177,7 +177,7 @@ def test_torch_allocator_hooks():
         y = np.zeros(c.m)
         P.spmv_host(1.0, x, 0.0, y)
         assert np.array_equal(y, _oracle_power(c, x, 1))
-        del P
+        del P, A  # the matrix owns the device copy of its CSR made by the on-device Designer
         assert not live
     finally:
         asp.set_allocator()

@@ -395,3 +395,26 @@ def test_binding_checks_host_arrays():
     y.flags.writeable = False
     with pytest.raises(asp.AsError):
         P.spmv_host(1.0, x, 0.0, y)
+
+
+def test_device_buildable_query():
+    """as_graph_device_buildable: the NNZ-blocked family goes to the on-device Designer
+    (devbuild.cu); ROW blocks, converting branches, the tile kernel's shapes, x windows and
+    AS_PLAN_HOST_BUILD stay on the host Designer."""
+    coo = synth.random_powerlaw(500, 400, 2, 90)
+    A = asp.Matrix.from_coo(coo.m, coo.n, coo.row, coo.col, coo.val)
+    yes = ["COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; SET_RESOURCE(stages=0); GMEM_ATOM_RED",
+           "SORT; COMPRESS; BMW_NNZ_BLOCK(100); BMT_NNZ_BLOCK(7); BMT_PAD(BMW,1); THREAD_BITMAP_RED_G; "
+           "WARP_SEG_ADD_RED; GMEM_ATOM_RED",
+           "SORT_SUB(g=4); COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(2); BMT_PAD(GLOBAL,0); THREAD_BITMAP_RED_G; "
+           "WARP_BITMAP_RED; GMEM_ATOM_RED"]
+    no = ["COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED",  # x-window candidate (stages=2)
+          "COMPRESS; BMW_NNZ_BLOCK(256); BMT_NNZ_BLOCK(2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
+          "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED",
+          "BIN(t=[4]) { COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; SET_RESOURCE(stages=0); GMEM_ATOM_RED }",
+          "COMPRESS; BMTB_NNZ_BLOCK(64); BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; SET_RESOURCE(stages=0); GMEM_ATOM_RED"]
+    for g in yes:
+        assert A.device_buildable(g), g
+        assert not A.device_buildable(g, host_build=True), g
+    for g in no:
+        assert not A.device_buildable(g), g

@@ -56,8 +56,10 @@ def main():
                                   "device_built": P.info()["device_built"], "kernels": P.info()["kernels"]}),
                       flush=True)
                 del P
-            same = bool(torch.equal(ys["device"], ys["host"]))
-            print(json.dumps({"config": wl, "graph": g, "y_bit_identical": same}), flush=True)
+            # real-valued data: atomics of straddling rows may add in another order
+            diff = float(((ys["device"].double() - ys["host"].double()).abs().max()
+                          / ys["host"].double().abs().max().clamp_min(1e-300)))
+            print(json.dumps({"config": wl, "graph": g, "y_max_rel_diff": diff}), flush=True)
         del A
 
 
