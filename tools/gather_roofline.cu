@@ -142,6 +142,70 @@ __global__ void __launch_bounds__(1024) k_gather(const V* __restrict__ val, cons
   if (acc == 1234.5678) out[0] = acc;  // keeps the loads live; practically never stores
 }
 
+// mode 5: x gathers issued as cp.async (LDGSTS) into a per-thread shared-memory staging
+// ring (no registers held while in flight), CH elements per chunk, 2 chunks in flight, the
+// first nh columns (relabeled / encoded hot set) read from a shared-memory copy.  Measures
+// whether register-free gathers raise the sustainable gather rate.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+template <class V>
+__device__ __forceinline__ void cp_async_x(V* dst, const V* src) {
+  if constexpr (sizeof(V) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+template <class V, int CH>
+__global__ void __launch_bounds__(1024) k_gather_async(const V* __restrict__ val, const int32_t* __restrict__ col,
+                                                        const V* __restrict__ x, const V* __restrict__ xh, int nh,
+                                                        int64_t nnz, double* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  V* sh = (V*)smem;
+  for (int i = threadIdx.x; i < nh; i += blockDim.x) sh[i] = xh[i];
+  V* ring = sh + ((nh + 3) & ~3) + threadIdx.x * (2 * CH + 1);
+  __syncthreads();
+  constexpr int W = Vec<V>::W;
+  static_assert(CH % W == 0, "chunk = whole vectors");
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nch = nnz / ((int64_t)CH * T);  // full chunk rounds (tail ignored: microbench)
+  double acc = 0.0;
+  V vprev[CH];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto chunk_base = [&](int64_t r) { return (r * T + tid) * CH; };
+  auto issue = [&](int64_t r, int buf, V* vv) {
+    const int64_t b = chunk_base(r);
+#pragma unroll
+    for (int q = 0; q < CH; q += W) {
+      double v[W];
+      int32_t c[W];
+      Vec<V>::ld(val + b + q, col + b + q, v, c);
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        vv[q + w] = (V)v[w];
+        V* d = ring + buf * CH + q + w;
+        if (c[w] < nh) *d = sh[c[w]];
+        else cp_async_x(d, x + c[w]);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (nch > 0) issue(0, 0, vprev);
+  for (int64_t r = 0; r < nch; ++r) {
+    V vcur[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) vcur[q] = vprev[q];
+    if (r + 1 < nch) {
+      issue(r + 1, (int)((r + 1) & 1), vprev);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    const V* xs = ring + (r & 1) * CH;
+#pragma unroll
+    for (int q = 0; q < CH; ++q) acc += (double)vcur[q] * (double)xs[q];
+  }
+  if (acc == 1234.5678) out[0] = acc;
+}
+
 __device__ __forceinline__ uint32_t mix(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
@@ -189,6 +253,27 @@ int gr_launch(int dtype, int mode, const void* val, const int32_t* col, const vo
     else L(double, 3);
   }
 #undef L
+  return (int)cudaGetLastError();
+}
+// cp.async-staged gathers (mode 5): ch = chunk elements (8 or 16), nh hot columns in smem
+int gr_launch_async(int dtype, int ch, const void* val, const int32_t* col, const void* x, const void* xh, int nh,
+                    int64_t nnz, double* out, int grid, int tpb, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sv = dtype ? 8 : 4;
+  size_t sm = ((size_t)((nh + 3) & ~3) + (size_t)tpb * (2 * ch + 1)) * sv;
+#define LA(V, C)                                                                                                    \
+  do {                                                                                                              \
+    cudaFuncSetAttribute(k_gather_async<V, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);               \
+    k_gather_async<V, C><<<grid, tpb, sm, s>>>((const V*)val, col, (const V*)x, (const V*)xh, nh, nnz, out);         \
+  } while (0)
+  if (dtype == 0) {
+    if (ch == 8) LA(float, 8);
+    else LA(float, 16);
+  } else {
+    if (ch == 8) LA(double, 8);
+    else LA(double, 16);
+  }
+#undef LA
   return (int)cudaGetLastError();
 }
 int gr_launch_hash(int dtype, const void* x, int64_t n, int64_t count, double* out, int grid, int tpb, void* stream) {

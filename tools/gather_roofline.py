@@ -35,6 +35,9 @@ def build():
     lib.gr_launch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                               ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
                               ctypes.c_int, ctypes.c_void_p]
+    lib.gr_launch_async.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                    ctypes.c_int, ctypes.c_void_p]
     lib.gr_launch_hash.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                    ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
     return lib
@@ -80,6 +83,8 @@ def main():
     ap.add_argument("--configs", nargs="+", default=["c3", "c4"])
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--hot", nargs="+", type=int, default=[8192, 16384, 32768, 49152])
+    ap.add_argument("--async-gather", action="store_true",
+                    help="also time cp.async-staged gathers (relabeled columns, hot prefix in smem)")
     ap.add_argument("--relabel", action="store_true",
                     help="also time the gathers with columns relabeled by descending reference count")
     args = ap.parse_args()
@@ -132,6 +137,33 @@ def main():
                               "min_us": mn * 1e3, "model_gbs": model / (med * 1e-3) / 1e9,
                               "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
             del denc
+        if args.async_gather:
+            rank = np.empty(n, np.int64)
+            rank[order] = np.arange(n)
+            rcol = torch.from_numpy(rank[col].astype(np.int32)).to(dev)
+            xr = x[torch.from_numpy(order).to(dev)].contiguous()
+            for (ch, K, tpb) in [(8, 0, 1024), (16, 0, 512), (8, 16384, 1024), (16, 16384, 512), (8, 8192, 1024)]:
+                def runa():
+                    rc = lib.gr_launch_async(dt, ch, dval.data_ptr(), rcol.data_ptr(), xr.data_ptr(), xr.data_ptr(), K,
+                                             nnz, out.data_ptr(), (2048 // tpb) * nsm if K == 0 else nsm, tpb, s)
+                    assert rc == 0, rc
+                try:
+                    med, mn = timeit(runa, args.reps, flush)
+                except AssertionError as e:
+                    print(json.dumps({**base, "kernel": f"async_ch{ch}_hot{K}_t{tpb}", "error": str(e)}), flush=True)
+                    continue
+                print(json.dumps({**base, "kernel": f"async_ch{ch}_hot{K}_t{tpb}", "median_us": med * 1e3,
+                                  "min_us": mn * 1e3, "model_gbs": model / (med * 1e-3) / 1e9,
+                                  "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
+            # the register-gather reference on the same relabeled columns
+            for K in (0, 16384):
+                def runr():
+                    rc = lib.gr_launch(dt, 3 if K else 1, dval.data_ptr(), rcol.data_ptr(), xr.data_ptr(), xr.data_ptr(),
+                                       K, nnz, out.data_ptr(), nsm if K else 2 * nsm, 1024, s)
+                    assert rc == 0, rc
+                med, mn = timeit(runr, args.reps, flush)
+                print(json.dumps({**base, "kernel": f"reg_relabel_hot{K}", "median_us": med * 1e3}), flush=True)
+            del rcol, xr
         if args.relabel:
             # column relabeling: rank[c] = position of c in the descending-count order; x permuted to match
             rank = np.empty(n, np.int64)
