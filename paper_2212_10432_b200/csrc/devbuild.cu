@@ -267,6 +267,15 @@ __global__ void k_widen_f32(const double* __restrict__ in, int64_t n, float* __r
 // copy; the fit rejects random data after a few elements)
 bool fit_model_d2h(const int32_t* d, int64_t n, cudaStream_t s, IdxModel* out) {
   if (n < 2) return false;
+  if (n > 8192) {  // probe: the first 4096 entries + the mid and last pairs decide most arrays
+    std::vector<int32_t> pre(4096), q(4);
+    ck(cudaMemcpyAsync(pre.data(), d, 4096 * 4, cudaMemcpyDeviceToHost, s), "model probe");
+    ck(cudaMemcpyAsync(q.data(), d + n / 2, 8, cudaMemcpyDeviceToHost, s), "model probe");
+    ck(cudaMemcpyAsync(q.data() + 2, d + n - 2, 8, cudaMemcpyDeviceToHost, s), "model probe");
+    ck(cudaStreamSynchronize(s), "model probe sync");
+    if (!model_may_fit(std::vector<int64_t>(pre.begin(), pre.end()), n, q[0], q[1], q[2], q[3], kMaxPatches))
+      return false;
+  }
   std::vector<int32_t> h((size_t)n);
   ck(cudaMemcpyAsync(h.data(), d, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "model d2h");
   ck(cudaStreamSynchronize(s), "model d2h sync");

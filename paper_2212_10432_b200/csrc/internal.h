@@ -76,6 +76,8 @@ bool is_branching(const std::string& name);
 
 // Model-Driven Format Compression (model.cpp, NEXT-2)
 bool fit_array_model(const std::vector<int64_t>& a, int budget, IdxModel* out);
+bool model_may_fit(const std::vector<int64_t>& pre, int64_t n, int64_t am0, int64_t am1, int64_t al0, int64_t al1,
+                   int budget);
 
 // search cost model (surrogate.cpp, NEXT-3)
 size_t graph_feature_count();

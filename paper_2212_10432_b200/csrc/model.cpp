@@ -9,6 +9,7 @@
 // Exact fitting with patches ("a small number of errors can be tolerated by adding if
 // statements"), at most `budget` (<= 8); fewest patches wins, earlier candidate on ties
 // (linear, periodic, step: SPEC S:337-340).
+#include <array>
 #include <cstring>
 
 #include "internal.h"
@@ -74,6 +75,30 @@ bool fit_array_model(const std::vector<int64_t>& a, int budget, IdxModel* out) {
   return true;
 }
 
+// Necessary condition for fit_array_model(a) on a long array seen through its first
+// elements `pre` (>= 258 of them) and a[n/2], a[n/2+1], a[n-2], a[n-1]: the same candidates,
+// patches counted on the prefix only (a lower bound of the full count).  false => no model
+// fits, so the caller can skip reading the whole array (device builds of 10^7-entry arrays).
+bool model_may_fit(const std::vector<int64_t>& pre, int64_t n, int64_t am0, int64_t am1, int64_t al0, int64_t al1,
+                   int budget) {
+  const int64_t np = (int64_t)pre.size();
+  if (np < 258 || np >= n) return true;
+  budget = std::min(budget, kMaxPatches);
+  std::vector<std::array<int64_t, 4>> cands;  // b, k1, k2, w
+  cands.push_back({pre[0] - (pre[1] - pre[0]) * 0, pre[1] - pre[0], 0, 1});
+  const int64_t jm = n / 2;
+  cands.push_back({am0 - (am1 - am0) * jm, am1 - am0, 0, 1});
+  cands.push_back({al0 - (al1 - al0) * (n - 2), al1 - al0, 0, 1});
+  for (int64_t w = 2; w <= 256 && w < n; w *= 2) cands.push_back({pre[0], pre[w] - pre[0], pre[1] - pre[0], w});
+  int64_t run = 1;
+  while (run < np && pre[run] == pre[0]) ++run;
+  if (run == np) return true;  // the step candidate needs more of the array
+  cands.push_back({pre[0], pre[run] - pre[0], 0, run});
+  for (auto& c : cands)
+    if (count_patches(pre, c[0], c[1], c[2], c[3], budget, nullptr) >= 0) return true;
+  return false;
+}
+
 }  // namespace as
 
 using namespace as;
@@ -85,6 +110,10 @@ as_status_t as_fit_array_model(const int64_t* a, size_t n, int budget, int64_t* 
     if ((n && !a) || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
     if (budget < 0 || budget > kMaxPatches) fail(AS_ERR_INVALID_ARG, "budget must be in [0, 8]");
     IdxModel m;
+    // the device build's shortcut: a prefix probe rejects most non-model arrays (model_may_fit)
+    if (n > 8192 && !model_may_fit(std::vector<int64_t>(a, a + 4096), (int64_t)n, a[n / 2], a[n / 2 + 1], a[n - 2],
+                                   a[n - 1], budget))
+      fail(AS_ERR_NOT_FOUND, "no model within the patch budget");
     if (!fit_array_model(std::vector<int64_t>(a, a + n), budget, &m)) fail(AS_ERR_NOT_FOUND, "no model within the patch budget");
     out[0] = m.kind;
     out[1] = m.b;

@@ -99,6 +99,36 @@ def test_abi_matches_oracle(k):
         assert got == ref, (k, budget, got, ref)
 
 
+def _long_cases():
+    """Arrays above 8192 entries, where the C-ABI (as the device build) first probes the
+    first 4096 entries and the mid / last pairs (model_may_fit) before reading the rest:
+    patches beyond the prefix, near the middle and at the end; a step longer than the probe;
+    periodic; random and cumulative arrays."""
+    g = np.random.default_rng(23)
+    out = []
+    for n in (9000, 20000, 33000):
+        i = np.arange(n, dtype=np.int64)
+        lin = 11 + 4 * i
+        for pos in ([5000], [n // 2], [n // 2 + 1], [n - 1], [n - 2], [100, 7000, n - 1], list(range(4090, 4099))):
+            a = lin.copy()
+            for j in pos:
+                a[j] += 7
+            out.append(a)
+        out.append(3 + 6 * (i // 5000))        # step wider than the probe
+        out.append(3 + 6 * (i // 700))         # step inside the probe
+        out.append(5 + 100 * (i // 64) + 2 * (i % 64))
+        out.append(g.integers(0, 2**31, n))
+        out.append(np.cumsum(g.integers(0, 3, n)))
+    return out
+
+
+@pytest.mark.parametrize("k", range(36))
+def test_abi_matches_oracle_long(k):
+    a = _long_cases()[k]
+    for budget in (0, 3, 8):
+        assert asp.fit_array_model(a, budget) == M.fit_array_model(a, budget), (k, budget)
+
+
 # ------------------------------------------------------------------ GPU: compressed plans
 def _gpu():
     torch = pytest.importorskip("torch")
