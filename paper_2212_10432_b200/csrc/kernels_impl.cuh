@@ -135,9 +135,12 @@ __global__ void __launch_bounds__(1024) k_thread_row_pad(DevPart p, const V* __r
 #ifndef AS_KBW_F32
 #define AS_KBW_F32 8
 #endif
+#ifndef AS_KBW_F64
+#define AS_KBW_F64 4
+#endif
 template <class V>
 constexpr int kbw_of() {
-  return sizeof(V) == 4 ? AS_KBW_F32 : 4;
+  return sizeof(V) == 4 ? AS_KBW_F32 : AS_KBW_F64;
 }
 
 template <class V>
