@@ -189,13 +189,22 @@ def reference_arm(args, coo, wl):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(coo, wl, budget_s=10.0):
+def cpu_baseline(coo, wl, budget_s=10.0, y_gpu=None):
+    """The oracle timed on the host cores; its first pass also checks the timed GPU y of the
+    same (A, x) row by row (north_star tolerance O2), at full size."""
     from oracle import spmv as S
     rp = csr_of(coo)
     x, _ = synth.vectors(coo.n, coo.m, 2, coo.val.dtype)
     cores = os.cpu_count() or 1
     col, val = coo.col, coo.val.astype(np.float64)
-    S.spmv_csr(rp, col, val, x, nthreads=cores)
+    yref, bound = S.spmv_csr(rp, col, val, x.astype(np.float64), nthreads=cores)
+    parity = None
+    if y_gpu is not None:
+        ok, ratio = S.check(y_gpu, yref, bound, coo.val.dtype)
+        parity = {"rows_checked": int(coo.m), "max_err_over_bound": float(ratio), "ok": bool(ok),
+                  "tol": 1e-12 if coo.val.dtype == np.float64 else 1e-5,
+                  "what": "every row of the last timed y vs the long-double oracle, |y - yref| <= tol * sum|a_ij x_j|"}
+    del yref, bound
     n, t_tot = 0, 0.0
     while t_tot < budget_s and n < 5000:
         t0 = time.perf_counter()
@@ -218,6 +227,7 @@ def cpu_baseline(coo, wl, budget_s=10.0):
         pass
     import platform
     return {"value": 2.0 * coo.nnz * n / t_tot / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "parity": parity,
             "sample": f"{n} full passes over {wl} ({coo.nnz} nnz), long double, {cores} threads, {t_tot:.1f} s",
             "value_1thread": 2.0 * nz1 / t1 / 1e9, "sample_1thread": f"first {r1} rows ({nz1} nnz)", "cpu": cpu,
             "long_double": "x87 80-bit extended" if platform.machine() in ("x86_64", "AMD64") else platform.machine()}
@@ -352,7 +362,7 @@ def run_config(args, torch, asp, name, A, coo, wl, seeds, graph, search, local, 
     if os.path.exists(prof):
         try:
             tj = json.load(open(prof))
-            if tj.get("kernels") == info["kernels"]:
+            if tj.get("kernels") == info["kernels"] and tj.get("graph", graph) == graph:
                 r["roofline"]["traffic"] = tj["dram_bytes_per_launch"]
                 r["roofline"]["traffic_src"] = tj.get("src")
         except Exception:
@@ -428,7 +438,9 @@ def single_gpu(args, torch, asp):
         except Exception as e:  # the measurement tool is optional; the SpMV numbers stand
             gr = {"error": str(e)[:200]}
     head["roofline"]["gather"] = gr
-    cpu = None if args.no_cpu_baseline else cpu_baseline(coo, wl)
+    y_gpu = dy.cpu().numpy()  # y of the last timed step (alpha 1, beta 0): checked by the oracle leg
+    cpu = None if args.no_cpu_baseline else cpu_baseline(coo, wl, y_gpu=y_gpu)
+    del y_gpu
     launches = head["launches"] * args.steps
     del P, dx, dy, A, coo
     torch.cuda.empty_cache()

@@ -103,6 +103,19 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
     P->canon = canon;
     P->device = device;
     P->stream = stream;
+    if (device >= 0) {
+      // A/B knob: L2 set-aside for persisting lines (the x gathers carry an evict_last
+      // policy; without a set-aside the L2 may treat them as normal lines)
+      static const char* sa = std::getenv("AS_L2_SETASIDE");
+      if (sa) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)std::atoll(sa));
+        cudaGetLastError();
+        cudaSetDevice(cur);
+      }
+    }
     DevSpec spec;
     if (device >= 0 && dev_build_spec(g, A, flags, &spec)) {
       // on-device Designer (devbuild.cu): the format is built on the GPU from the cached
