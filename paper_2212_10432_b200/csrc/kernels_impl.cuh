@@ -354,14 +354,37 @@ __device__ __forceinline__ void batch_load(const V* pv, const int32_t* pc, int64
 }
 
 // ... and their use: x gathers, then the branch-free bitmap-segmented accumulation.
+// Scheduling knobs of the predicated-emit scan (A/B builds): AS_PE_BM_ONCE loads a BMT's
+// first two bitmap words once (k <= 64: every batch's word) instead of once per batch;
+// AS_PE_PREFETCH issues the next batch's value / column loads before the current batch's
+// gathers and accumulation (one batch of look-ahead).
+#ifndef AS_PE_BM_ONCE
+#define AS_PE_BM_ONCE 0
+#endif
+#ifndef AS_PE_PREFETCH
+#define AS_PE_PREFETCH 0
+#endif
+struct BmWords {
+  const uint32_t* bm;
+  uint32_t w0, w1;
+  __device__ __forceinline__ uint32_t at(int j0) const {
+    if constexpr (AS_PE_BM_ONCE) {
+      const int w = j0 >> 5;
+      return w == 0 ? w0 : w == 1 ? w1 : ldm(bm + w);
+    } else {
+      return ldm(bm + (j0 >> 5));
+    }
+  }
+};
+
 template <class V, int KB, int EM, bool FULL, class XA>
-__device__ __forceinline__ void batch_use(const DevPart& p, V* y, XA xa, const uint32_t* bm, int j0, int len,
+__device__ __forceinline__ void batch_use(const DevPart& p, V* y, XA xa, const BmWords& bm, int j0, int len,
                                           const V* v, const int32_t* c, int32_t& row, double& acc, bool& inside,
                                           double& first) {
   V xv[KB];
 #pragma unroll
   for (int q = 0; q < KB; ++q) xv[q] = (FULL || j0 + q < len) ? xa.v(c[q]) : (V)0;
-  const uint32_t wd = (ldm(bm + (j0 >> 5)) >> (j0 & 31)) & ~(uint32_t)(j0 == 0);
+  const uint32_t wd = (bm.at(j0) >> (j0 & 31)) & ~(uint32_t)(j0 == 0);
 #pragma unroll
   for (int q = 0; q < KB; ++q) {
     const bool h = (FULL || j0 + q < len) && ((wd >> q) & 1u);
@@ -388,21 +411,48 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   const int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
   const int64_t e = p.bmt_start ? ldm(p.bmt_start + t + 1) : min(a + p.k, p.nnz_p);
   const int len = (int)(e - a);
-  const uint32_t* bm = bmt_bits(p, t);
+  const uint32_t* bmp = bmt_bits(p, t);
   const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;  // batch base
   const int32_t* pc = PAD ? p.pad_col + pp.base : p.col + a;
-  ScanPE o;
-  o.s0 = ldm(bm) & 1u;
-  o.inside = o.s0;
-  o.row = (int32_t)bmt_row0(p, t);  // device row indices are int32 (A36)
-  o.acc = 0.0;
-  o.first = 0.0;
   const int full = len & ~(KB - 1);
   int j0 = 0;
   // pv / pc advance to the batch's first element (slot-major: KB/VEC chunk rows per batch)
   const int64_t adv = PAD ? (KB / VEC) * pp.stride : KB;
   V v[KB];
   int32_t c[KB];
+#if AS_PE_PREFETCH
+  if (full > 0) batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, 0, len, v, c);
+  else if (len > 0) batch_load<V, PAD, VEC, KB, false>(pv, pc, pp.stride, 0, len, v, c);
+#endif
+  BmWords bm{bmp, 0u, 0u};
+  if constexpr (AS_PE_BM_ONCE) {
+    bm.w0 = ldm(bmp);
+    bm.w1 = p.bm_words > 1 ? ldm(bmp + 1) : 0u;
+  }
+  ScanPE o;
+  o.s0 = (AS_PE_BM_ONCE ? bm.w0 : ldm(bmp)) & 1u;
+  o.inside = o.s0;
+  o.row = (int32_t)bmt_row0(p, t);  // device row indices are int32 (A36)
+  o.acc = 0.0;
+  o.first = 0.0;
+#if AS_PE_PREFETCH
+  for (; j0 < full; j0 += KB) {
+    pv += adv;
+    pc += adv;
+    V vn[KB];
+    int32_t cn[KB];
+    const int jn = j0 + KB;
+    if (jn < full) batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, jn, len, vn, cn);
+    else if (jn < len) batch_load<V, PAD, VEC, KB, false>(pv, pc, pp.stride, jn, len, vn, cn);
+    batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      v[q] = vn[q];
+      c[q] = cn[q];
+    }
+  }
+  if (j0 < len) batch_use<V, KB, EM, false>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
+#else
   for (; j0 < full; j0 += KB, pv += adv, pc += adv) {
     batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, j0, len, v, c);
     batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
@@ -411,6 +461,7 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
     batch_load<V, PAD, VEC, KB, false>(pv, pc, pp.stride, j0, len, v, c);
     batch_use<V, KB, EM, false>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
   }
+#endif
   return o;
 }
 
