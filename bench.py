@@ -404,11 +404,28 @@ def e2e_of(args, torch, asp, P, A, coo, graph, local, timer):
             P_e.spmv_host(1.0, xn, 0.0, yn, timer.stream)
         ms = timer.steps(lambda: P_e.spmv_host(1.0, xn, 0.0, yn, timer.stream), max(3, args.steps // 3))
         res.append((statistics.median(ms), g_e, int(P_e.info()["n_launches"])))
-    tm, g_e, l_e = min(res)
+    names = ["searched", "pipelined"][:len(res)]
+    # a batch of K steps through as_spmv_host_batch: step i+1's x goes up and step i-1's y
+    # comes down while SpMV i runs (every step still copies its x up and its y back); timed
+    # as one event window over the K steps, L2 flushed before it
+    K = max(4, args.steps // 2)
+    try:
+        ys = [torch.zeros_like(yh).pin_memory().numpy() for _ in range(K)]
+        xs = [xn] * K
+        P.spmv_host_batch(1.0, xs[:2], 0.0, ys[:2], timer.stream)
+        bms = [t / K for t in timer.steps(lambda: P.spmv_host_batch(1.0, xs, 0.0, ys, timer.stream), 3)]
+        res.append((statistics.median(bms), graph, int(P.info()["n_launches"])))
+        names.append(f"batch{K}")
+        del ys
+    except Exception as e:  # the per-call numbers stand
+        names.append(f"batch_error: {str(e)[:120]}")
+    best = min(range(len(res)), key=lambda i: res[i][0])
+    tm, g_e, l_e = res[best]
     sv = xn.itemsize
     return {"value": 2.0 * coo.nnz / (tm * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": tm,
             "h2d_bytes_per_step": int(coo.n * sv), "d2h_bytes_per_step": int(coo.m * sv), "graph": g_e,
-            "launches_per_step": l_e, "candidates_ms": {("pipelined" if i else "searched"): r[0] for i, r in enumerate(res)}}
+            "launches_per_step": l_e, "how": names[best],
+            "candidates_ms": {names[i]: r[0] for i, r in enumerate(res)}}
 
 
 def single_gpu(args, torch, asp):

@@ -164,6 +164,13 @@ as_status_t as_spmv(as_plan_t, const void* alpha, const void* x, const void* bet
  * result is identical either way (same kernels, same order on the device). */
 as_status_t as_spmv_host(as_plan_t, const void* alpha, const void* x_host, const void* beta,
                          void* y_host, void* stream);
+/* k independent SpMVs y_i = alpha*A*x_i + beta*y_i on host buffers (pinned for overlap),
+ * pipelined across i: x_{i+1} is copied up while SpMV i runs and y_{i-1} is copied down
+ * (two device buffer pairs, two copy streams); every x_i goes up and every y_i comes back.
+ * Blocking; the steady state per SpMV is max(H2D x, kernels, D2H y).  Same errors as
+ * as_spmv_host. */
+as_status_t as_spmv_host_batch(as_plan_t, int64_t k, const void* alpha, const void* const* x_host,
+                               const void* beta, void* const* y_host, void* stream);
 
 /* SpMM (NEXT-4): Y = alpha*A*X + beta*Y with k right-hand sides.  X[n x k] and Y[m x k]
  * are row-major device arrays of the plan's dtype with leading dimensions ldx, ldy >= k;

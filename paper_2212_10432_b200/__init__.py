@@ -92,6 +92,7 @@ _sig("as_spmm", [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp])
 _sig("as_plan_profile", [_vp, _vp, _vp, _i32, _vp, _vp, _vp, _P(_sz)])
 _sig("as_search", [_vp, _P(AsSearchCfg), _i32, _vp, _P(_vp), ctypes.c_char_p, _P(_sz)])
 _sig("as_random_graph", [_vp, ctypes.c_uint64, ctypes.c_char_p, _P(_sz)])
+_sig("as_spmv_host_batch", [_vp, _i64, _vp, _vp, _vp, _vp, _vp])
 _sig("as_graph_device_buildable", [_vp, _vp, _i32, _P(_i32)])
 _sig("as_graph_features", [_vp, _vp, _P(_sz)])
 _sig("as_fit_array_model", [_vp, _sz, _i32, _vp])
@@ -119,7 +120,7 @@ EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create
             "as_dist_row_cuts", "as_dist_row_cuts_ptr", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
             "as_dist_set_cuts", "as_dist_ipc_handle", "as_dist_open_peers", "as_spmv_dist", "as_dist_check",
             "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows", "as_fit_array_model", "as_spmm", "as_plan_profile",
-            "as_graph_device_buildable"]
+            "as_graph_device_buildable", "as_spmv_host_batch"]
 
 
 class AsError(RuntimeError):
@@ -401,6 +402,21 @@ class Plan:
         a, b = self._scalars(alpha, beta)
         _ck(_lib.as_spmv_host(self._h, ctypes.byref(a), x.ctypes.data, ctypes.byref(b), y.ctypes.data,
                               _stream_handle(stream)))
+
+    def spmv_host_batch(self, alpha, xs, beta, ys, stream=None):
+        """as_spmv_host_batch: y_i = alpha*A*x_i + beta*y_i for host arrays xs[i], ys[i], the
+        copies of consecutive SpMVs overlapped with the kernels (blocking)."""
+        if len(xs) != len(ys):
+            raise AsError(1, "xs and ys differ in length")
+        for x in xs:
+            self._check_host(x, self.n, "x")
+        for y in ys:
+            self._check_host(y, self.m, "y", writable=True)
+        a, b = self._scalars(alpha, beta)
+        k = len(xs)
+        xp = (ctypes.c_void_p * max(k, 1))(*[x.ctypes.data for x in xs])
+        yp = (ctypes.c_void_p * max(k, 1))(*[y.ctypes.data for y in ys])
+        _ck(_lib.as_spmv_host_batch(self._h, k, ctypes.byref(a), xp, ctypes.byref(b), yp, _stream_handle(stream)))
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib:

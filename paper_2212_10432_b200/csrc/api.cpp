@@ -590,6 +590,81 @@ as_status_t as_spmv_host(as_plan_t h, const void* alpha, const void* x_host, con
   });
 }
 
+// k independent host-buffer SpMVs, pipelined across them: x_{i+1} goes up on a copy stream
+// while SpMV i runs and y_{i-1} comes down on another (PCIe is full duplex), with two device
+// buffer pairs; every x_i is copied up and every y_i copied back.  Steady state per SpMV =
+// max(H2D x, kernels, D2H y) instead of their sum.
+as_status_t as_spmv_host_batch(as_plan_t h, int64_t k, const void* alpha, const void* const* x_host,
+                               const void* beta, void* const* y_host, void* stream) {
+  return guard([&] {
+    NvtxRange nv("as_spmv_host_batch");
+    if (!h || !alpha || !beta || (k > 0 && (!x_host || !y_host))) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    if (k < 0) fail(AS_ERR_INVALID_ARG, "k < 0");
+    Plan& P = *h->P;
+    if (P.device < 0) fail(AS_ERR_INVALID_ARG, "host-only plan");
+    for (int64_t i = 0; i < k; ++i)
+      if ((P.n > 0 && !x_host[i]) || (P.m > 0 && !y_host[i])) fail(AS_ERR_INVALID_ARG, "NULL x or y");
+    const size_t sv = P.dt == AS_R64F ? 8 : 4;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    cudaSetDevice(P.device);
+    void** bx[2] = {&P.d_x, &P.d_x1};
+    void** by[2] = {&P.d_y, &P.d_y1};
+    for (int j = 0; j < 2; ++j) {
+      if (!*bx[j]) *bx[j] = dev_alloc(std::max<size_t>(16, P.n * sv), P.stream);
+      if (!*by[j]) *by[j] = dev_alloc(std::max<size_t>(16, P.m * sv), P.stream);
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const double a = P.dt == AS_R64F ? *(const double*)alpha : (double)*(const float*)alpha;
+    const double b = P.dt == AS_R64F ? *(const double*)beta : (double)*(const float*)beta;
+    cudaError_t prior = cudaGetLastError();
+    if (prior != cudaSuccess) fail(AS_ERR_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(prior));
+    if (!P.s_h2d) {
+      check_cuda(cudaStreamCreateWithFlags(&P.s_h2d, cudaStreamNonBlocking), "copy stream");
+      check_cuda(cudaStreamCreateWithFlags(&P.s_d2h, cudaStreamNonBlocking), "copy stream");
+    }
+    size_t ev = 0;
+    auto mark = [&](cudaStream_t on) {
+      cudaEvent_t e = P.host_event(ev++);
+      check_cuda(cudaEventRecord(e, on), "event");
+      return e;
+    };
+    // the copy streams start after everything already queued on s
+    cudaEvent_t start = mark(s);
+    check_cuda(cudaStreamWaitEvent(P.s_h2d, start, 0), "wait");
+    check_cuda(cudaStreamWaitEvent(P.s_d2h, start, 0), "wait");
+    std::vector<cudaEvent_t> computed((size_t)k), drained((size_t)k);
+    int err = 0;
+    for (int64_t i = 0; i < k && !err; ++i) {
+      const int j = (int)(i & 1);
+      char* dx = (char*)*bx[j];
+      char* dy = (char*)*by[j];
+      // buffer pair j is free once SpMV i-2 finished reading x and its y came down
+      if (i >= 2) {
+        check_cuda(cudaStreamWaitEvent(P.s_h2d, computed[(size_t)i - 2], 0), "wait");
+        check_cuda(cudaStreamWaitEvent(P.s_h2d, drained[(size_t)i - 2], 0), "wait");
+      }
+      check_cuda(cudaMemcpyAsync(dx, x_host[i], P.n * sv, cudaMemcpyHostToDevice, P.s_h2d), "H2D x");
+      if (b != 0.0) check_cuda(cudaMemcpyAsync(dy, y_host[i], P.m * sv, cudaMemcpyHostToDevice, P.s_h2d), "H2D y");
+      check_cuda(cudaStreamWaitEvent(s, mark(P.s_h2d), 0), "wait");
+      err = run_plan(P, dx, dy, a, b, s, [](size_t) {}, [](size_t) {});
+      if (err) break;
+      computed[(size_t)i] = mark(s);
+      check_cuda(cudaStreamWaitEvent(P.s_d2h, computed[(size_t)i], 0), "wait");
+      check_cuda(cudaMemcpyAsync(y_host[i], dy, P.m * sv, cudaMemcpyDeviceToHost, P.s_d2h), "D2H y");
+      drained[(size_t)i] = mark(P.s_d2h);
+    }
+    check_cuda(cudaStreamWaitEvent(s, mark(P.s_d2h), 0), "wait");
+    check_cuda(cudaStreamWaitEvent(s, mark(P.s_h2d), 0), "wait");
+    if (err) {
+      cudaSetDevice(cur);
+      fail(AS_ERR_CUDA, std::string("launch: ") + cudaGetErrorString((cudaError_t)err));
+    }
+    check_cuda(cudaStreamSynchronize(s), "sync");
+    cudaSetDevice(cur);
+  });
+}
+
 as_status_t as_plan_profile(as_plan_t h, const void* x, void* y, int reps, void* stream, double* ms, double* bytes,
                             size_t* n) {
   return guard([&] {

@@ -287,6 +287,8 @@ Plan::~Plan() {
     for (void* p : allocs) dev_free(p, stream);
     if (d_x) dev_free(d_x, stream);
     if (d_y) dev_free(d_y, stream);
+    if (d_x1) dev_free(d_x1, stream);
+    if (d_y1) dev_free(d_y1, stream);
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (gexec) cudaGraphExecDestroy(gexec);

@@ -23,6 +23,8 @@ struct Plan {
   as_plan_info_t info{};
   void* d_x = nullptr;           // scratch for as_spmv_host
   void* d_y = nullptr;
+  void* d_x1 = nullptr;          // second buffer pair of as_spmv_host_batch
+  void* d_y1 = nullptr;
   // per launch: x columns read [clo, chi] and global y rows written [rlo, rhi] (supersets;
   // empty = clo > chi).  as_spmv_host pipelines chunked copies against launches with them.
   struct Span {

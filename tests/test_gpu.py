@@ -411,3 +411,28 @@ def test_smem_optin_not_lowered_by_later_plans():
     Q_small = asp.Plan(_mat(coo), cs_small, device=0)
     run_check(coo, cs_big, 1.0, 0.0, int_mode=True, seed=2, plan=Q_big)
     run_check(coo, cs_small, 1.0, 0.0, int_mode=True, seed=2, plan=Q_small)
+
+
+@pytest.mark.parametrize("graph", [
+    "COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; SET_RESOURCE(stages=0); GMEM_ATOM_RED",
+    "ROW_DIV(cuts=[700,1500]) { COMPRESS; BMW_NNZ_BLOCK(64); BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; "
+    "GMEM_ATOM_RED }",
+])
+@pytest.mark.parametrize("beta", [0.0, -1.0])
+def test_spmv_host_batch(graph, beta):
+    """as_spmv_host_batch: k independent host-buffer SpMVs pipelined over two device buffer
+    pairs; every y_i equals the oracle's (integer-exact: bit-identical), including k = 1, 2
+    and odd k (buffer reuse across the pair)."""
+    coo = synth.random_powerlaw(2500, 2300, 8, 700, int_mode=True)
+    P = asp.Plan(_mat(coo), graph, device=0)
+    for k in (1, 2, 5):
+        xs, ys, refs = [], [], []
+        for i in range(k):
+            x, y0 = synth.vectors(coo.n, coo.m, 40 + i, np.float64, True)
+            yref, _ = S.spmv_coo(coo.m, coo.row, coo.col, coo.val, x, 2.0, beta, y0)
+            xs.append(torch.from_numpy(x).pin_memory().numpy())
+            ys.append(torch.from_numpy(y0.copy()).pin_memory().numpy())
+            refs.append(yref)
+        P.spmv_host_batch(2.0, xs, beta, ys)
+        for i in range(k):
+            assert np.array_equal(ys[i], refs[i].astype(np.float64)), (graph, k, i)
