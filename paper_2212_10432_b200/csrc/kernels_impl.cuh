@@ -354,21 +354,17 @@ __device__ __forceinline__ void batch_load(const V* pv, const int32_t* pc, int64
 }
 
 // ... and their use: x gathers, then the branch-free bitmap-segmented accumulation.
-// Scheduling knobs of the predicated-emit scan (A/B builds): AS_PE_BM_ONCE loads a BMT's
-// first two bitmap words once (k <= 64: every batch's word) instead of once per batch;
-// AS_PE_PREFETCH issues the next batch's value / column loads before the current batch's
-// gathers and accumulation (one batch of look-ahead).
-#ifndef AS_PE_BM_ONCE
-#define AS_PE_BM_ONCE 0
-#endif
-#ifndef AS_PE_PREFETCH
-#define AS_PE_PREFETCH 0
-#endif
+// Bitmap words of one BMT.  BMO: the first two words are loaded once per BMT (k <= 64: every
+// batch's word) instead of once per batch -- the thread-level kernel gains (C5 2632 -> 2468
+// us), the register-bound warp-level kernel loses (C3 886 -> 904 us), so it is a template
+// choice of the kernel (profiles/r02/ab_pe.jsonl; a one-batch load prefetch spilled and lost
+// everywhere: C3 1277, C5 6459 us).
+template <bool BMO>
 struct BmWords {
   const uint32_t* bm;
   uint32_t w0, w1;
   __device__ __forceinline__ uint32_t at(int j0) const {
-    if constexpr (AS_PE_BM_ONCE) {
+    if constexpr (BMO) {
       const int w = j0 >> 5;
       return w == 0 ? w0 : w == 1 ? w1 : ldm(bm + w);
     } else {
@@ -377,8 +373,8 @@ struct BmWords {
   }
 };
 
-template <class V, int KB, int EM, bool FULL, class XA>
-__device__ __forceinline__ void batch_use(const DevPart& p, V* y, XA xa, const BmWords& bm, int j0, int len,
+template <class V, int KB, int EM, bool FULL, class XA, class BW>
+__device__ __forceinline__ void batch_use(const DevPart& p, V* y, XA xa, const BW& bm, int j0, int len,
                                           const V* v, const int32_t* c, int32_t& row, double& acc, bool& inside,
                                           double& first) {
   V xv[KB];
@@ -405,7 +401,7 @@ struct ScanPE {
   int32_t row;
   bool s0, inside;
 };
-template <class V, bool PAD, int VEC, int KB, int EM, class XA>
+template <class V, bool PAD, int VEC, int KB, int EM, bool BMO, class XA>
 __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int64_t t, PadPos pp) {
   static_assert(32 % KB == 0 && KB % VEC == 0, "KB divides 32 and is a multiple of VEC");
   const int64_t a = p.bmt_start ? ldm(p.bmt_start + t) : t * p.k;
@@ -414,45 +410,23 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   const uint32_t* bmp = bmt_bits(p, t);
   const V* pv = PAD ? (const V*)p.pad_val + pp.base : (const V*)p.val + a;  // batch base
   const int32_t* pc = PAD ? p.pad_col + pp.base : p.col + a;
+  BmWords<BMO> bm{bmp, 0u, 0u};
+  if constexpr (BMO) {
+    bm.w0 = ldm(bmp);
+    bm.w1 = p.bm_words > 1 ? ldm(bmp + 1) : 0u;
+  }
+  ScanPE o;
+  o.s0 = (BMO ? bm.w0 : ldm(bmp)) & 1u;
+  o.inside = o.s0;
+  o.row = (int32_t)bmt_row0(p, t);  // device row indices are int32 (A36)
+  o.acc = 0.0;
+  o.first = 0.0;
   const int full = len & ~(KB - 1);
   int j0 = 0;
   // pv / pc advance to the batch's first element (slot-major: KB/VEC chunk rows per batch)
   const int64_t adv = PAD ? (KB / VEC) * pp.stride : KB;
   V v[KB];
   int32_t c[KB];
-#if AS_PE_PREFETCH
-  if (full > 0) batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, 0, len, v, c);
-  else if (len > 0) batch_load<V, PAD, VEC, KB, false>(pv, pc, pp.stride, 0, len, v, c);
-#endif
-  BmWords bm{bmp, 0u, 0u};
-  if constexpr (AS_PE_BM_ONCE) {
-    bm.w0 = ldm(bmp);
-    bm.w1 = p.bm_words > 1 ? ldm(bmp + 1) : 0u;
-  }
-  ScanPE o;
-  o.s0 = (AS_PE_BM_ONCE ? bm.w0 : ldm(bmp)) & 1u;
-  o.inside = o.s0;
-  o.row = (int32_t)bmt_row0(p, t);  // device row indices are int32 (A36)
-  o.acc = 0.0;
-  o.first = 0.0;
-#if AS_PE_PREFETCH
-  for (; j0 < full; j0 += KB) {
-    pv += adv;
-    pc += adv;
-    V vn[KB];
-    int32_t cn[KB];
-    const int jn = j0 + KB;
-    if (jn < full) batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, jn, len, vn, cn);
-    else if (jn < len) batch_load<V, PAD, VEC, KB, false>(pv, pc, pp.stride, jn, len, vn, cn);
-    batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
-#pragma unroll
-    for (int q = 0; q < KB; ++q) {
-      v[q] = vn[q];
-      c[q] = cn[q];
-    }
-  }
-  if (j0 < len) batch_use<V, KB, EM, false>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
-#else
   for (; j0 < full; j0 += KB, pv += adv, pc += adv) {
     batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, j0, len, v, c);
     batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
@@ -461,7 +435,6 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
     batch_load<V, PAD, VEC, KB, false>(pv, pc, pp.stride, j0, len, v, c);
     batch_use<V, KB, EM, false>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
   }
-#endif
   return o;
 }
 
@@ -470,7 +443,7 @@ template <class V, bool PAD, int VEC, int KB, int EM, class XA>
 __device__ __forceinline__ void nnz_thread_bmt_pe(const DevPart& p, XA xa, V* __restrict__ y, int64_t t) {
   PadPos pp{0, 0};
   if constexpr (PAD) pp = p.n_grp == 1 ? PadPos{t * VEC, p.n_bmt * VEC} : pad_pos<VEC>(p, t);
-  const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM>(p, y, xa, t, pp);
+  const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM, true>(p, y, xa, t, pp);
   // first segment closed inside the BMT but begun before it: straddler
   if (!o.s0 && o.inside) write_atom(p, y, bmt_row0(p, t), o.first);
   // open last segment: exclusive iff it began at a head here and the next BMT starts a row
@@ -774,7 +747,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __rest
           else if (p.n_grp == 1) pp = PadPos{t * VEC, p.n_bmt * VEC};
           else pp = pad_pos<VEC>(p, t);
         }
-        const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM>(p, y, xa, t, pp);
+        const ScanPE o = bmt_scan_pe<V, PAD, VEC, KB, EM, false>(p, y, xa, t, pp);
         b0 = o.s0;
         hh = o.inside;
         const int64_t row0 = bmt_row0(p, t);
