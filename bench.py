@@ -362,7 +362,8 @@ def run_config(args, torch, asp, name, A, coo, wl, seeds, graph, search, local, 
     if os.path.exists(prof):
         try:
             tj = json.load(open(prof))
-            if tj.get("kernels") == info["kernels"] and tj.get("graph", graph) == graph:
+            same = tj.get("graph", graph) == graph or ("bytes_model" in tj and tj["bytes_model"] == info["bytes_model"])
+            if tj.get("kernels") == info["kernels"] and same:
                 r["roofline"]["traffic"] = tj["dram_bytes_per_launch"]
                 r["roofline"]["traffic_src"] = tj.get("src")
         except Exception:
