@@ -132,3 +132,75 @@ def test_device_build_real_values_and_cache_reuse():
         torch.cuda.synchronize()
         ok, ratio = S.check(dy.cpu().numpy(), yref, bound, np.float32)
         assert ok, ratio
+
+
+def _random_dev_graph(rng):
+    """A random graph of the on-device Designer's family."""
+    parts = []
+    r = rng.integers(0, 3)
+    if r == 1:
+        parts.append("SORT")
+    elif r == 2:
+        parts.append(f"SORT_SUB(g={int(rng.choice([2, 5, 64, 1000]))})")
+    parts.append("COMPRESS")
+    k = int(rng.choice([1, 3, 4, 8, 13, 32, 40, 64, 100]))
+    K = int(rng.choice([0, 5, 32, 96, 100, 256, 1000])) if rng.random() < 0.7 else 0
+    if K:
+        parts.append(f"BMW_NNZ_BLOCK({K})")
+    parts.append(f"BMT_NNZ_BLOCK({k})")
+    if rng.random() < 0.6:
+        scope = "BMW" if K and rng.random() < 0.5 else "GLOBAL"
+        parts.append(f"BMT_PAD({scope},{int(rng.choice([0, 1, 2, 4]))})")
+    parts.append("THREAD_BITMAP_RED_G")
+    if K:
+        parts.append(str(rng.choice(["WARP_SEG_ADD_RED", "WARP_BITMAP_RED"])))
+    xc = int(rng.choice([0, 0, 17, 500]))
+    parts.append(f"SET_RESOURCE(tpb={int(rng.choice([64, 256, 1024]))},grid={int(rng.choice([0, 1, 2]))},"
+                 f"stages=0,xcache={xc})")
+    parts.append("GMEM_ATOM_RED")
+    return "; ".join(parts)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_device_build_fuzz(seed):
+    """Random graphs of the family on random matrices: device-built arrays = oracle arrays,
+    y bit-identical in integer mode, and the host build reports the same plan."""
+    rng = np.random.default_rng(1000 + seed)
+    dt = np.float32 if seed % 2 else np.float64
+    coo = (synth.random_powerlaw(int(rng.integers(50, 3000)), int(rng.integers(40, 2500)), seed, 400, int_mode=True)
+           if seed % 3 else synth.random_matrix(int(rng.integers(20, 400)), int(rng.integers(20, 300)), 0.05, seed,
+                                                int_mode=True, dense_rows=1)).astype(dt)
+    if coo.row.shape[0] == 0:
+        return
+    A = _mat(coo)
+    for _ in range(3):
+        graph = _random_dev_graph(rng)
+        if not A.device_buildable(graph):  # the tile-kernel shapes stay on the host Designer
+            continue
+        try:
+            P = asp.Plan(A, graph, device=0)
+        except asp.AsError as e:
+            H = None
+            try:
+                H = asp.Plan(A, graph, device=0, host_build=True)
+            except asp.AsError:
+                pass
+            assert H is None, (graph, str(e))  # infeasible for both Designers or neither
+            continue
+        assert P.info()["device_built"] == 1
+        csr = B.Csr(coo.m, coo.n, coo.row, coo.col, coo.val)
+        parts, w = B.build(csr, G.parse(graph), coo.val.dtype)
+        ref = B.export(parts, w)
+        for k in P.device_keys():
+            got, want = P.export(k), ref[k[len("dev."):]]
+            assert got.shape == want.shape and np.array_equal(got.astype(want.dtype), want), (graph, k)
+        x, y0 = synth.vectors(coo.n, coo.m, seed, dt, True)
+        dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y0.copy()).cuda()
+        P.spmv(-1.5, dx, 0.5, dy)
+        torch.cuda.synchronize()
+        yref, _ = S.spmv_coo(coo.m, coo.row, coo.col, coo.val.astype(np.float64), x.astype(np.float64), -1.5, 0.5,
+                             y0.astype(np.float64))
+        assert np.array_equal(dy.cpu().numpy().astype(np.float64), yref), graph
+        hi = asp.Plan(A, graph, device=0, host_build=True).info()
+        for key in ("kernels", "stored_slots", "prepass_rows", "bytes_model", "modeled_arrays"):
+            assert P.info()[key] == hi[key], (graph, key)
