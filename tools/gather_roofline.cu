@@ -206,6 +206,63 @@ __global__ void __launch_bounds__(1024) k_gather_async(const V* __restrict__ val
   if (acc == 1234.5678) out[0] = acc;
 }
 
+// mode 6: the hot-x copy distributed over a thread-block cluster of C CTAs (DSMEM): CTA r of
+// the cluster holds hot slots [r*Kl, (r+1)*Kl); a gather of hot slot s reads CTA s/Kl's
+// shared memory through mapa + ld.shared::cluster.  C times the hot set of one CTA at the same
+// shared-memory (and L1) footprint per SM.
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <class V>
+__device__ __forceinline__ double ld_dsm(const V* local_base, int64_t s, int kl) {
+  const unsigned owner = (unsigned)(s / kl), off = (unsigned)(s - (int64_t)owner * kl);
+  const unsigned a = smem_u32(local_base + off);
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(owner));
+  if constexpr (sizeof(V) == 4) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra));
+    return (double)v;
+  } else {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
+    return v;
+  }
+}
+template <class V>
+__global__ void __launch_bounds__(1024) k_gather_dsm(const V* __restrict__ val, const int32_t* __restrict__ col,
+                                                      const V* __restrict__ x, const V* __restrict__ xh, int kl,
+                                                      int64_t nnz, double* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  V* sh = (V*)smem;
+  const unsigned rk = cluster_rank();
+  for (int i = threadIdx.x; i < kl; i += blockDim.x) sh[i] = xh[(int64_t)rk * kl + i];
+  cluster_sync();
+  constexpr int W = Vec<V>::W;
+  const int64_t nv = nnz / W;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (UNR - 1) * T < nv; i += UNR * T) {
+    double v[UNR * W];
+    int32_t c[UNR * W];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) Vec<V>::ld(val + (i + u * T) * W, col + (i + u * T) * W, v + u * W, c + u * W);
+    double xv[UNR * W];
+#pragma unroll
+    for (int q = 0; q < UNR * W; ++q) xv[q] = c[q] < 0 ? ld_dsm(sh, ~c[q], kl) : ldx(x, c[q]);
+#pragma unroll
+    for (int q = 0; q < UNR * W; ++q) acc += v[q] * xv[q];
+  }
+  cluster_sync();  // no CTA leaves while a partner may still read its shared memory
+  if (acc == 1234.5678) out[0] = acc;
+}
+
 __device__ __forceinline__ uint32_t mix(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
@@ -274,6 +331,37 @@ int gr_launch_async(int dtype, int ch, const void* val, const int32_t* col, cons
     else LA(double, 16);
   }
 #undef LA
+  return (int)cudaGetLastError();
+}
+// cluster-distributed hot-x gathers (mode 6): csize CTAs per cluster, kl hot entries per CTA
+int gr_launch_dsm(int dtype, int csize, const void* val, const int32_t* col, const void* x, const void* xh, int kl,
+                  int64_t nnz, double* out, int grid, int tpb, void* stream) {
+  const size_t sm = (size_t)kl * (dtype ? 8 : 4);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)tpb);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (dtype == 0) {
+    cudaFuncSetAttribute(k_gather_dsm<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (csize > 8) cudaFuncSetAttribute(k_gather_dsm<float>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaLaunchKernelEx(&cfg, k_gather_dsm<float>, (const float*)val, col, (const float*)x, (const float*)xh, kl, nnz,
+                           out);
+  } else {
+    cudaFuncSetAttribute(k_gather_dsm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (csize > 8) cudaFuncSetAttribute(k_gather_dsm<double>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaLaunchKernelEx(&cfg, k_gather_dsm<double>, (const double*)val, col, (const double*)x, (const double*)xh,
+                           kl, nnz, out);
+  }
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }
 int gr_launch_hash(int dtype, const void* x, int64_t n, int64_t count, double* out, int grid, int tpb, void* stream) {

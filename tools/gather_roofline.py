@@ -38,6 +38,9 @@ def build():
     lib.gr_launch_async.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
                                     ctypes.c_int, ctypes.c_void_p]
+    lib.gr_launch_dsm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                  ctypes.c_int, ctypes.c_void_p]
     lib.gr_launch_hash.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                    ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
     return lib
@@ -83,6 +86,8 @@ def main():
     ap.add_argument("--configs", nargs="+", default=["c3", "c4"])
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--hot", nargs="+", type=int, default=[8192, 16384, 32768, 49152])
+    ap.add_argument("--dsm", action="store_true",
+                    help="also time the hot-x copy distributed over a thread-block cluster (DSMEM)")
     ap.add_argument("--async-gather", action="store_true",
                     help="also time cp.async-staged gathers (relabeled columns, hot prefix in smem)")
     ap.add_argument("--relabel", action="store_true",
@@ -137,6 +142,32 @@ def main():
                               "min_us": mn * 1e3, "model_gbs": model / (med * 1e-3) / 1e9,
                               "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
             del denc
+        if args.dsm:
+            for (csize, kl) in [(1, 24576), (2, 24576), (4, 24576), (8, 24576), (2, 16384), (4, 16384), (8, 16384),
+                                (16, 12288)]:
+                if kl * sv > 200 * 1024:
+                    continue
+                K = csize * kl
+                hot = order[:K]
+                slot = np.full(n, -1, np.int64)
+                slot[hot] = np.arange(K)
+                enc = np.where(slot[col] >= 0, ~slot[col], col).astype(np.int32)
+                denc = torch.from_numpy(enc).to(dev)
+                xh = x[torch.from_numpy(hot).to(dev)].contiguous()
+                cover = float(cnt[hot].sum()) / nnz
+
+                def rund():
+                    rc = lib.gr_launch_dsm(dt, csize, dval.data_ptr(), denc.data_ptr(), x.data_ptr(), xh.data_ptr(), kl,
+                                           nnz, out.data_ptr(), (nsm // csize) * csize, 1024, s)
+                    assert rc == 0, rc
+                try:
+                    med, mn = timeit(rund, args.reps, flush)
+                    print(json.dumps({**base, "kernel": f"dsm_c{csize}_kl{kl}", "hot_cover": cover,
+                                      "median_us": med * 1e3, "min_us": mn * 1e3,
+                                      "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
+                except AssertionError as e:
+                    print(json.dumps({**base, "kernel": f"dsm_c{csize}_kl{kl}", "error": str(e)}), flush=True)
+                del denc, xh
         if args.async_gather:
             rank = np.empty(n, np.int64)
             rank[order] = np.arange(n)
