@@ -208,7 +208,21 @@ typedef struct {
   const char* const* seed_graphs;
   int n_seed_graphs;
   const char* log_path;
+  /* Optional cost-model history from earlier searches (NEXT-3; the paper's model is trained
+   * on other matrices): n_history timed candidates, each a graph text, the
+   * AS_MATRIX_FEATURES features of its matrix (history_matrix[i*AS_MATRIX_FEATURES ...]) and
+   * log(median ms / nnz).  The model stage then fits graph + matrix features on the history
+   * and the candidates of this search together (target log time per nonzero). */
+  const char* const* history_graphs;
+  const double* history_matrix;
+  const double* history_log_t_per_nnz;
+  int n_history;
 } as_search_cfg_t;
+#define AS_MATRIX_FEATURES 8
+/* The matrix features of the search's cost model: log2(1+m), log2(1+n), log2(1+nnz), average
+ * row length, log2(1+row-length variance), log2(1+max row length), empty-row fraction, value
+ * size in bytes.  out holds AS_MATRIX_FEATURES doubles. */
+as_status_t as_matrix_features(as_matrix_t, double* out);
 as_status_t as_search(as_matrix_t, const as_search_cfg_t*, int device, void* stream,
                       as_plan_t* best, char* best_graph, size_t* len);
 /* Model-Driven Format Compression (§V-D): fit an index array a[n] (n >= 2) to

@@ -58,7 +58,10 @@ class AsPlanInfo(ctypes.Structure):
 class AsSearchCfg(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("max_candidates", ctypes.c_int), ("budget_seconds", ctypes.c_double),
                 ("warmup", ctypes.c_int), ("reps", ctypes.c_int), ("flush_l2", ctypes.c_int),
-                ("seed_graphs", _P(ctypes.c_char_p)), ("n_seed_graphs", ctypes.c_int), ("log_path", ctypes.c_char_p)]
+                ("seed_graphs", _P(ctypes.c_char_p)), ("n_seed_graphs", ctypes.c_int), ("log_path", ctypes.c_char_p),
+                ("history_graphs", _P(ctypes.c_char_p)), ("history_matrix", _P(ctypes.c_double)),
+                ("history_log_t_per_nnz", _P(ctypes.c_double)), ("n_history", ctypes.c_int)]
+AS_MATRIX_FEATURES = 8
 
 
 def _sig(name, args, res=ctypes.c_int):
@@ -94,6 +97,7 @@ _sig("as_search", [_vp, _P(AsSearchCfg), _i32, _vp, _P(_vp), ctypes.c_char_p, _P
 _sig("as_random_graph", [_vp, ctypes.c_uint64, ctypes.c_char_p, _P(_sz)])
 _sig("as_spmv_host_batch", [_vp, _i64, _vp, _vp, _vp, _vp, _vp])
 _sig("as_graph_device_buildable", [_vp, _vp, _i32, _P(_i32)])
+_sig("as_matrix_features", [_vp, _P(ctypes.c_double)])
 _sig("as_graph_features", [_vp, _vp, _P(_sz)])
 _sig("as_fit_array_model", [_vp, _sz, _i32, _vp])
 _sig("as_surrogate_fit_predict", [_vp, _vp, _sz, _sz, _vp, _sz, _vp])
@@ -120,7 +124,7 @@ EXPORTED = ["as_last_error", "as_version", "as_matrix_create", "as_matrix_create
             "as_dist_row_cuts", "as_dist_row_cuts_ptr", "as_matrix_col_span", "as_set_allocator", "as_dist_unique_id", "as_dist_init",
             "as_dist_set_cuts", "as_dist_ipc_handle", "as_dist_open_peers", "as_spmv_dist", "as_dist_check",
             "as_dist_destroy", "as_graph_features", "as_surrogate_fit_predict", "as_dist_set_windows", "as_fit_array_model", "as_spmm", "as_plan_profile",
-            "as_graph_device_buildable", "as_spmv_host_batch"]
+            "as_graph_device_buildable", "as_spmv_host_batch", "as_matrix_features"]
 
 
 class AsError(RuntimeError):
@@ -227,6 +231,12 @@ class Matrix:
 
     def random_graph(self, seed: int) -> str:
         return _string(_lib.as_random_graph, self._h, ctypes.c_uint64(seed))
+
+    def features(self) -> list:
+        """as_matrix_features: the cost model's AS_MATRIX_FEATURES matrix features."""
+        out = (ctypes.c_double * AS_MATRIX_FEATURES)()
+        _ck(_lib.as_matrix_features(self._h, out))
+        return list(out)
 
     def device_buildable(self, graph, host_build: bool = False) -> bool:
         """Whether as_plan builds `graph` with the on-device Designer (as_graph_device_buildable)."""
@@ -434,11 +444,17 @@ def row_cuts_from_ptr(row_ptr, world: int) -> np.ndarray:
 
 def search(matrix: Matrix, device: int = 0, stream=None, seed: int = 1, max_candidates: int = 32,
            budget_seconds: float = 30.0, warmup: int = 3, reps: int = 10, flush_l2: bool = True,
-           seed_graphs=(), log_path: str | None = None):
-    """a7: time random legal graphs on the device, keep the fastest -> (Plan, canonical graph)."""
+           seed_graphs=(), log_path: str | None = None, history=()):
+    """a7: time random legal graphs on the device, keep the fastest -> (Plan, canonical graph).
+    history: (graph text, matrix features, median ms, nnz) records of earlier searches for the
+    cost model (as_search_cfg_t.history_*)."""
     arr = (ctypes.c_char_p * max(1, len(seed_graphs)))(*[g.encode() for g in seed_graphs])
+    nh = len(history)
+    hg = (ctypes.c_char_p * max(1, nh))(*[h[0].encode() for h in history])
+    hm = (ctypes.c_double * max(1, nh * AS_MATRIX_FEATURES))(*[v for h in history for v in h[1]])
+    hy = (ctypes.c_double * max(1, nh))(*[float(np.log(h[2] / h[3])) for h in history])
     cfg = AsSearchCfg(seed, max_candidates, budget_seconds, warmup, reps, int(flush_l2), arr, len(seed_graphs),
-                      log_path.encode() if log_path else None)
+                      log_path.encode() if log_path else None, hg, hm, hy, nh)
     h = _vp()
     n = _sz(4096)
     buf = ctypes.create_string_buffer(4096)

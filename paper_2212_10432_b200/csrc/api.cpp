@@ -17,6 +17,7 @@ as_stats_t matrix_stats(const Matrix&);
 Matrix matrix_row_slice(const Matrix&, int64_t, int64_t);
 as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device, void* stream, as_plan_t* best,
                         char* best_graph, size_t* len);
+std::vector<double> matrix_features(const Matrix& A);
 
 namespace {
 thread_local std::string g_last_error;
@@ -774,6 +775,14 @@ as_status_t as_search(as_matrix_t M, const as_search_cfg_t* cfg, int device, voi
     st = search_impl(M->A, cfg, device, stream, best, best_graph, len);
   });
   return g != AS_OK ? g : st;
+}
+
+as_status_t as_matrix_features(as_matrix_t M, double* out) {
+  return guard([&] {
+    if (!M || !out) fail(AS_ERR_INVALID_ARG, "NULL argument");
+    std::vector<double> f = matrix_features(M->A);
+    std::copy(f.begin(), f.end(), out);
+  });
 }
 
 as_status_t as_graph_device_buildable(as_matrix_t M, as_graph_t G, int flags, int* out) {

@@ -323,6 +323,16 @@ std::string mutate_graph(const Seq& g0, Rng& r) {
 
 }  // namespace
 
+// matrix features of the cost model (as_matrix_features, AS_MATRIX_FEATURES of them)
+std::vector<double> matrix_features(const Matrix& A) {
+  const Stats st = stats_of(A);
+  int64_t empty = 0;
+  for (int64_t r = 0; r < A.m; ++r) empty += A.row_ptr[r + 1] == A.row_ptr[r];
+  return {std::log2(1.0 + (double)A.m), std::log2(1.0 + (double)A.n), std::log2(1.0 + (double)A.nnz()), st.avg,
+          std::log2(1.0 + st.var), std::log2(1.0 + (double)st.maxlen), A.m ? (double)empty / (double)A.m : 0.0,
+          A.dt == AS_R64F ? 8.0 : 4.0};
+}
+
 std::string random_graph(const Matrix& A, uint64_t seed) {
   Rng r(seed);
   Stats st = stats_of(A);
@@ -596,7 +606,27 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
   // after every 4 new timings; up to 80 % of the budget
   if (use_model) {
     Rng pr(cfg->seed ^ 0xA24BAED4963EE407ull);
-    const size_t d = graph_feature_count();
+    // with a history of other matrices' searches the model learns graph + matrix features
+    // -> log time per nonzero (the paper's offline-trained model); else graph features ->
+    // log time on this matrix
+    const bool hist = cfg->n_history > 0 && cfg->history_graphs && cfg->history_matrix && cfg->history_log_t_per_nnz;
+    const std::vector<double> mf = hist ? matrix_features(M) : std::vector<double>();
+    const double lognnz = std::log((double)std::max<int64_t>(1, M.nnz()));
+    std::vector<double> HX, Hy;
+    if (hist) {
+      for (int h = 0; h < cfg->n_history; ++h) {
+        std::vector<double> f;
+        try {
+          f = graph_features(parse_graph(cfg->history_graphs[h]));
+        } catch (const Error&) {
+          continue;
+        }
+        f.insert(f.end(), cfg->history_matrix + (size_t)h * mf.size(), cfg->history_matrix + (size_t)(h + 1) * mf.size());
+        HX.insert(HX.end(), f.begin(), f.end());
+        Hy.push_back(cfg->history_log_t_per_nnz[h]);
+      }
+    }
+    const size_t d = graph_feature_count() + mf.size();
     int ran = 0;
     const int cap = std::max(4, maxc / 2);
     while (cfg->budget_seconds <= 0 || elapsed() < 0.8 * cfg->budget_seconds) {
@@ -604,11 +634,12 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       for (auto& c : ranked)
         if (c.t > 0) okc.push_back(c);
       if (okc.size() < 8 || ran >= cap) break;
-      std::vector<double> X, y;
+      std::vector<double> X = HX, y = Hy;
       for (auto& c : okc) {
         std::vector<double> f = graph_features(parse_graph(c.canon));
+        f.insert(f.end(), mf.begin(), mf.end());
         X.insert(X.end(), f.begin(), f.end());
-        y.push_back(std::log(c.t));
+        y.push_back(std::log(c.t) - (hist ? lognnz : 0.0));
       }
       std::sort(okc.begin(), okc.end(), [](const Cand& a, const Cand& b) { return a.t < b.t; });
       std::vector<std::string> pool;
@@ -632,6 +663,7 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       std::vector<double> Xq;
       for (auto& c : pool) {
         std::vector<double> f = graph_features(parse_graph(c));
+        f.insert(f.end(), mf.begin(), mf.end());
         Xq.insert(Xq.end(), f.begin(), f.end());
       }
       std::vector<double> pred(pool.size());
@@ -641,7 +673,7 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
       std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return pred[a] < pred[b]; });
       for (size_t k = 0; k < std::min<size_t>(4, order.size()) && ran < cap; ++k) {
         if (cfg->budget_seconds > 0 && elapsed() > 0.8 * cfg->budget_seconds) break;
-        pred_ms = std::exp(pred[order[k]]);
+        pred_ms = std::exp(pred[order[k]] + (hist ? lognnz : 0.0));
         evaluate(2000 + ran, pool[order[k]], sampled ? "sample_model" : "model");
         pred_ms = -1;
         ++ran;

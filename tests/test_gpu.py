@@ -436,3 +436,22 @@ def test_spmv_host_batch(graph, beta):
         P.spmv_host_batch(2.0, xs, beta, ys)
         for i in range(k):
             assert np.array_equal(ys[i], refs[i].astype(np.float64)), (graph, k, i)
+
+
+def test_search_with_history(tmp_path):
+    """as_search with a cost-model history (graph + matrix features -> log time per nonzero,
+    NEXT-3): the model stage runs on history + own candidates, the winner validates and passes
+    O2."""
+    import json
+    other = synth.random_powerlaw(6000, 5000, 3, 800)
+    B_ = _mat(other)
+    hist = [(B_.random_graph(s), B_.features(), 0.01 + 0.001 * (s % 7), other.row.shape[0]) for s in range(40)]
+    hist = [h for h in hist if G.is_legal(h[0])]
+    coo = synth.random_powerlaw(8000, 7000, 5, 1500)
+    log = str(tmp_path / "s.jsonl")
+    best, text = asp.search(_mat(coo), device=0, seed=3, max_candidates=20, budget_seconds=40, warmup=1, reps=3,
+                            log_path=log, history=hist)
+    rows = [json.loads(l) for l in open(log)]
+    assert any("pred_ms" in r for r in rows)  # the model stage ran with the history
+    assert G.is_legal(text), text
+    run_check(coo, text, 1.0, 0.5, plan=best)

@@ -418,3 +418,13 @@ def test_device_buildable_query():
         assert not A.device_buildable(g, host_build=True), g
     for g in no:
         assert not A.device_buildable(g), g
+
+
+def test_matrix_features():
+    """as_matrix_features (the search cost model's matrix features) against a direct count."""
+    coo = synth.random_powerlaw(700, 500, 3, 120).astype(np.float32)
+    A = asp.Matrix.from_coo(coo.m, coo.n, coo.row, coo.col, coo.val)
+    L = np.bincount(coo.row, minlength=coo.m).astype(np.float64)
+    want = [np.log2(1 + coo.m), np.log2(1 + coo.n), np.log2(1 + L.sum()), L.mean(), np.log2(1 + L.var()),
+            np.log2(1 + L.max()), float((L == 0).mean()), 4.0]
+    assert np.allclose(A.features(), want, rtol=1e-12, atol=1e-12)
