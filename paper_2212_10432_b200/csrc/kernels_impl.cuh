@@ -401,14 +401,6 @@ struct ScanPE {
   int32_t row;
   bool s0, inside;
 };
-// A/B knob AS_PE_L2PF: at the start of a BMT, request its later batches' value / column
-// lines into L2 (prefetch.global.L2, no registers held), so the batch loads that follow the
-// first batch's gathers hit L2 instead of waiting on DRAM.
-#ifndef AS_PE_L2PF
-#define AS_PE_L2PF 0
-#endif
-__device__ __forceinline__ void pf_l2(const void* a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); }
-
 template <class V, bool PAD, int VEC, int KB, int EM, bool BMO, class XA>
 __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int64_t t, PadPos pp) {
   static_assert(32 % KB == 0 && KB % VEC == 0, "KB divides 32 and is a multiple of VEC");
@@ -433,19 +425,6 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   int j0 = 0;
   // pv / pc advance to the batch's first element (slot-major: KB/VEC chunk rows per batch)
   const int64_t adv = PAD ? (KB / VEC) * pp.stride : KB;
-  if constexpr (AS_PE_L2PF) {
-    if constexpr (PAD) {
-      for (int j = KB; j < len; j += VEC) {  // every later chunk row of this BMT
-        pf_l2(pv + (j / VEC) * pp.stride);
-        pf_l2(pc + (j / VEC) * pp.stride);
-      }
-    } else {
-      for (int j = 32; j < len; j += 32) {  // contiguous: one 128-byte line per 32 fp32 / 16 fp64
-        pf_l2(pv + j);
-        pf_l2(pc + j);
-      }
-    }
-  }
   V v[KB];
   int32_t c[KB];
   for (; j0 < full; j0 += KB, pv += adv, pc += adv) {
