@@ -164,7 +164,9 @@ as_status_t as_spmv(as_plan_t, const void* alpha, const void* x, const void* bet
  * result is identical either way (same kernels, same order on the device). */
 as_status_t as_spmv_host(as_plan_t, const void* alpha, const void* x_host, const void* beta,
                          void* y_host, void* stream);
-/* k independent SpMVs y_i = alpha*A*x_i + beta*y_i on host buffers (pinned for overlap),
+/* (as_spmv_host and as_spmv_host_batch use the plan's device scratch buffers and copy
+ * streams: calls on the same plan must not run concurrently from several host threads.)
+ * k independent SpMVs y_i = alpha*A*x_i + beta*y_i on host buffers (pinned for overlap),
  * pipelined across i: x_{i+1} is copied up while SpMV i runs and y_{i-1} is copied down
  * (two device buffer pairs, two copy streams); every x_i goes up and every y_i comes back.
  * Blocking; the steady state per SpMV is max(H2D x, kernels, D2H y).  Same errors as

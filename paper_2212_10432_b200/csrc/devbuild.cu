@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "internal.h"
 #include "plan.h"
@@ -364,8 +365,15 @@ void dev_build(Plan& P, const Matrix& A, const DevSpec& sp, cudaStream_t s) {
   const int64_t m = A.m, n = A.n, nnz = A.nnz();
   const bool f64 = A.dt == AS_R64F;
   const int64_t sv = f64 ? 8 : 4;
-  // canonical CSR, uploaded once per (matrix, device)
-  std::shared_ptr<DevCsr> C = A.dcache;
+  // canonical CSR, uploaded once per (matrix, device); the cache slot is shared by threads
+  // planning the same matrix, so it is read and replaced under a lock (the upload itself runs
+  // outside it: two threads may both upload, the later one's copy is kept)
+  static std::mutex cache_mu;
+  std::shared_ptr<DevCsr> C;
+  {
+    std::lock_guard<std::mutex> lk(cache_mu);
+    C = A.dcache;
+  }
   if (!C || C->device != P.device) {
     C = std::make_shared<DevCsr>();
     C->device = P.device;
@@ -388,7 +396,10 @@ void dev_build(Plan& P, const Matrix& A, const DevSpec& sp, cudaStream_t s) {
       }
     }
     ck(cudaStreamSynchronize(s), "upload csr");
-    if (!std::getenv("AS_NO_DEV_CACHE")) A.dcache = C;
+    if (!std::getenv("AS_NO_DEV_CACHE")) {
+      std::lock_guard<std::mutex> lk(cache_mu);
+      A.dcache = C;
+    }
   }
   Scratch S(s);
   // row lengths, SORT / SORT_SUB permutation, COMPRESS
