@@ -508,7 +508,9 @@ as_status_t search_impl(const Matrix& A, const as_search_cfg_t* cfg, int device,
   // that family (the generator's proposals outside it, which would need the host Designer,
   // are redrawn); AS_SEARCH_SAMPLE=1 restores the row-sample ranking over every family.
   const int64_t kSample = int64_t(1) << 26;
-  const bool big = A.nnz() > 4 * kSample;
+  static const char* big_env = std::getenv("AS_SEARCH_BIG_NNZ");  // tests: the large-matrix threshold
+  const int64_t big_nnz = big_env ? std::atoll(big_env) : 4 * kSample;
+  const bool big = A.nnz() > big_nnz;
   const bool dev_full = big && !std::getenv("AS_SEARCH_SAMPLE");
   const bool sampled = big && !dev_full;
   auto in_family = [&](const std::string& text) {

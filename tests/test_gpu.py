@@ -455,3 +455,33 @@ def test_search_with_history(tmp_path):
     assert any("pred_ms" in r for r in rows)  # the model stage ran with the history
     assert G.is_legal(text), text
     run_check(coo, text, 1.0, 0.5, plan=best)
+
+
+def test_search_large_matrix_mode(tmp_path):
+    """Above the large-matrix threshold (here lowered with AS_SEARCH_BIG_NNZ) the search times
+    candidates at full size over the on-device Designer's family: every timed candidate but the
+    seed graphs is device-buildable, and the winner validates and passes O2."""
+    import json
+    import subprocess
+    import sys
+    log = str(tmp_path / "s.jsonl")
+    code = f'''
+import sys, json
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import synth, paper_2212_10432_b200 as asp
+coo = synth.random_powerlaw(20000, 18000, 6, 3000)
+A = asp.Matrix.from_coo(coo.m, coo.n, coo.row, coo.col, coo.val)
+seed = "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED"
+P, g = asp.search(A, device=0, seed=5, max_candidates=14, budget_seconds=40, warmup=1, reps=3,
+                  seed_graphs=[seed], log_path={log!r})
+rows = [json.loads(l) for l in open({log!r})]
+timed = [r for r in rows if r["median_ms"] > 0 and r["i"] >= 1]
+assert timed, rows
+assert all(A.device_buildable(r["graph"]) for r in timed), [r["graph"] for r in timed if not A.device_buildable(r["graph"])]
+print("WINNER", g)
+'''
+    env = dict(os.environ, AS_SEARCH_BIG_NNZ="100000")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    winner = [l for l in r.stdout.splitlines() if l.startswith("WINNER")][0][7:]
+    assert G.is_legal(winner), winner
