@@ -240,8 +240,8 @@ as_status_t as_fit_array_model(const int64_t* a, size_t n, int budget, int64_t* 
 /* The search's cost model (NEXT-3; the paper's learned performance model of P:369 step 3,
  * P:371-377).  as_graph_features: fixed-length feature vector of a graph -- per operator
  * the occurrence count over all branches (24: ROW_DIV ... SHMEM_OFFSET_RED, SET_RESOURCE),
- * per numeric parameter class the mean log2(1 + value) (15: BMT/BMW/BMTB block sizes,
- * tpb, grid, stages, vec, DIA theta/max, DENSE b/theta, SORT_SUB g), then the number of
+ * per numeric parameter class the mean log2(1 + value) (17: BMT/BMW/BMTB block sizes,
+ * tpb, grid, stages, xcache, stream, vec, DIA theta/max, DENSE b/theta, SORT_SUB g), then the number of
  * leaves.  out == NULL -> *n = length.  as_surrogate_fit_predict: fits the gradient-boosted
  * regression-tree ensemble the search uses (60 rounds, depth 3, shrinkage 0.2, squared
  * loss) on X[n x d] (row-major) -> y[n] and writes its predictions for Xq[nq x d] to

@@ -84,6 +84,15 @@ class Part:
     excl_rows: np.ndarray         # global rows written exclusively (one writer unit)
     atom_rows: np.ndarray         # global rows written by several units of this part (atomics)
     ops: list = None              # mapping + implementing ops (csr parts)
+    stream: int = 0               # SET_RESOURCE stream of the part's branch (R-conc)
+
+
+def _stream_of(seq):
+    """The launch stream a branch's SET_RESOURCE names (R-conc; 0 when it names none)."""
+    for op in seq:
+        if op.name == "SET_RESOURCE":
+            return op.params["stream"]
+    return 0
 
 
 def build(csr: Csr, graph, dtype=np.float64):
@@ -165,6 +174,7 @@ def _run_seq(csr, seq, st, parts, dtype):
             return
         if nm == "COMPRESS":
             parts.append(_compress_and_map(csr, st, seq[k + 1:], dtype))
+            parts[-1].stream = _stream_of(seq[k + 1:])
             return
         raise AssertionError(nm)
 
@@ -204,7 +214,7 @@ def _dia_decom(csr, op, st, parts, dtype):
     arrays = {"dia.off": np.asarray(sel, np.int64), "dia.val": dia_val,
               "origin_rows": np.arange(r0, r0 + mb, dtype=np.int64) if D else np.zeros(0, np.int64)}
     excl = arrays["origin_rows"].copy()
-    parts.append(Part("dia", arrays, excl, np.zeros(0, np.int64)))
+    parts.append(Part("dia", arrays, excl, np.zeros(0, np.int64), stream=_stream_of(op.branches[0])))
     _residual(csr, op, State(rows, mask, True), parts, dtype)
 
 
@@ -255,7 +265,8 @@ def _dense_decom(csr, op, st, parts, dtype):
     arrays = {"tile.row_id": np.asarray(row_id, np.int64), "tile.row_ptr": np.asarray(row_ptr, np.int64),
               "tile.col": np.asarray([J for _, J in tiles], np.int64), "tile.val": tile_val,
               "origin_rows": np.asarray(excl, np.int64)}
-    parts.append(Part("dense", arrays, np.asarray(excl, np.int64), np.zeros(0, np.int64)))
+    parts.append(Part("dense", arrays, np.asarray(excl, np.int64), np.zeros(0, np.int64),
+                      stream=_stream_of(op.branches[0])))
     _residual(csr, op, State(rows, mask, True), parts, dtype)
 
 
@@ -435,17 +446,25 @@ def _sort_bmtb(row_ptr, col, val, origin, bmtb):
 # ------------------------------------------------------------------ writer rule (A22)
 def writer_rule(m, parts):
     """Launch order = non-empty parts by descending count of exclusively written rows
-    (stable).  Walking that order: a part whose exclusive rows are all first writes
+    (stable).  Parts naming a SET_RESOURCE stream other than the first part's run beside
+    it into scratch (mode 3, R-conc; below).  Walking that order: a part whose exclusive rows are all first writes
     STOREs alpha*s + beta*y; otherwise it ADDs and its first-written exclusive rows join
     the beta pre-pass.  Atomic rows first written by a part, and rows no part writes,
     join the pre-pass (y <- beta*y, or 0 when beta == 0)."""
     live = [i for i, p in enumerate(parts) if p.excl_rows.shape[0] + p.atom_rows.shape[0] > 0]
     live.sort(key=lambda i: -parts[i].excl_rows.shape[0])
+    # R-conc: the main stream is the launch stream of the first part in launch order; parts
+    # naming another stream run beside it (mode 3): each sums into a scratch vector of its
+    # own, added into y after the streams join -- so the rule runs over the main-stream
+    # parts only, and rows of side parts that no main part writes join the pre-pass
+    main = parts[live[0]].stream if live else 0
     written = np.zeros(m, bool)
     prepass = np.zeros(m, bool)
     mode = {}
     for i in live:
         p = parts[i]
+        if p.stream != main:
+            continue
         first = ~written[p.excl_rows]
         if first.all():
             mode[i] = 0   # STORE
@@ -455,6 +474,13 @@ def writer_rule(m, parts):
         prepass[p.atom_rows[~written[p.atom_rows]]] = True
         written[p.excl_rows] = True
         written[p.atom_rows] = True
+    for i in live:
+        p = parts[i]
+        if p.stream == main:
+            continue
+        mode[i] = 3
+        prepass[p.excl_rows[~written[p.excl_rows]]] = True
+        prepass[p.atom_rows[~written[p.atom_rows]]] = True
     prepass |= ~written
     return {"launch_order": np.asarray(live, np.int64),
             "mode": np.asarray([mode.get(i, 0) for i in range(len(parts))], np.int64),

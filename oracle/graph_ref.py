@@ -57,8 +57,11 @@ SCHEMA: dict[str, list[tuple[str, str, Any]]] = {
     "BMT_PAD": [("scope", "scope", "GLOBAL"), ("vec", "int", 0)],
     "SORT_BMTB": [],
     # stages / xcache: shared-memory resource choices of the implementing stage (TMA staging of
-    # CSR-stream blocks; x entries staged per CTA); they do not change what y is (R-xcache)
-    "SET_RESOURCE": [("tpb", "int", 256), ("grid", "int", 0), ("stages", "int", 2), ("xcache", "int", 0)],
+    # CSR-stream blocks; x entries staged per CTA); they do not change what y is (R-xcache).
+    # stream: the launch stream of the branch's kernel; parts on different streams run
+    # concurrently, which changes the writer rule (R-conc, writer_rule in builder_ref)
+    "SET_RESOURCE": [("tpb", "int", 256), ("grid", "int", 0), ("stages", "int", 2), ("xcache", "int", 0),
+                     ("stream", "int", 0)],
     **{r: [] for r in REDUCTIONS},
 }
 ALIASES = {"WARP_SEG_RED": "WARP_SEG_ADD_RED", "THREAD_BITMAP_RED": "THREAD_BITMAP_RED_G",
@@ -277,7 +280,9 @@ def to_string(seq) -> str:
     for op in seq:
         s = op.name
         if SCHEMA[op.name]:
-            s += "(" + ",".join(f"{k}={_fmt(op.params[k])}" for k, _, _ in SCHEMA[op.name]) + ")"
+            # SET_RESOURCE stream (R-conc) is printed only when non-zero
+            s += "(" + ",".join(f"{k}={_fmt(op.params[k])}" for k, _, _ in SCHEMA[op.name]
+                                if not (k == "stream" and op.params[k] == 0)) + ")"
         if op.branches:
             s += " { " + " | ".join(to_string(b) for b in op.branches) + " }"
         out.append(s)
@@ -319,8 +324,8 @@ def _check_params(op: Op, nid: int):
             bad("vec in {0,1,2,4}")
     elif op.name == "SET_RESOURCE":
         if (p["tpb"] < 32 or p["tpb"] > 1024 or p["tpb"] % 32 or p["grid"] < 0 or p["stages"] not in (0, 2)
-                or not 0 <= p["xcache"] <= 65536):
-            bad("tpb multiple of 32 in [32,1024], grid >= 0, stages in {0,2}, xcache in [0,65536]")
+                or not 0 <= p["xcache"] <= 65536 or not 0 <= p["stream"] <= 3):
+            bad("tpb multiple of 32 in [32,1024], grid >= 0, stages in {0,2}, xcache in [0,65536], stream in [0,3]")
 
 
 def validate(seq):

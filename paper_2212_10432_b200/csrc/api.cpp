@@ -204,6 +204,27 @@ int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s
       err = launch_prepass(P.d_prepass, P.n_prepass, b, y, P.dt == AS_R64F ? 1 : 0, s);
   }
   if (P.n_heavy && !err) err = (int)cudaMemsetAsync(P.d_heavy_acc, 0, (size_t)P.n_heavy * 8, s);
+  // R-conc: launches naming another stream than the first launch's run on side streams,
+  // forked here (after the pre-pass) and joined below; each writes its own scratch vector,
+  // added into y after the join (writer mode 3)
+  const int dtype = P.dt == AS_R64F ? 1 : 0;
+  auto on = [&](size_t i) -> cudaStream_t {
+    const int k = P.launch_stream[i];
+    return (P.concurrent && k != P.main_stream) ? P.side[k] : s;
+  };
+  if (P.concurrent && !err) {
+    for (size_t i = 0; i < P.launches.size() && !err; ++i) {
+      const int k = P.launch_stream[i];
+      if (k != P.main_stream && !P.side[k]) {
+        err = (int)cudaStreamCreateWithFlags(&P.side[k], cudaStreamNonBlocking);
+        if (!err) err = (int)cudaEventCreateWithFlags(&P.ev_join[k], cudaEventDisableTiming);
+      }
+    }
+    if (!P.ev_fork && !err) err = (int)cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming);
+    if (!err) err = (int)cudaEventRecord(P.ev_fork, s);
+    for (int k = 0; k < 4 && !err; ++k)
+      if (P.side[k]) err = (int)cudaStreamWaitEvent(P.side[k], P.ev_fork, 0);
+  }
   for (size_t i = 0; i < P.launches.size() && !err; ++i) {
     before(i);
     DevPart d = P.launches[i];
@@ -215,9 +236,25 @@ int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s
       d.peer_lo[q] = peer_lo[q];
       d.peer_hi[q] = peer_hi[q];
     }
-    err = launch_part(d, x, y, s);
+    void* yd = y;
+    if (i < P.side_y.size() && P.side_y[i]) {  // side part: STOREs alpha*s into its scratch
+      yd = P.side_y[i];
+      d.beta = 0.0;
+      d.mode = 0;
+      d.n_peer = 0;
+      if (P.n_side_zero[i]) err = launch_prepass(P.side_zero[i], P.n_side_zero[i], 0.0, yd, dtype, on(i));
+    }
+    if (!err) err = launch_part(d, x, yd, on(i));
     if (!err) after(i);
   }
+  if (P.concurrent)
+    for (int k = 0; k < 4 && !err; ++k)
+      if (P.side[k]) {
+        err = (int)cudaEventRecord(P.ev_join[k], P.side[k]);
+        if (!err) err = (int)cudaStreamWaitEvent(s, P.ev_join[k], 0);
+      }
+  for (size_t i = 0; i < P.side_y.size() && !err; ++i)
+    if (P.side_y[i]) err = launch_side_add(P.side_rows[i], P.n_side_rows[i], P.side_y[i], y, dtype, s);
   if (P.n_heavy && !err) err = launch_heavy_epilogue(P.d_heavy_rows, P.d_heavy_acc, P.n_heavy, y, s);
   return err;
 }
@@ -502,7 +539,7 @@ as_status_t as_spmv_host(as_plan_t h, const void* alpha, const void* x_host, con
     cudaError_t prior = cudaGetLastError();
     if (prior != cudaSuccess) fail(AS_ERR_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(prior));
     const size_t L = P.launches.size();
-    const bool pipe = L >= 2 && !P.n_heavy && P.spans.size() == L && !std::getenv("AS_HOST_NOPIPE");
+    const bool pipe = L >= 2 && !P.n_heavy && !P.concurrent && P.spans.size() == L && !std::getenv("AS_HOST_NOPIPE");
     char* dx = (char*)P.d_x;
     char* dy = (char*)P.d_y;
     int err = 0;
@@ -689,6 +726,14 @@ as_status_t as_plan_profile(as_plan_t h, const void* x, void* y, int reps, void*
     for (auto& e : ev) check_cuda(cudaEventCreate(&e), "event");
     std::vector<double> acc(L + 2, 0.0);
     int err = 0;
+    // per-launch times need the launches in one stream order: a concurrent plan (R-conc) is
+    // profiled serialised (its parts add atomically, so the result is the same)
+    struct Serial {
+      Plan& P;
+      bool c;
+      ~Serial() { P.concurrent = c; }
+    } serial{P, P.concurrent};
+    P.concurrent = false;
     for (int r = 0; r < reps && !err; ++r) {
       check_cuda(cudaEventRecord(ev[0], s), "event");
       err = run_plan(

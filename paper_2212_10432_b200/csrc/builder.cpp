@@ -249,6 +249,7 @@ struct Builder {
       P.tpb = (int)op.br[0][1].geti("tpb");
       P.grid = (int)op.br[0][1].geti("grid");
       P.stages = (int)op.br[0][1].geti("stages");
+      P.stream = (int)op.br[0][1].geti("stream");
     }
     hp.parts.push_back(std::move(P));
     residual(op, BState{st.rows, mk, true});
@@ -340,6 +341,7 @@ struct Builder {
       P.tpb = (int)op.br[0][1].geti("tpb");
       P.grid = (int)op.br[0][1].geti("grid");
       P.stages = (int)op.br[0][1].geti("stages");
+      P.stream = (int)op.br[0][1].geti("stream");
     }
     hp.parts.push_back(std::move(P));
     residual(op, BState{st.rows, mk, true});
@@ -400,6 +402,7 @@ struct Builder {
         P.grid = (int)op.geti("grid");
         P.stages = (int)op.geti("stages");
         P.xcache = op.geti("xcache");
+        P.stream = (int)op.geti("stream");
       } else if (nm == "THREAD_TOTAL_RED") P.red[2] = RED_TOTAL;
       else if (nm == "THREAD_BITMAP_RED_G") P.red[2] = RED_BITMAP;
       else if (nm == "WARP_TOTAL_RED") P.red[1] = RED_TOTAL;
@@ -660,9 +663,15 @@ void writer_rule(HostPlan& hp) {
     if (!hp.parts[i].excl.empty() || !hp.parts[i].atom.empty()) live.push_back((int64_t)i);
   std::stable_sort(live.begin(), live.end(),
                    [&](int64_t a, int64_t b) { return hp.parts[a].excl.size() > hp.parts[b].excl.size(); });
+  // R-conc: the main stream is the stream of the first part in launch order; parts naming
+  // another stream run beside it into a scratch vector of their own (mode 3), added into y
+  // after the streams join -- so the rule below runs over the main-stream parts only, and
+  // rows of side parts that no main part writes join the pre-pass (y <- beta*y first)
+  const int main_stream = live.empty() ? 0 : hp.parts[live[0]].stream;
   std::vector<uint8_t> written(hp.m, 0), pre(hp.m, 0);
   for (int64_t i : live) {
     HostPart& p = hp.parts[i];
+    if (p.stream != main_stream) continue;
     bool all_first = true;
     for (int64_t r : p.excl)
       if (written[r]) {
@@ -677,6 +686,15 @@ void writer_rule(HostPlan& hp) {
       if (!written[r]) pre[r] = 1;
     for (int64_t r : p.excl) written[r] = 1;
     for (int64_t r : p.atom) written[r] = 1;
+  }
+  for (int64_t i : live) {
+    HostPart& p = hp.parts[i];
+    if (p.stream == main_stream) continue;
+    p.mode = 3;
+    for (int64_t r : p.excl)
+      if (!written[r]) pre[r] = 1;
+    for (int64_t r : p.atom)
+      if (!written[r]) pre[r] = 1;
   }
   for (int64_t r = 0; r < hp.m; ++r)
     if (pre[r] || !written[r]) hp.prepass.push_back(r);

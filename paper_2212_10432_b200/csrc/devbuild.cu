@@ -718,6 +718,7 @@ void dev_build(Plan& P, const Matrix& A, const DevSpec& sp, cudaStream_t s) {
   P.bytes_model = bytes_model;
   P.launches.push_back(d);
   P.launch_part.push_back(0);
+  P.launch_stream.push_back(0);  // one part: nothing runs beside it
   P.spans.push_back(span);
   P.launch_bytes.push_back(bytes_model + (double)distinct * sv + (double)n_excl * sv + 2.0 * (double)n_atom * sv);
   P.single_writer = n_pre == 0 && P.n_heavy == 0 && n_atom == 0;

@@ -142,6 +142,7 @@ struct DevPart {
 int launch_part(const DevPart& p, const void* x, void* y, void* stream);      // returns cudaError_t
 int launch_prepass(const int32_t* rows, int64_t n, double beta, void* y, int dtype, void* stream);
 int launch_l2_flush(void* buf, size_t bytes, int pattern, void* stream);  // memset + read-back
+int launch_side_add(const int32_t* rows, int64_t n, const void* ys, void* y, int dtype, void* stream);  // R-conc
 int launch_heavy_epilogue(const int32_t* rows, const double* acc, int64_t n, void* y, void* stream);  // fp32 y
 int prepare_part(DevPart& p);  // per-kernel attributes (smem opt-in); returns cudaError_t
 // compose.cu

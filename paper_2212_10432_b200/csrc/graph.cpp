@@ -55,7 +55,7 @@ const std::vector<OpSpec>& specs() {
       {"SORT_BMTB", 2, {}},
       {"SET_RESOURCE", 3,
        {{"tpb", P_INT, true, 256, nullptr}, {"grid", P_INT, true, 0, nullptr}, {"stages", P_INT, true, 2, nullptr},
-        {"xcache", P_INT, true, 0, nullptr}}},
+        {"xcache", P_INT, true, 0, nullptr}, {"stream", P_INT, true, 0, nullptr}}},
       {"THREAD_TOTAL_RED", 3, {}},
       {"THREAD_BITMAP_RED_G", 3, {}},
       {"WARP_TOTAL_RED", 3, {}},
@@ -387,8 +387,10 @@ void check_params(const Op& o) {
     int64_t tpb = o.geti("tpb");
     int64_t st = o.geti("stages");
     const int64_t xc = o.geti("xcache");
-    if (tpb < 32 || tpb > 1024 || tpb % 32 || o.geti("grid") < 0 || (st != 0 && st != 2) || xc < 0 || xc > 65536)
-      bad("tpb multiple of 32 in [32,1024], grid >= 0, stages in {0,2}, xcache in [0,65536]");
+    const int64_t sq = o.geti("stream");
+    if (tpb < 32 || tpb > 1024 || tpb % 32 || o.geti("grid") < 0 || (st != 0 && st != 2) || xc < 0 || xc > 65536 ||
+        sq < 0 || sq > 3)
+      bad("tpb multiple of 32 in [32,1024], grid >= 0, stages in {0,2}, xcache in [0,65536], stream in [0,3]");
   }
 }
 
@@ -529,6 +531,9 @@ void print_seq(const Seq& s, std::string& out) {
     if (!o.params.empty()) {
       out += "(";
       for (size_t j = 0; j < o.params.size(); ++j) {
+        // SET_RESOURCE stream (R-conc) is printed only when it names a side stream, so the
+        // canonical text of every single-stream graph is unchanged
+        if (o.params[j].first == "stream" && o.params[j].second.i == 0) continue;
         if (j) out += ",";
         out += o.params[j].first;
         out += "=";

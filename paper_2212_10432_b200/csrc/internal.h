@@ -128,6 +128,8 @@ struct HostPart {
   Red red[3] = {RED_NONE, RED_NONE, RED_NONE};  // per level (BMTB, BMW, BMT)
   int tpb = 0, grid = 0, stages = 2;  // SET_RESOURCE
   int64_t xcache = 0;                 // SET_RESOURCE xcache: hot x entries staged in shared memory per CTA
+  int stream = 0;                     // SET_RESOURCE stream: launch stream (R-conc); parts on different
+                                      // streams run concurrently
   // DIA
   int64_t r0 = 0, mb = 0;
   std::vector<int64_t> dia_off;
@@ -138,7 +140,7 @@ struct HostPart {
   std::vector<double> tile_val;
   // writer rule
   std::vector<int64_t> excl, atom;  // global rows
-  int mode = 0;                      // 0 STORE, 1 ADD
+  int mode = 0;                      // 0 STORE, 1 ADD, 3 side stream: scratch + add epilogue (R-conc)
   Fam fam = FAM_NONE;
   std::string fam_name;
 };

@@ -76,14 +76,28 @@ __device__ __forceinline__ uint64_t pol_el() {
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// AS_X_LD (A/B build knob, default 0): L1 behaviour of the x gathers -- 0 L1-allocating,
+// 1 L1::no_allocate, 2 .cg (L2 only), 3 L1::evict_first; all with the L2 evict_last policy.
+#ifndef AS_X_LD
+#define AS_X_LD 0
+#endif
+#if AS_X_LD == 1
+#define AS_XQ "ld.global.nc.L1::no_allocate.L2::cache_hint."
+#elif AS_X_LD == 2
+#define AS_XQ "ld.global.cg.L2::cache_hint."
+#elif AS_X_LD == 3
+#define AS_XQ "ld.global.nc.L1::evict_first.L2::cache_hint."
+#else
+#define AS_XQ "ld.global.nc.L2::cache_hint."
+#endif
 __device__ __forceinline__ double ldx(const double* x, int64_t c) {
   double v;
-  AS_LDASM("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
+  AS_LDASM(AS_XQ "f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
   return v;
 }
 __device__ __forceinline__ double ldx(const float* x, int64_t c) {
   float v;
-  AS_LDASM("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  AS_LDASM(AS_XQ "f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
   return (double)v;
 }
 // the same gathers in the value type (fp32 operands are widened only at the FMA: the
@@ -92,9 +106,25 @@ __device__ __forceinline__ double ldx(const float* x, int64_t c) {
 __device__ __forceinline__ double ldxv(const double* x, int64_t c) { return ldx(x, c); }
 __device__ __forceinline__ float ldxv(const float* x, int64_t c) {
   float v;
-  AS_LDASM("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  AS_LDASM(AS_XQ "f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
   return v;
 }
+// x gathers of the hot-x (xcache) kernels: the columns outside the shared-memory copy of a
+// scattered matrix are rarely re-read from L1 (C3: 10 % L1 hits), so they are read at L2
+// only (.cg): C3 877.6 -> 863 us, gather microbenchmark 750 -> 672 us
+// (profiles/r02/ab_xld.jsonl, gather_xld.jsonl)
+__device__ __forceinline__ double ldx_l2(const double* x, int64_t c) {
+  double v;
+  AS_LDASM("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
+  return v;
+}
+__device__ __forceinline__ float ldxv_l2(const float* x, int64_t c) {
+  float v;
+  AS_LDASM("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  return v;
+}
+__device__ __forceinline__ double ldxv_l2(const double* x, int64_t c) { return ldx_l2(x, c); }
+
 // metadata: small, reused by neighbours -> plain non-coherent load
 __device__ __forceinline__ int32_t ldm(const int32_t* p) { return __ldg(p); }
 __device__ __forceinline__ uint32_t ldm(const uint32_t* p) { return __ldg(p); }

@@ -24,6 +24,14 @@ __global__ void k_prepass(const int32_t* __restrict__ rows, int64_t n, double be
     y[r] = beta == 0.0 ? (V)0 : (V)(beta * (double)y[r]);
   }
 }
+// R-conc: a side-stream part's scratch rows added into y after the streams join
+template <class V>
+__global__ void k_side_add(const int32_t* __restrict__ rows, int64_t n, const V* __restrict__ ys, V* __restrict__ y) {
+  for (int64_t i = gtid(); i < n; i += gthreads()) {
+    const int64_t r = ldm(rows + i);
+    y[r] = (V)((double)y[r] + (double)ys[r]);
+  }
+}
 // heavy rows of fp32 plans: y[r] += (float)acc (one rounding of the fp64 sum)
 __global__ void k_heavy_epilogue(const int32_t* __restrict__ rows, const double* __restrict__ acc, int64_t n,
                                  float* __restrict__ y) {
@@ -55,6 +63,14 @@ int launch_prepass(const int32_t* rows, int64_t n, double beta, void* y, int dty
   int64_t g = std::min<int64_t>((n + 255) / 256, 148 * 16);
   if (dtype == 1) k_prepass<double><<<g, 256, 0, (cudaStream_t)stream>>>(rows, n, beta, (double*)y);
   else k_prepass<float><<<g, 256, 0, (cudaStream_t)stream>>>(rows, n, beta, (float*)y);
+  return (int)cudaGetLastError();
+}
+
+int launch_side_add(const int32_t* rows, int64_t n, const void* ys, void* y, int dtype, void* stream) {
+  if (n <= 0) return 0;
+  int64_t g = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (dtype == 1) k_side_add<double><<<g, 256, 0, (cudaStream_t)stream>>>(rows, n, (const double*)ys, (double*)y);
+  else k_side_add<float><<<g, 256, 0, (cudaStream_t)stream>>>(rows, n, (const float*)ys, (float*)y);
   return (int)cudaGetLastError();
 }
 

@@ -158,8 +158,8 @@ template <class V>
 struct XHot {
   const V* __restrict__ x;
   const V* sm;
-  __device__ __forceinline__ double operator()(int64_t c) const { return c < 0 ? (double)sm[~c] : ldx(x, c); }
-  __device__ __forceinline__ V v(int64_t c) const { return c < 0 ? sm[~c] : ldxv(x, c); }
+  __device__ __forceinline__ double operator()(int64_t c) const { return c < 0 ? (double)sm[~c] : (double)ldxv_l2(x, c); }
+  __device__ __forceinline__ V v(int64_t c) const { return c < 0 ? sm[~c] : ldxv_l2(x, c); }
 };
 // All CTAs fill at kernel start, so the fill's latency is exposed once per CTA: 8 column
 // indices, then 8 gathers, are in flight per thread (a one-load-at-a-time loop cost ~25 us

@@ -294,6 +294,11 @@ Plan::~Plan() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (s_d2h) cudaStreamDestroy(s_d2h);
+    for (int k = 0; k < 4; ++k) {
+      if (side[k]) cudaStreamDestroy(side[k]);
+      if (ev_join[k]) cudaEventDestroy(ev_join[k]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
     cudaSetDevice(cur);
   }
 }
@@ -686,6 +691,7 @@ void Plan::upload(cudaStream_t s) {
     if (d.fam == FAM_BLOCK_OFFSET && d.variant == 1) fn += "_tma";
     launches.push_back(d);
     launch_part.push_back(pi);
+    launch_stream.push_back(h.stream);
     spans.push_back(part_span(h, host.n));
     launch_bytes.push_back(bytes_model - bytes_before);
   }
@@ -712,6 +718,31 @@ void Plan::upload(cudaStream_t s) {
     std::string& fn = host.parts[host.launch_order[i]].fam_name;
     const size_t at = fn.find("_xh");
     if (at != std::string::npos) fn.erase(at, 3);
+  }
+  main_stream = launch_stream.empty() ? 0 : launch_stream[0];
+  for (int k : launch_stream) concurrent = concurrent || k != main_stream;
+  const size_t L = launches.size();
+  side_y.assign(L, nullptr);
+  side_rows.assign(L, nullptr);
+  side_zero.assign(L, nullptr);
+  n_side_rows.assign(L, 0);
+  n_side_zero.assign(L, 0);
+  for (size_t i = 0; i < L; ++i) {
+    const HostPart& h = host.parts[host.launch_order[i]];
+    if (h.mode != 3) continue;
+    side_y[i] = up(nullptr, 0, s, (size_t)m * (dt == AS_R64F ? 8 : 4));
+    std::vector<int64_t> rows(h.excl);
+    rows.insert(rows.end(), h.atom.begin(), h.atom.end());
+    std::sort(rows.begin(), rows.end());
+    rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
+    side_rows[i] = up_i32(rows, s, "side rows");
+    n_side_rows[i] = (int64_t)rows.size();
+    if (!h.atom.empty()) {
+      std::vector<int64_t> z(h.atom);
+      std::sort(z.begin(), z.end());
+      side_zero[i] = up_i32(z, s, "side atomic rows");
+      n_side_zero[i] = (int64_t)z.size();
+    }
   }
   single_writer = host.prepass.empty() && n_heavy == 0;
   for (int64_t pi : host.launch_order)
@@ -741,7 +772,7 @@ void Plan::upload_spmm(cudaStream_t s) {
       sp.col = (const int32_t*)up(h.col.data(), h.col.size() * 4, s);
       sp.val = up_vals(h.val, s);
       std::vector<uint8_t> add((size_t)sp.m_p);
-      for (int64_t i = 0; i < sp.m_p; ++i) add[(size_t)i] = (h.mode == 1 || atom[(size_t)h.origin[i]]) ? 1 : 0;
+      for (int64_t i = 0; i < sp.m_p; ++i) add[(size_t)i] = (h.mode != 0 || atom[(size_t)h.origin[i]]) ? 1 : 0;
       sp.add = (const uint8_t*)up(add.data(), add.size(), s);
       ck(cudaStreamSynchronize(s), "spmm upload");
     }

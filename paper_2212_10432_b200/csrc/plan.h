@@ -51,6 +51,19 @@ struct Plan {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // as_spmv_host copy streams (lazy)
   std::vector<cudaEvent_t> evs;                    // as_spmv_host events (lazy)
   cudaEvent_t host_event(size_t i);
+  // R-conc: per launch its SET_RESOURCE stream.  Launches naming the first launch's stream
+  // run on the caller's stream; the others (side parts, writer mode 3) on side stream k
+  // (created lazily), forked after the pre-pass and joined before the epilogues.  A side
+  // part writes its own scratch vector side_y (its atomic rows zeroed first), whose rows
+  // side_rows are added into y after the join (k_side_add).
+  std::vector<int> launch_stream;
+  int main_stream = 0;
+  bool concurrent = false;
+  cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<void*> side_y;
+  std::vector<const int32_t*> side_rows, side_zero;
+  std::vector<int64_t> n_side_rows, n_side_zero;
   std::string canon;
 
   ~Plan();

@@ -239,12 +239,15 @@ std::string gen_path(Rng& r, const Stats& st, bool can_decom, bool can_sort, boo
                       ",max=" + std::to_string(r.pick(std::vector<int64_t>{4, 8, 16, 32})) + ") { DIA";
       if (r.coin(0.7))
         s += "; SET_RESOURCE(tpb=" + std::to_string(r.pick(std::vector<int>{64, 128, 256, 512})) +
-             ",grid=" + std::to_string(r.pick(std::vector<int>{0, 4, 8, 16})) + ")";
+             ",grid=" + std::to_string(r.pick(std::vector<int>{0, 4, 8, 16})) +
+             (r.coin(0.3) ? ",stream=1" : "") + ")";  // R-conc: beside the residual
       return s + " | " + gen_path(r, st, false, can_sort, false, depth + 1) + " }";
     }
     case 6: {
       std::string s = "DENSE_DECOM(b=" + std::to_string(r.pick(std::vector<int64_t>{16, 32, 64, 128})) +
-                      ",theta=" + std::string(r.pick(std::vector<const char*>{"0.5", "0.75", "0.9"})) + ") { DENSE | " +
+                      ",theta=" + std::string(r.pick(std::vector<const char*>{"0.5", "0.75", "0.9"})) + ") { DENSE" +
+                      // R-conc: the HBM-streaming tiles beside the gather-bound residual
+                      (r.coin(0.4) ? "; SET_RESOURCE(tpb=256,stream=1)" : "") + " | " +
                       gen_path(r, st, false, can_sort, false, depth + 1) + " }";
       return s;
     }
@@ -307,6 +310,7 @@ std::string mutate_graph(const Seq& g0, Rng& r) {
   else if (k == "grid") step({0, 1, 2, 4, 8, 16});
   else if (k == "stages") v.i = v.i ? 0 : 2;
   else if (k == "xcache") step({0, 4096, 8192, 16384, 24576, 32768});
+  else if (k == "stream") v.i = v.i ? 0 : 1;  // R-conc: this branch beside / after the others
   else if (k == "vec") step({0, 1, 2, 4});
   else if (k == "max") step({4, 8, 16, 32});
   else if (k == "b") step({16, 32, 64, 128});

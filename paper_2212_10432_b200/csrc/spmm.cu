@@ -159,7 +159,7 @@ __global__ void k_spmm_dia(DevPart p, double alpha, double beta, const V* __rest
       const int64_t col = r + p.dia_off[d];
       if (col >= 0 && col < p.n) acc += (double)__ldg(dv + d * p.dia_stride + i) * (double)__ldg(X + col * ldx + c);
     }
-    put(Y + r * ldy + c, acc, alpha, beta, p.mode == 1);
+    put(Y + r * ldy + c, acc, alpha, beta, p.mode != 0);
   }
 }
 
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256) k_spmm_dense_dmma(DevPart p, double alpha
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int64_t c = c0 + ch * 32 + nb * 8 + 2 * tig + e;
-              if (c < k) put(Y + row * ldy + c, acc[h][nb][e], alpha, beta, p.mode == 1);
+              if (c < k) put(Y + row * ldy + c, acc[h][nb][e], alpha, beta, p.mode != 0);
             }
         }
       }

@@ -35,6 +35,7 @@ struct PClass {
 const PClass kPar[] = {{"BMT_ROW_BLOCK", "rows"}, {"BMT_NNZ_BLOCK", "nnz"},  {"BMW_ROW_BLOCK", "rows"},
                        {"BMW_NNZ_BLOCK", "nnz"},  {"BMTB_ROW_BLOCK", "rows"}, {"BMTB_NNZ_BLOCK", "nnz"},
                        {"SET_RESOURCE", "tpb"},   {"SET_RESOURCE", "grid"},   {"SET_RESOURCE", "stages"}, {"SET_RESOURCE", "xcache"},
+                       {"SET_RESOURCE", "stream"},
                        {"BMT_PAD", "vec"},        {"DIA_DECOM", "theta"},     {"DIA_DECOM", "max"},
                        {"DENSE_DECOM", "b"},      {"DENSE_DECOM", "theta"},   {"SORT_SUB", "g"}};
 constexpr int kNPar = sizeof(kPar) / sizeof(kPar[0]);

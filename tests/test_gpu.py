@@ -19,7 +19,7 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 asp = pytest.importorskip("paper_2212_10432_b200")
 
-from test_host import COMPOSE_GRAPHS, FAMILY_GRAPHS, assert_infeasible_justified, compare_export  # noqa: E402
+from test_host import COMPOSE_GRAPHS, CONC_GRAPHS, FAMILY_GRAPHS, assert_infeasible_justified, compare_export  # noqa: E402
 
 
 def _mat(coo):
@@ -47,7 +47,7 @@ def run_check(coo, graph, alpha=1.0, beta=0.0, int_mode=False, seed=0, keep_host
     return P, ratio
 
 
-@pytest.mark.parametrize("graph", FAMILY_GRAPHS + COMPOSE_GRAPHS)
+@pytest.mark.parametrize("graph", FAMILY_GRAPHS + COMPOSE_GRAPHS + CONC_GRAPHS)
 @pytest.mark.parametrize("seed", range(3))
 def test_family_integer_exact(graph, seed):
     coo = synth.random_matrix(33 + 40 * seed, 29 + 17 * seed, 0.12 + 0.06 * seed, seed, int_mode=True,
@@ -61,7 +61,7 @@ def test_family_integer_exact(graph, seed):
     compare_export(P, coo, graph)
 
 
-@pytest.mark.parametrize("graph", FAMILY_GRAPHS + COMPOSE_GRAPHS)
+@pytest.mark.parametrize("graph", FAMILY_GRAPHS + COMPOSE_GRAPHS + CONC_GRAPHS)
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_family_real(graph, dtype):
     coo = synth.random_powerlaw(700, 650, 3, 300).astype(dtype)
@@ -485,3 +485,70 @@ print("WINNER", g)
     assert r.returncode == 0, r.stderr[-2000:]
     winner = [l for l in r.stdout.splitlines() if l.startswith("WINNER")][0][7:]
     assert G.is_legal(winner), winner
+
+
+@pytest.mark.parametrize("graph", CONC_GRAPHS)
+def test_concurrent_branches_every_entry_point(graph):
+    """R-conc (SET_RESOURCE stream): side-stream parts write their own scratch, added after the
+    join -- checked bit-exact in integer mode through as_spmv (also repeated, so the side
+    streams and events are reused), CUDA-graph replay (the fork/join captured), the host
+    path, a batch, and the serialised as_plan_profile; every row against the oracle."""
+    coo = synth.random_matrix(900, 700, 0.02, 5, int_mode=True, dense_rows=1).astype(np.float64)
+    x, y0 = synth.vectors(coo.n, coo.m, 5, np.float64, True)
+    yref, _ = S.spmv_coo(coo.m, coo.row, coo.col, coo.val, x, 2.0, -1.0, y0)
+    A = _mat(coo)
+    try:
+        P = asp.Plan(A, graph, device=0, keep_host=True)
+    except asp.AsError as e:
+        assert_infeasible_justified(coo, graph, e)
+        return
+    modes = P.export("mode").tolist()
+    # a part runs beside the main stream (DIA / DENSE parts may be empty on a random matrix)
+    assert 3 in modes or graph.startswith(("DIA", "DENSE")), modes
+    dx = torch.from_numpy(x).cuda()
+    for _ in range(3):
+        dy = torch.from_numpy(y0.copy()).cuda()
+        P.spmv(2.0, dx, -1.0, dy)
+        torch.cuda.synchronize()
+        assert np.array_equal(dy.cpu().numpy(), yref), graph
+    G = asp.Plan(A, graph, device=0, graph_replay=True)
+    for _ in range(2):
+        dy = torch.from_numpy(y0.copy()).cuda()
+        G.spmv(2.0, dx, -1.0, dy)
+        torch.cuda.synchronize()
+        assert np.array_equal(dy.cpu().numpy(), yref), graph
+    yh = y0.copy()
+    P.spmv_host(2.0, x, -1.0, yh)
+    assert np.array_equal(yh, yref)
+    ys = [y0.copy() for _ in range(3)]
+    P.spmv_host_batch(2.0, [x, x, x], -1.0, ys)
+    assert all(np.array_equal(v, yref) for v in ys)
+    dy = torch.from_numpy(y0.copy()).cuda()
+    prof = P.profile(dx, dy, reps=2)
+    assert len(prof) >= 2 and all(ms >= 0 for _, ms, _ in prof)
+    run_check(coo.astype(np.float32), graph, 1.5, -0.5, seed=7)   # fp32, north_star tolerance
+
+
+def test_concurrent_dense_beside_residual_c4_shape():
+    """R-conc on a C4-shaped matrix (planted 64x64 tiles + diagonal + scatter): the DENSE part
+    on a side stream, the NNZ residual on the main stream -- bit-identical to the same graph on
+    one stream and to the oracle (integer mode), fp64 and fp32."""
+    A, _ = synth.c4_blockdense(m=65536, b=64, n_tiles=192, nnz=1_500_000, seed=9, int_mode=True)
+    res = ("COMPRESS; BMW_NNZ_BLOCK(nnz=1024); BMT_NNZ_BLOCK(nnz=32); BMT_PAD(scope=BMW,vec=1); "
+           "THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=512,grid=2); GMEM_ATOM_RED")
+    seq = f"DENSE_DECOM(b=64,theta=0.5) {{ DENSE; SET_RESOURCE(tpb=256) | {res} }}"
+    conc = f"DENSE_DECOM(b=64,theta=0.5) {{ DENSE; SET_RESOURCE(tpb=256,stream=1) | {res} }}"
+    for dt in (np.float64, np.float32):
+        coo = A.astype(dt)
+        x, y0 = synth.vectors(coo.n, coo.m, 9, dt, True)
+        out = []
+        for g in (seq, conc):
+            P = asp.Plan(_mat(coo), g, device=0, keep_host=True)
+            dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y0.copy()).cuda()
+            P.spmv(1.0, dx, 1.0, dy)
+            torch.cuda.synchronize()
+            out.append(dy.cpu().numpy())
+        assert P.export("mode").tolist() == [3, 0]          # DENSE beside the residual
+        yref, _ = S.spmv_coo(coo.m, coo.row, coo.col, coo.val.astype(np.float64), x.astype(np.float64), 1.0, 1.0,
+                             y0.astype(np.float64))
+        assert np.array_equal(out[0], out[1]) and np.array_equal(out[1].astype(np.float64), yref)

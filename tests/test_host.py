@@ -285,6 +285,16 @@ COMPOSE_GRAPHS = [
     "COL_DIV(cuts=[14]) { COMPRESS; BMTB_NNZ_BLOCK(64); BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; SHMEM_OFFSET_RED; GMEM_ATOM_RED }",
 ]
 
+# R-conc: branches whose SET_RESOURCE names different launch streams run concurrently;
+# every part then adds atomically onto a fully pre-passed y (writer_rule, mode 2)
+CONC_GRAPHS = [
+    "DENSE_DECOM(b=4,theta=0.25) { DENSE; SET_RESOURCE(tpb=128,stream=1) | COMPRESS; BMW_NNZ_BLOCK(64); BMT_NNZ_BLOCK(2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(tpb=256,grid=1); GMEM_ATOM_RED }",
+    "DIA_DECOM(theta=0.2,max=3) { DIA; SET_RESOURCE(stream=2) | COMPRESS; BMT_NNZ_BLOCK(5); BMT_PAD(GLOBAL,1); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
+    "COL_DIV(cuts=[7, 15]) { COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; SET_RESOURCE(stream=1); GMEM_ATOM_RED | COMPRESS; BMT_NNZ_BLOCK(2); THREAD_BITMAP_RED_G; GMEM_ATOM_RED | COMPRESS; BMTB_ROW_BLOCK(4); BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; SHMEM_OFFSET_RED; SET_RESOURCE(64,stream=3); GMEM_ATOM_RED }",
+    "ROW_DIV(cuts=[9]) { COMPRESS; BMW_ROW_BLOCK(1); WARP_TOTAL_RED; SET_RESOURCE(stream=1); GMEM_ATOM_RED | COMPRESS; BMT_NNZ_BLOCK(3); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
+    "HYB_DECOM(w=2) { COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED | COMPRESS; BMT_NNZ_BLOCK(4); THREAD_BITMAP_RED_G; SET_RESOURCE(stream=1); GMEM_ATOM_RED }",
+]
+
 # Product-only infeasibility: device resource limits the oracle does not model:
 # shared memory (P2), the padded-slot cap (P4b), int32 device indices (A36), > 64 DIA
 # diagonals, DENSE tiles > 128.  Any other AS_ERR_PLAN_INFEASIBLE must be infeasible for the
@@ -302,7 +312,7 @@ def assert_infeasible_justified(coo, graph, err):
         B.build(csr, G.parse(graph), coo.val.dtype)
 
 
-@pytest.mark.parametrize("graph", FAMILY_GRAPHS + COMPOSE_GRAPHS)
+@pytest.mark.parametrize("graph", FAMILY_GRAPHS + COMPOSE_GRAPHS + CONC_GRAPHS)
 @pytest.mark.parametrize("seed", range(3))
 def test_host_plan_matches_oracle(graph, seed):
     coo = synth.random_matrix(33 + seed, 29, 0.12 + 0.06 * seed, seed, int_mode=True, dense_rows=seed % 2)

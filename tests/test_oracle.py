@@ -321,6 +321,8 @@ FUZZ_GRAPHS = [
     "DENSE_DECOM(b=4,theta=0.3) { DENSE | DIA_DECOM(0.5) { DIA | COMPRESS; BMW_ROW_BLOCK(1); WARP_TOTAL_RED; GMEM_ATOM_RED } }",
     "HYB_DECOM(w=2) { COMPRESS; BMT_ROW_BLOCK(1); BMT_PAD(GLOBAL); THREAD_TOTAL_RED; GMEM_ATOM_RED | COMPRESS; BMT_NNZ_BLOCK(3); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
     "BIN(t=[3]) { HYB_DECOM(w=1) { COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED } }",
+    "DIA_DECOM(theta=0.3,max=3) { DIA; SET_RESOURCE(stream=1) | COMPRESS; BMT_NNZ_BLOCK(5); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
+    "COL_DIV(cuts=[10]) { COMPRESS; BMTB_NNZ_BLOCK(11); SHMEM_OFFSET_RED; SET_RESOURCE(stream=2); GMEM_ATOM_RED | COMPRESS; BMT_ROW_BLOCK(2); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
 ]
 
 
@@ -387,6 +389,33 @@ def test_dia_on_lap2d_closed_form():
     dv = ex["p0.dia.val"]
     assert dv.shape[0] == 5 * g * g and int((dv == 0).sum()) == 4 * g
     assert ex["prepass"].tolist() == [] and ex["mode"].tolist() == [0]
+
+
+def test_writer_rule_concurrent_pin():
+    """R-conc on the canonical 4x4 (hand-derived).  DIA_DECOM(0.75) selects offset 0 (3 of 4
+    band positions filled; every other offset fills <= 1/2), so the DIA part writes rows
+    0-3 and the residual {(0,2), (2,0), (2,1), (2,3)} rows 0 and 2.  One stream: DIA STOREs
+    first, the residual ADDs onto rows DIA wrote, no pre-pass (A22).  Residual on another
+    stream: it runs beside DIA into its own scratch and is added after the join (mode 3);
+    DIA already writes rows 0 and 2, so still no pre-pass.  ROW_DIV(2) bands on two
+    streams: band 0 (first in launch order) is the main stream and STOREs rows 0-1; band 1
+    runs beside it, and its rows 2-3, which no main-stream part writes, are pre-passed."""
+    seq = "DIA_DECOM(theta=0.75,max=8) { DIA%s | COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED%s; GMEM_ATOM_RED }"
+    ex, parts = _build(seq % ("", ""))
+    assert ex["p0.dia.off"].tolist() == [0] and ex["p1.origin_rows"].tolist() == [0, 2]
+    assert ex["launch_order"].tolist() == [0, 1] and ex["mode"].tolist() == [0, 1] and ex["prepass"].tolist() == []
+    for a, b in [("; SET_RESOURCE(stream=1)", ""), ("", "; SET_RESOURCE(stream=2)")]:
+        ex, parts = _build(seq % (a, b))
+        assert ex["launch_order"].tolist() == [0, 1] and ex["mode"].tolist() == [0, 3], (a, b)
+        assert ex["prepass"].tolist() == []
+    assert [p.stream for p in parts] == [0, 2]
+    # the same stream named on both branches is one stream: the sequential rule
+    ex, _ = _build(seq % ("; SET_RESOURCE(stream=2)", "; SET_RESOURCE(stream=2)"))
+    assert ex["mode"].tolist() == [0, 1] and ex["prepass"].tolist() == []
+    band = "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED%s; GMEM_ATOM_RED"
+    ex, _ = _build("ROW_DIV(cuts=[2]) { %s | %s }" % (band % "; SET_RESOURCE(stream=1)", band % ""))
+    assert ex["launch_order"].tolist() == [0, 1] and ex["mode"].tolist() == [0, 3]
+    assert ex["prepass"].tolist() == [2, 3]
 
 
 def test_dense_extracts_planted_tiles():

@@ -14,7 +14,7 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 asp = pytest.importorskip("paper_2212_10432_b200")
 
-from test_host import COMPOSE_GRAPHS, FAMILY_GRAPHS, assert_infeasible_justified  # noqa: E402
+from test_host import COMPOSE_GRAPHS, CONC_GRAPHS, FAMILY_GRAPHS, assert_infeasible_justified  # noqa: E402
 
 EXTRA = [
     "DIA_DECOM(theta=0.2,max=6) { DIA | COMPRESS; BMT_NNZ_BLOCK(5); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
@@ -62,7 +62,7 @@ def run(coo, graph, k, alpha, beta, int_mode, seed, pad=0):
         assert torch.count_nonzero(Yd[:, k:]) == 0  # columns beyond k untouched
 
 
-@pytest.mark.parametrize("graph", FAMILY_GRAPHS + EXTRA)
+@pytest.mark.parametrize("graph", FAMILY_GRAPHS + EXTRA + CONC_GRAPHS)
 @pytest.mark.parametrize("k", [1, 8, 19])
 def test_spmm_integer_exact(graph, k):
     coo = synth.random_matrix(130, 120, 0.15, 3, int_mode=True, dense_rows=1)

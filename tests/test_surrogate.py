@@ -12,7 +12,7 @@ import pytest
 
 asp = pytest.importorskip("paper_2212_10432_b200")
 
-N_OPS, N_PAR = 24, 16  # parameter classes incl. SET_RESOURCE xcache
+N_OPS, N_PAR = 24, 17  # parameter classes incl. SET_RESOURCE xcache and stream (R-conc)
 
 
 def test_feature_layout_hand_derived():
@@ -36,6 +36,13 @@ def test_feature_branches_and_means():
     assert f[10] == 1 and f[9] == 1 and f[8] == 1          # BMT/BMW/BMTB_ROW_BLOCK
     assert f[N_OPS + 6] == pytest.approx((math.log2(129) + math.log2(513)) / 2)   # mean tpb class
     assert f[-1] == 3
+
+
+def test_feature_stream_class():
+    """R-conc: SET_RESOURCE stream is its own parameter class (index 10, after xcache)."""
+    f = asp.Graph("DIA_DECOM(0.5) { DIA; SET_RESOURCE(stream=1) | COMPRESS; BMT_NNZ_BLOCK(4); "
+                  "THREAD_BITMAP_RED_G; GMEM_ATOM_RED }").features()
+    assert f[N_OPS + 10] == pytest.approx(1.0)   # mean log2(1 + 1) over the one SET_RESOURCE
 
 
 def _gbr_sklearn(X, y, Xq):

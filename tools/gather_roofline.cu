@@ -69,6 +69,34 @@ __device__ __forceinline__ double ldx(const double* x, int64_t c) {
   return v;
 }
 
+// x-gather load variants (A/B of the L1 behaviour of the gathers): 0 = L1-allocating .nc with
+// an L2 evict_last policy (the product's ldx), 1 = L1::no_allocate, 2 = .cg (L2 only),
+// 3 = L1::evict_first, 4 = plain .nc without an L2 policy
+template <int XLD>
+__device__ __forceinline__ double ldxv_(const float* x, int64_t c) {
+  float v;
+  if (XLD == 0) asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  else if (XLD == 1)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  else if (XLD == 2) asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  else if (XLD == 3)
+    asm volatile("ld.global.nc.L1::evict_first.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(x + c), "l"(pol_el()));
+  else asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(x + c));
+  return (double)v;
+}
+template <int XLD>
+__device__ __forceinline__ double ldxv_(const double* x, int64_t c) {
+  double v;
+  if (XLD == 0) asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
+  else if (XLD == 1)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
+  else if (XLD == 2) asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
+  else if (XLD == 3)
+    asm volatile("ld.global.nc.L1::evict_first.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pol_el()));
+  else asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(x + c));
+  return v;
+}
+
 // 4 (fp32) / 2 (fp64) elements per vector, UNR vectors in flight per thread
 template <class V>
 struct Vec;
@@ -95,7 +123,7 @@ struct Vec<double> {
 
 constexpr int UNR = 4;
 
-template <class V, int MODE>  // MODE 0 stream, 1 gather, 2 gather with hot smem (~slot), 3 hot = col < nh (relabeled)
+template <class V, int MODE, int XLD = 0>  // MODE 0 stream, 1 gather, 2 gather with hot smem (~slot), 3 hot = col < nh (relabeled)
 __global__ void __launch_bounds__(1024) k_gather(const V* __restrict__ val, const int32_t* __restrict__ col,
                                                  const V* __restrict__ x, const V* __restrict__ xh, int nh,
                                                  int64_t nnz, double* out) {
@@ -119,9 +147,9 @@ __global__ void __launch_bounds__(1024) k_gather(const V* __restrict__ val, cons
 #pragma unroll
     for (int q = 0; q < UNR * W; ++q) {
       if (MODE == 0) xv[q] = (double)c[q];
-      else if (MODE == 1) xv[q] = ldx(x, c[q]);
-      else if (MODE == 2) xv[q] = c[q] < 0 ? (double)sh[~c[q]] : ldx(x, c[q]);
-      else xv[q] = c[q] < nh ? (double)sh[c[q]] : ldx(x, c[q]);
+      else if (MODE == 1) xv[q] = ldxv_<XLD>(x, c[q]);
+      else if (MODE == 2) xv[q] = c[q] < 0 ? (double)sh[~c[q]] : ldxv_<XLD>(x, c[q]);
+      else xv[q] = c[q] < nh ? (double)sh[c[q]] : ldxv_<XLD>(x, c[q]);
     }
 #pragma unroll
     for (int q = 0; q < UNR * W; ++q) acc += v[q] * xv[q];
@@ -133,9 +161,9 @@ __global__ void __launch_bounds__(1024) k_gather(const V* __restrict__ val, cons
 #pragma unroll
     for (int q = 0; q < W; ++q) {
       double xv = MODE == 0   ? (double)c[q]
-                  : MODE == 1 ? ldx(x, c[q])
-                  : MODE == 2 ? (c[q] < 0 ? (double)sh[~c[q]] : ldx(x, c[q]))
-                              : (c[q] < nh ? (double)sh[c[q]] : ldx(x, c[q]));
+                  : MODE == 1 ? ldxv_<XLD>(x, c[q])
+                  : MODE == 2 ? (c[q] < 0 ? (double)sh[~c[q]] : ldxv_<XLD>(x, c[q]))
+                              : (c[q] < nh ? (double)sh[c[q]] : ldxv_<XLD>(x, c[q]));
       acc += v[q] * xv;
     }
   }
@@ -310,6 +338,37 @@ int gr_launch(int dtype, int mode, const void* val, const int32_t* col, const vo
     else L(double, 3);
   }
 #undef L
+  return (int)cudaGetLastError();
+}
+// mode 1 / 2 with the x-gather load variant xld (0..4, see ldxv_)
+int gr_launch_x(int dtype, int mode, int xld, const void* val, const int32_t* col, const void* x, const void* xh,
+                int nh, int64_t nnz, double* out, int grid, int tpb, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t sm = mode >= 2 ? (size_t)nh * (dtype ? 8 : 4) : 0;
+#define LX(V, M, X)                                                                                          \
+  do {                                                                                                       \
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_gather<V, M, X>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             (int)sm);                                                       \
+    k_gather<V, M, X><<<grid, tpb, sm, s>>>((const V*)val, col, (const V*)x, (const V*)xh, nh, nnz, out);    \
+  } while (0)
+#define LXM(V, X)            \
+  do {                       \
+    if (mode == 1) LX(V, 1, X); \
+    else LX(V, 2, X);        \
+  } while (0)
+#define LXV(V)                  \
+  do {                          \
+    if (xld == 0) LXM(V, 0);    \
+    else if (xld == 1) LXM(V, 1); \
+    else if (xld == 2) LXM(V, 2); \
+    else if (xld == 3) LXM(V, 3); \
+    else LXM(V, 4);             \
+  } while (0)
+  if (dtype == 0) LXV(float);
+  else LXV(double);
+#undef LXV
+#undef LXM
+#undef LX
   return (int)cudaGetLastError();
 }
 // cp.async-staged gathers (mode 5): ch = chunk elements (8 or 16), nh hot columns in smem

@@ -41,6 +41,9 @@ def build():
     lib.gr_launch_dsm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
                                   ctypes.c_int, ctypes.c_void_p]
+    lib.gr_launch_x.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
+                                ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
     lib.gr_launch_hash.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                    ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
     return lib
@@ -92,6 +95,11 @@ def main():
                     help="also time cp.async-staged gathers (relabeled columns, hot prefix in smem)")
     ap.add_argument("--relabel", action="store_true",
                     help="also time the gathers with columns relabeled by descending reference count")
+    ap.add_argument("--xld", nargs="+", type=int, default=[],
+                    help="also time gather / hot K with x-load variants (0 L1-allocating, 1 L1::no_allocate, "
+                         "2 .cg, 3 L1::evict_first, 4 .nc without L2 policy) and hot-x copies up to --xld-hot-max")
+    ap.add_argument("--xld-hot", nargs="+", type=int, default=[0, 24576, 32768, 40960, 49152])
+    ap.add_argument("--xld-tpb", nargs="+", type=int, default=[1024])
     args = ap.parse_args()
     import torch
     lib = build()
@@ -142,6 +150,33 @@ def main():
                               "min_us": mn * 1e3, "model_gbs": model / (med * 1e-3) / 1e9,
                               "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
             del denc
+        for xld in args.xld:
+            for K in args.xld_hot:
+                if K * sv > 220 * 1024:
+                    continue
+                if K:
+                    hot = order[:K]
+                    slot = np.full(n, -1, np.int64)
+                    slot[hot] = np.arange(K)
+                    enc = np.where(slot[col] >= 0, ~slot[col], col).astype(np.int32)
+                    cover = float(cnt[hot].sum()) / nnz
+                    denc = torch.from_numpy(enc).to(dev)
+                    xh = x[torch.from_numpy(hot).to(dev)].contiguous()
+                else:
+                    cover, denc, xh = 0.0, dcol, x
+                for tpb in args.xld_tpb:
+                    grid = nsm * max(1, 1024 // tpb) if K else 2 * nsm * max(1, 1024 // tpb)
+
+                    def runx():
+                        rc = lib.gr_launch_x(dt, 2 if K else 1, xld, dval.data_ptr(), denc.data_ptr(), x.data_ptr(),
+                                             xh.data_ptr(), K, nnz, out.data_ptr(), grid, tpb, s)
+                        assert rc == 0, rc
+                    med, mn = timeit(runx, args.reps, flush)
+                    print(json.dumps({**base, "kernel": f"gather_xld{xld}_hot{K}", "xld": xld, "hot": K,
+                                      "tpb": tpb, "grid": grid, "hot_cover": cover, "median_us": med * 1e3,
+                                      "min_us": mn * 1e3, "model_gbs": model / (med * 1e-3) / 1e9,
+                                      "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
+                del denc
         if args.dsm:
             for (csize, kl) in [(1, 24576), (2, 24576), (4, 24576), (8, 24576), (2, 16384), (4, 16384), (8, 16384),
                                 (16, 12288)]:
