@@ -121,9 +121,10 @@ struct Vec<double> {
   }
 };
 
-constexpr int UNR = 4;
 
-template <class V, int MODE, int XLD = 0>  // MODE 0 stream, 1 gather, 2 gather with hot smem (~slot), 3 hot = col < nh (relabeled)
+constexpr int UNR = 4;  // vectors in flight per thread (other kernels)
+
+template <class V, int MODE, int XLD = 0, int UNR = 4>  // MODE 0 stream, 1 gather, 2 gather with hot smem (~slot), 3 hot = col < nh (relabeled)
 __global__ void __launch_bounds__(1024) k_gather(const V* __restrict__ val, const int32_t* __restrict__ col,
                                                  const V* __restrict__ x, const V* __restrict__ xh, int nh,
                                                  int64_t nnz, double* out) {
@@ -369,6 +370,32 @@ int gr_launch_x(int dtype, int mode, int xld, const void* val, const int32_t* co
 #undef LXV
 #undef LXM
 #undef LX
+  return (int)cudaGetLastError();
+}
+// hot-x gathers (mode 2, .cg) with UNR vectors in flight per thread (1, 2, 4, 8): how the
+// gather rate depends on the loads a thread keeps in flight
+int gr_launch_unr(int dtype, int unr, const void* val, const int32_t* col, const void* x, const void* xh, int nh,
+                  int64_t nnz, double* out, int grid, int tpb, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t sm = (size_t)nh * (dtype ? 8 : 4);
+#define LU(V, U)                                                                                                \
+  do {                                                                                                          \
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_gather<V, 2, 2, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             (int)sm);                                                          \
+    k_gather<V, 2, 2, U><<<grid, tpb, sm, s>>>((const V*)val, col, (const V*)x, (const V*)xh, nh, nnz, out);    \
+  } while (0)
+  if (dtype == 0) {
+    if (unr == 1) LU(float, 1);
+    else if (unr == 2) LU(float, 2);
+    else if (unr == 8) LU(float, 8);
+    else LU(float, 4);
+  } else {
+    if (unr == 1) LU(double, 1);
+    else if (unr == 2) LU(double, 2);
+    else if (unr == 8) LU(double, 8);
+    else LU(double, 4);
+  }
+#undef LU
   return (int)cudaGetLastError();
 }
 // cp.async-staged gathers (mode 5): ch = chunk elements (8 or 16), nh hot columns in smem

@@ -44,6 +44,7 @@ def build():
     lib.gr_launch_x.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
                                 ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+    lib.gr_launch_unr.argtypes = lib.gr_launch_x.argtypes[:1] + lib.gr_launch_x.argtypes[2:]
     lib.gr_launch_hash.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                    ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
     return lib
@@ -100,6 +101,8 @@ def main():
                          "2 .cg, 3 L1::evict_first, 4 .nc without L2 policy) and hot-x copies up to --xld-hot-max")
     ap.add_argument("--xld-hot", nargs="+", type=int, default=[0, 24576, 32768, 40960, 49152])
     ap.add_argument("--xld-tpb", nargs="+", type=int, default=[1024])
+    ap.add_argument("--unr", nargs="+", type=int, default=[],
+                    help="also time hot-x .cg gathers with 1/2/4/8 vectors in flight per thread (--xld-hot sizes)")
     args = ap.parse_args()
     import torch
     lib = build()
@@ -176,6 +179,23 @@ def main():
                                       "tpb": tpb, "grid": grid, "hot_cover": cover, "median_us": med * 1e3,
                                       "min_us": mn * 1e3, "model_gbs": model / (med * 1e-3) / 1e9,
                                       "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
+                del denc
+        for unr in args.unr:
+            for K in [k for k in args.xld_hot if k]:
+                hot = order[:K]
+                slot = np.full(n, -1, np.int64)
+                slot[hot] = np.arange(K)
+                denc = torch.from_numpy(np.where(slot[col] >= 0, ~slot[col], col).astype(np.int32)).to(dev)
+                xh = x[torch.from_numpy(hot).to(dev)].contiguous()
+
+                def runu():
+                    rc = lib.gr_launch_unr(dt, unr, dval.data_ptr(), denc.data_ptr(), x.data_ptr(), xh.data_ptr(), K,
+                                           nnz, out.data_ptr(), nsm, 1024, s)
+                    assert rc == 0, rc
+                med, mn = timeit(runu, args.reps, flush)
+                print(json.dumps({**base, "kernel": f"gather_cg_unr{unr}_hot{K}", "unr": unr, "hot": K,
+                                  "in_flight_per_thread": unr * (4 if dt == 0 else 2), "median_us": med * 1e3,
+                                  "min_us": mn * 1e3, "gathers_per_s": nnz / (med * 1e-3)}), flush=True)
                 del denc
         if args.dsm:
             for (csize, kl) in [(1, 24576), (2, 24576), (4, 24576), (8, 24576), (2, 16384), (4, 16384), (8, 16384),
