@@ -392,6 +392,26 @@ __device__ __forceinline__ void batch_use(const DevPart& p, V* y, XA xa, const B
   }
 }
 
+// AS_L1_PREFETCH (A/B build knob): request the next batch's value / column lines into L1
+// while the current batch waits on its gathers, so the batch's loads hit L1 instead of
+// exposing the HBM latency (the prefetch issues the same L1->L2 requests the loads would).
+#ifndef AS_L1_PREFETCH
+#define AS_L1_PREFETCH 0
+#endif
+template <class V, bool PAD, int VEC, int KB>
+__device__ __forceinline__ void batch_prefetch_l1(const V* pv, const int32_t* pc, int64_t stride) {
+  if constexpr (PAD) {
+#pragma unroll
+    for (int q = 0; q < KB; q += VEC) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(pv + (q / VEC) * stride));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(pc + (q / VEC) * stride));
+    }
+  } else {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(pv));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(pc));
+  }
+}
+
 // One BMT in predicated-emit form: rows closed inside the BMT are stored in the loop; the
 // caller gets the straddling first segment (`first`, valid when !s0 && inside), the open last
 // segment (`acc`, of row `row`), and whether the BMT starts at a row head (s0) / holds a
@@ -429,6 +449,8 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   int32_t c[KB];
   for (; j0 < full; j0 += KB, pv += adv, pc += adv) {
     batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, j0, len, v, c);
+    if constexpr (AS_L1_PREFETCH)
+      if (j0 + KB < len) batch_prefetch_l1<V, PAD, VEC, KB>(pv + adv, pc + adv, pp.stride);
     batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
   }
   if (j0 < len) {
