@@ -88,6 +88,12 @@ def test_random_graphs(seed):
     "COMPRESS; BMW_NNZ_BLOCK(64); BMT_NNZ_BLOCK(2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; GMEM_ATOM_RED",
     "COMPRESS; BMTB_NNZ_BLOCK(32); SHMEM_OFFSET_RED; GMEM_ATOM_RED",
     "COL_DIV(cuts=[5000,10000,20000]) { COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
+    # R-conc: the hub row's partials come from side-stream parts too (their atomic rows go to
+    # the fp64 heavy-row scratch, their stores to their own scratch vectors)
+    "COL_DIV(cuts=[5000,10000,20000]) { COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; GMEM_ATOM_RED"
+    " | COMPRESS; BMT_NNZ_BLOCK(8); THREAD_BITMAP_RED_G; SET_RESOURCE(stream=1); GMEM_ATOM_RED"
+    " | COMPRESS; BMW_NNZ_BLOCK(64); BMT_NNZ_BLOCK(2); THREAD_BITMAP_RED_G; WARP_SEG_ADD_RED; SET_RESOURCE(stream=2); GMEM_ATOM_RED"
+    " | COMPRESS; BMTB_NNZ_BLOCK(32); SHMEM_OFFSET_RED; SET_RESOURCE(stream=3); GMEM_ATOM_RED }",
 ])
 def test_fp32_heavy_rows(graph):
     """A25: an fp32 hub row split over thousands of writer units must stay within 1e-5 of
