@@ -151,7 +151,10 @@ void as_plan_destroy(as_plan_t);
  * aligned to the value size, non-aliasing (a ROW_DIV band may write into a slice of a
  * larger y); alpha/beta point to HOST scalars of the plan's dtype.
  * beta == 0: y is write-only (NaN in y not propagated).  Asynchronous on `stream`;
- * device faults surface as AS_ERR_CUDA at a later call. */
+ * device faults surface as AS_ERR_CUDA at a later call.  Parts whose SET_RESOURCE names
+ * another stream than the first part's (DESIGN.md R-conc) run on plan-owned side streams
+ * forked from `stream` after the beta pre-pass and joined back into it before the call's
+ * last launch, so the call stays ordered on `stream` (also under CUDA-graph capture). */
 as_status_t as_spmv(as_plan_t, const void* alpha, const void* x, const void* beta, void* y,
                     void* stream);
 /* Same with HOST x[n] / y[m] (pinned for overlap; pageable works): copies x (and y when
@@ -160,7 +163,8 @@ as_status_t as_spmv(as_plan_t, const void* alpha, const void* x, const void* bet
  * column chunks on a plan-owned copy stream, launch i waits only for the chunk holding the
  * last column it reads, and each y row range no later launch writes goes down on a second
  * copy stream once its last writer is done (PCIe is full duplex).  Not pipelined: a single
- * launch, fp32 plans with heavy rows, or AS_HOST_NOPIPE set in the environment.  The
+ * launch, fp32 plans with heavy rows, plans with concurrent branches (R-conc), or
+ * AS_HOST_NOPIPE set in the environment.  The
  * result is identical either way (same kernels, same order on the device). */
 as_status_t as_spmv_host(as_plan_t, const void* alpha, const void* x_host, const void* beta,
                          void* y_host, void* stream);
@@ -168,8 +172,10 @@ as_status_t as_spmv_host(as_plan_t, const void* alpha, const void* x_host, const
  * streams: calls on the same plan must not run concurrently from several host threads.)
  * k independent SpMVs y_i = alpha*A*x_i + beta*y_i on host buffers (pinned for overlap),
  * pipelined across i: x_{i+1} is copied up while SpMV i runs and y_{i-1} is copied down
- * (two device buffer pairs, two copy streams); every x_i goes up and every y_i comes back.
- * Blocking; the steady state per SpMV is max(H2D x, kernels, D2H y).  Same errors as
+ * (two device buffer pairs, two copy streams; x buffer j is reused once SpMV i-2 read it,
+ * y buffer j once y_{i-2} came down, so both directions run at once); every x_i goes up and
+ * every y_i comes back.  Blocking; the steady state per SpMV is max(H2D x, kernels,
+ * D2H y) with both copy directions sharing the link.  Same errors as
  * as_spmv_host. */
 as_status_t as_spmv_host_batch(as_plan_t, int64_t k, const void* alpha, const void* const* x_host,
                                const void* beta, void* const* y_host, void* stream);
@@ -190,7 +196,8 @@ as_status_t as_spmm(as_plan_t, int64_t k, const void* alpha, const void* X, int6
  * as_plan_info_t.kernels ([pre-pass], parts in launch order, [heavy-row epilogue]), the mean
  * device time in ms and the entry's algorithmic bytes under the plan's model (arrays read
  * + x of the part's distinct columns + its y traffic; beta == 0).  ms == NULL or bytes ==
- * NULL -> *n = number of entries.  Overwrites y. */
+ * NULL -> *n = number of entries.  Overwrites y.  Concurrent branches (R-conc) are
+ * profiled serialised on `stream` (same result; per-launch times of each kernel alone). */
 as_status_t as_plan_profile(as_plan_t, const void* x, void* y, int reps, void* stream,
                             double* ms, double* bytes, size_t* n);
 

@@ -13,7 +13,7 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 import paper_2212_10432_b200 as asp  # noqa: E402
 from oracle import spmv as S  # noqa: E402
-from test_host import FAMILY_GRAPHS  # noqa: E402
+from test_host import CONC_GRAPHS, FAMILY_GRAPHS  # noqa: E402
 
 EXTRA = [
     "DIA_DECOM(theta=0.5,max=8) { DIA | COMPRESS; BMT_NNZ_BLOCK(3); THREAD_BITMAP_RED_G; GMEM_ATOM_RED }",
@@ -27,7 +27,7 @@ EXTRA = [
 
 def main():
     fails = 0
-    cases = [(synth.random_powerlaw(900, 800, 3, 300), FAMILY_GRAPHS + EXTRA[:3]),
+    cases = [(synth.random_powerlaw(900, 800, 3, 300), FAMILY_GRAPHS + EXTRA[:3] + CONC_GRAPHS),
              (synth.c5_band_csr(m=1 << 19, nnz=1 << 23, band=512).to_coo(), EXTRA[3:])]  # x-window form
     for coo, graphs in cases:
         A = asp.Matrix.from_coo(coo.m, coo.n, coo.row, coo.col, coo.val)
