@@ -156,8 +156,10 @@ Plan* make_plan(const Matrix& A, const Seq& g, const std::string& canon, int dev
     info.nnz_real = A.nnz();
     info.n_parts = (int64_t)P->host.parts.size();
     info.prepass_rows = (int64_t)P->host.prepass.size();
+    int64_t side_adds = 0;  // R-conc: one k_side_add per side-stream part after the join
+    for (void* ys : P->side_y) side_adds += ys != nullptr;
     info.n_launches = (int64_t)P->host.launch_order.size() + (P->host.prepass.empty() ? 0 : 1) +
-                      (P->n_heavy ? 1 : 0);  // heavy-row epilogue (the scratch memset is a copy op)
+                      (P->n_heavy ? 1 : 0) + side_adds;  // heavy-row epilogue (the scratch memset is a copy op)
     int64_t slots = 0;
     for (auto& p : P->host.parts) {
       if (p.kind == "csr") slots += p.pad ? (int64_t)p.pad_val.size() : (int64_t)p.val.size();

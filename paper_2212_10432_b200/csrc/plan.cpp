@@ -789,6 +789,14 @@ void Plan::compute_model() {
   for (int64_t pi : host.launch_order) {
     const HostPart& h = host.parts[pi];
     double ex = (double)h.excl.size(), at = (double)h.atom.size();
+    if (h.mode == 3) {
+      // R-conc side part: STOREs (and atomics onto zeroed rows) into its scratch, then
+      // k_side_add reads each written row's scratch value and updates y
+      const double t = ex * sv + at * (4 + 3 * sv) + (ex + at) * (4 + 3 * sv);
+      ybytes0 += t;
+      ybytes1 += t;
+      continue;
+    }
     if (h.mode == 0) {
       ybytes0 += ex * sv;
       ybytes1 += 2 * ex * sv;
@@ -816,7 +824,7 @@ void Plan::compute_model() {
         xc = spans[i].chi - spans[i].clo + 1;
       }
       const double ex = (double)h.excl.size(), at = (double)h.atom.size();
-      launch_bytes[i] += (double)xc * sv + (h.mode == 0 ? ex * sv : 2 * ex * sv) + 2 * at * sv;
+      launch_bytes[i] += (double)xc * sv + (h.mode == 0 || h.mode == 3 ? ex * sv : 2 * ex * sv) + 2 * at * sv;
     }
   }
   double pre = (double)host.prepass.size();
