@@ -214,16 +214,8 @@ int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s
     const int k = P.launch_stream[i];
     return (P.concurrent && k != P.main_stream) ? P.side[k] : s;
   };
-  if (P.concurrent && !err) {
-    for (size_t i = 0; i < P.launches.size() && !err; ++i) {
-      const int k = P.launch_stream[i];
-      if (k != P.main_stream && !P.side[k]) {
-        err = (int)cudaStreamCreateWithFlags(&P.side[k], cudaStreamNonBlocking);
-        if (!err) err = (int)cudaEventCreateWithFlags(&P.ev_join[k], cudaEventDisableTiming);
-      }
-    }
-    if (!P.ev_fork && !err) err = (int)cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming);
-    if (!err) err = (int)cudaEventRecord(P.ev_fork, s);
+  if (P.concurrent && !err) {  // side streams / events: created by Plan::upload
+    err = (int)cudaEventRecord(P.ev_fork, s);
     for (int k = 0; k < 4 && !err; ++k)
       if (P.side[k]) err = (int)cudaStreamWaitEvent(P.side[k], P.ev_fork, 0);
   }

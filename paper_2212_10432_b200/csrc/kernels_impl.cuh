@@ -132,6 +132,10 @@ __global__ void __launch_bounds__(1024) k_thread_row_pad(DevPart p, const V* __r
 // next to the warp-combine state; fp32 operands stay fp32 in registers until the FMA, so
 // fp32 affords 8 gathers in flight per lane at 64 registers (C3 winner family: 924.7 ->
 // 885.7 us; 16 spills 120-184 bytes and is slower, 949 us; profiles/r02/ab_kb.jsonl).
+// AS_NWPE_LB (A/B build knob): launch bound of k_nnz_warp_pe (its register budget)
+#ifndef AS_NWPE_LB
+#define AS_NWPE_LB 1024
+#endif
 #ifndef AS_KBW_F32
 #define AS_KBW_F32 8
 #endif
@@ -739,7 +743,7 @@ __global__ void __launch_bounds__(1024) k_nnz_warp(DevPart p, const V* __restric
 // inside the BMT stored by one predicated store, no divergent writer calls), then the same
 // warp combine of (cin, cout, head flag) as above.  Same writes as k_nnz_warp.
 template <class V, int WRED, bool PAD, int VEC, int KB, int EM, bool XH>
-__global__ void __launch_bounds__(1024) k_nnz_warp_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
+__global__ void __launch_bounds__(AS_NWPE_LB) k_nnz_warp_pe(DevPart p, const V* __restrict__ x, V* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   extern __shared__ __align__(128) unsigned char xh_smem[];
   if constexpr (XH) xhot_fill(p, x, (V*)xh_smem);

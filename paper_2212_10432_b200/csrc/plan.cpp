@@ -721,6 +721,16 @@ void Plan::upload(cudaStream_t s) {
   }
   main_stream = launch_stream.empty() ? 0 : launch_stream[0];
   for (int k : launch_stream) concurrent = concurrent || k != main_stream;
+  // side streams and fork/join events are created here, once, so concurrent as_spmv calls on
+  // the plan never race on creating them
+  if (concurrent) {
+    for (int k : launch_stream)
+      if (k != main_stream && !side[k]) {
+        ck(cudaStreamCreateWithFlags(&side[k], cudaStreamNonBlocking), "side stream");
+        ck(cudaEventCreateWithFlags(&ev_join[k], cudaEventDisableTiming), "join event");
+      }
+    ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "fork event");
+  }
   const size_t L = launches.size();
   side_y.assign(L, nullptr);
   side_rows.assign(L, nullptr);

@@ -53,7 +53,7 @@ struct Plan {
   cudaEvent_t host_event(size_t i);
   // R-conc: per launch its SET_RESOURCE stream.  Launches naming the first launch's stream
   // run on the caller's stream; the others (side parts, writer mode 3) on side stream k
-  // (created lazily), forked after the pre-pass and joined before the epilogues.  A side
+  // (created by upload), forked after the pre-pass and joined before the epilogues.  A side
   // part writes its own scratch vector side_y (its atomic rows zeroed first), whose rows
   // side_rows are added into y after the join (k_side_add).
   std::vector<int> launch_stream;
