@@ -28,6 +28,7 @@ from __future__ import annotations
 import argparse
 import ctypes
 import json
+import re
 import os
 import statistics
 import subprocess
@@ -280,7 +281,7 @@ def dominant_of(P, dx, dy, timer, npass):
     return {"kernel": name, "ms": dms, "bytes": dby, "launches": [{"kernel": n, "ms": ms, "bytes": by} for n, ms, by in per]}
 
 
-def gather_roofline(torch, coo, dx, timer, reps):
+def gather_roofline(torch, coo, dx, timer, reps, hot_k=0):
     """tools/gather_roofline.cu on this matrix's own (val, col) arrays in CSR order: stream
     every pair once and gather x[col] (no reduction, no y).  Returns the median time."""
     here = os.path.join(ROOT, "tools")
@@ -307,8 +308,34 @@ def gather_roofline(torch, coo, dx, timer, reps):
     for _ in range(3):
         run()
     ms = statistics.median(timer.steps(run, reps))
+    hot = None
+    if hot_k:
+        # the same gathers with the plan's hot-x copy in shared memory and the rest read at L2
+        # only (.cg), the kernel's own access pattern without the reduction: the request-rate
+        # ceiling of this matrix
+        lib.gr_launch_x.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
+                                    ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        cnt = np.bincount(coo.col, minlength=coo.n)
+        order = np.argsort(-cnt, kind="stable")[:hot_k]
+        slot = np.full(coo.n, -1, np.int64)
+        slot[order] = np.arange(hot_k)
+        sl = slot[coo.col]
+        denc = torch.from_numpy(np.where(sl >= 0, ~sl, coo.col).astype(np.int32)).cuda()
+        del sl
+        xh = dx[torch.from_numpy(order).cuda()].contiguous()
+
+        def run_hot():
+            rc = lib.gr_launch_x(dt, 2, 2, dval.data_ptr(), denc.data_ptr(), dx.data_ptr(), xh.data_ptr(), hot_k,
+                                 coo.nnz, out.data_ptr(), nsm, 1024, s)
+            assert rc == 0, rc
+        for _ in range(3):
+            run_hot()
+        hot = {"ms": statistics.median(timer.steps(run_hot, reps)), "hot": hot_k,
+               "cover": float(cnt[order].sum()) / coo.nnz}
+        del denc, xh
     del dcol, dval
-    return ms
+    return ms, hot
 
 
 def run_config(args, torch, asp, name, A, coo, wl, seeds, graph, search, local, timer, with_e2e, budget):
@@ -447,12 +474,19 @@ def single_gpu(args, torch, asp):
     gr = None
     if not args.no_gather and name in ("c3", "c4", "c5", "c3s", "c5s"):
         try:
-            gms = gather_roofline(torch, coo, dx, timer, max(5, args.steps // 2))
+            m_hot = re.search(r"xcache=(\d+)", head["graph"])
+            gms, hot = gather_roofline(torch, coo, dx, timer, max(5, args.steps // 2),
+                                       int(m_hot.group(1)) if m_hot else 0)
             dk = head["roofline"]["dominant"]
             gr = {"ms": gms, "achieved_gbs": head["bytes_model"] / (gms * 1e-3) / 1e9,
                   "frac_step": gms / head["ms_per_step"], "frac_dominant": gms / dk["ms"] if dk["ms"] else None,
                   "note": "time to stream every (val, col) pair once and gather x[col] (no reduction, no y), "
                           "CSR order, same x, L2 flushed: frac = gather time / SpMV time"}
+            if hot:
+                gr["hot_cg"] = {**hot, "frac_step": hot["ms"] / head["ms_per_step"],
+                                "note": "same stream and gathers with the plan's xcache hot columns read from shared "
+                                        "memory and the rest at L2 only (.cg): the L1->L2 request-rate ceiling of "
+                                        "this access pattern (DESIGN.md section 4)"}
         except Exception as e:  # the measurement tool is optional; the SpMV numbers stand
             gr = {"error": str(e)[:200]}
     head["roofline"]["gather"] = gr

@@ -241,11 +241,12 @@ int run_plan(Plan& P, const void* x, void* y, double a, double b, cudaStream_t s
     if (!err) err = launch_part(d, x, yd, on(i));
     if (!err) after(i);
   }
-  if (P.concurrent)
-    for (int k = 0; k < 4 && !err; ++k)
+  if (P.concurrent)  // joined even after a failed launch: nothing queued on a side stream outlives the call's order
+    for (int k = 0; k < 4; ++k)
       if (P.side[k]) {
-        err = (int)cudaEventRecord(P.ev_join[k], P.side[k]);
-        if (!err) err = (int)cudaStreamWaitEvent(s, P.ev_join[k], 0);
+        int e = (int)cudaEventRecord(P.ev_join[k], P.side[k]);
+        if (!e) e = (int)cudaStreamWaitEvent(s, P.ev_join[k], 0);
+        if (!err) err = e;
       }
   for (size_t i = 0; i < P.side_y.size() && !err; ++i)
     if (P.side_y[i]) err = launch_side_add(P.side_rows[i], P.n_side_rows[i], P.side_y[i], y, dtype, s);
