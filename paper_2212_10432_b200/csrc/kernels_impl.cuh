@@ -377,10 +377,18 @@ struct BmWords {
   }
 };
 
-template <class V, int KB, int EM, bool FULL, class XA, class BW>
+// AS_F32_ACC (A/B build knob): fp32 data accumulate each lane's BMT segment in fp32 (FFMA)
+// instead of fp64; a segment holds at most k products, so its rounding error is at most
+// k * 2^-24 * sum|a x| (k = 32: 1.9e-6, inside the north_star fp32 tolerance of 1e-5)
+#ifndef AS_F32_ACC
+#define AS_F32_ACC 0
+#endif
+template <class V>
+using AccOf = std::conditional_t<AS_F32_ACC && sizeof(V) == 4, float, double>;
+template <class V, int KB, int EM, bool FULL, class XA, class BW, class A>
 __device__ __forceinline__ void batch_use(const DevPart& p, V* y, XA xa, const BW& bm, int j0, int len,
-                                          const V* v, const int32_t* c, int32_t& row, double& acc, bool& inside,
-                                          double& first) {
+                                          const V* v, const int32_t* c, int32_t& row, A& acc, bool& inside,
+                                          A& first) {
   V xv[KB];
 #pragma unroll
   for (int q = 0; q < KB; ++q) xv[q] = (FULL || j0 + q < len) ? xa.v(c[q]) : (V)0;
@@ -388,11 +396,11 @@ __device__ __forceinline__ void batch_use(const DevPart& p, V* y, XA xa, const B
 #pragma unroll
   for (int q = 0; q < KB; ++q) {
     const bool h = (FULL || j0 + q < len) && ((wd >> q) & 1u);
-    emit_excl<V, EM>(p, y, h && inside, row, acc);
+    emit_excl<V, EM>(p, y, h && inside, row, (double)acc);
     first = (h && !inside) ? acc : first;
     row += h ? 1 : 0;
     inside = inside || h;
-    acc = (h ? 0.0 : acc) + (double)v[q] * (double)xv[q];
+    acc = (h ? (A)0 : acc) + (A)v[q] * (A)xv[q];
   }
 }
 
@@ -443,8 +451,7 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
   o.s0 = (BMO ? bm.w0 : ldm(bmp)) & 1u;
   o.inside = o.s0;
   o.row = (int32_t)bmt_row0(p, t);  // device row indices are int32 (A36)
-  o.acc = 0.0;
-  o.first = 0.0;
+  AccOf<V> acc = 0, first = 0;
   const int full = len & ~(KB - 1);
   int j0 = 0;
   // pv / pc advance to the batch's first element (slot-major: KB/VEC chunk rows per batch)
@@ -455,12 +462,14 @@ __device__ __forceinline__ ScanPE bmt_scan_pe(const DevPart& p, V* y, XA xa, int
     batch_load<V, PAD, VEC, KB, true>(pv, pc, pp.stride, j0, len, v, c);
     if constexpr (AS_L1_PREFETCH)
       if (j0 + KB < len) batch_prefetch_l1<V, PAD, VEC, KB>(pv + adv, pc + adv, pp.stride);
-    batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
+    batch_use<V, KB, EM, true>(p, y, xa, bm, j0, len, v, c, o.row, acc, o.inside, first);
   }
   if (j0 < len) {
     batch_load<V, PAD, VEC, KB, false>(pv, pc, pp.stride, j0, len, v, c);
-    batch_use<V, KB, EM, false>(p, y, xa, bm, j0, len, v, c, o.row, o.acc, o.inside, o.first);
+    batch_use<V, KB, EM, false>(p, y, xa, bm, j0, len, v, c, o.row, acc, o.inside, first);
   }
+  o.acc = (double)acc;
+  o.first = (double)first;
   return o;
 }
 
