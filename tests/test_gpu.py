@@ -558,3 +558,18 @@ def test_concurrent_dense_beside_residual_c4_shape():
         yref, _ = S.spmv_coo(coo.m, coo.row, coo.col, coo.val.astype(np.float64), x.astype(np.float64), 1.0, 1.0,
                              y0.astype(np.float64))
         assert np.array_equal(out[0], out[1]) and np.array_equal(out[1].astype(np.float64), yref)
+
+
+def test_concurrent_dia_side_part():
+    """R-conc with a DIA part on the side stream: ROW_DIV puts the DIA band (1024 rows) beside
+    the larger CSR band, which leads the launch order and so is the main stream; the DIA rows
+    are pre-passed and added from the DIA part's scratch after the join (integer mode,
+    bit-identical to the oracle)."""
+    coo = synth.c2_lap2d(64)
+    ints = np.where(coo.val > 0, 4.0, -1.0)
+    coo = synth.Coo(coo.m, coo.n, coo.row, coo.col, ints)
+    g = ("ROW_DIV(cuts=[1024]) { DIA_DECOM(theta=0.5,max=8) { DIA; SET_RESOURCE(stream=1) } | "
+         "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED }")
+    P, _ = run_check(coo, g, 2.0, -1.0, int_mode=True, seed=4, keep_host=True)
+    assert P.export("mode").tolist() == [3, 0]
+    assert P.export("prepass").tolist() == list(range(1024))

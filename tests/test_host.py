@@ -438,3 +438,14 @@ def test_matrix_features():
     want = [np.log2(1 + coo.m), np.log2(1 + coo.n), np.log2(1 + L.sum()), L.mean(), np.log2(1 + L.var()),
             np.log2(1 + L.max()), float((L == 0).mean()), 4.0]
     assert np.allclose(A.features(), want, rtol=1e-12, atol=1e-12)
+
+
+def test_conc_dia_side_part_export():
+    """R-conc with the DIA part beside a CSR band (the CSR band leads the launch order): the
+    C++ writer rule (modes, pre-pass) and every exported array equal the oracle's."""
+    coo = synth.c2_lap2d(16)
+    g = ("ROW_DIV(cuts=[64]) { DIA_DECOM(theta=0.5,max=8) { DIA; SET_RESOURCE(stream=1) } | "
+         "COMPRESS; BMT_ROW_BLOCK(1); THREAD_TOTAL_RED; GMEM_ATOM_RED }")
+    P = asp.Plan(_mat(coo), g, device=-1, keep_host=True)
+    assert P.export("mode").tolist() == [3, 0] and P.export("prepass").tolist() == list(range(64))
+    assert compare_export(P, coo, g)
