@@ -388,11 +388,13 @@ def run_config(args, torch, asp, name, A, coo, wl, seeds, graph, search, local, 
     r["roofline"]["traffic"] = None
     if os.path.exists(prof):
         try:
-            tj = json.load(open(prof))
-            same = tj.get("graph", graph) == graph or ("bytes_model" in tj and tj["bytes_model"] == info["bytes_model"])
-            if tj.get("kernels") == info["kernels"] and same:
-                r["roofline"]["traffic"] = tj["dram_bytes_per_launch"]
-                r["roofline"]["traffic_src"] = tj.get("src")
+            tjs = json.load(open(prof))
+            for tj in (tjs if isinstance(tjs, list) else [tjs]):  # one capture per graph shape
+                same = tj.get("graph", graph) == graph or ("bytes_model" in tj and tj["bytes_model"] == info["bytes_model"])
+                if tj.get("kernels") == info["kernels"] and same:
+                    r["roofline"]["traffic"] = tj["dram_bytes_per_launch"]
+                    r["roofline"]["traffic_src"] = tj.get("src")
+                    break
         except Exception:
             pass
     if with_e2e:
