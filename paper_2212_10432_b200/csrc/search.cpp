@@ -310,7 +310,10 @@ std::string mutate_graph(const Seq& g0, Rng& r) {
   else if (k == "grid") step({0, 1, 2, 4, 8, 16});
   else if (k == "stages") v.i = v.i ? 0 : 2;
   else if (k == "xcache") step({0, 4096, 8192, 16384, 24576, 32768});
-  else if (k == "stream") v.i = v.i ? 0 : 1;  // R-conc: this branch beside / after the others
+  else if (k == "stream") {  // R-conc: this branch beside / after the others (branching graphs only)
+    if (print_graph(g0).find('{') == std::string::npos) return "";
+    v.i = v.i ? 0 : 1;
+  }
   else if (k == "vec") step({0, 1, 2, 4});
   else if (k == "max") step({4, 8, 16, 32});
   else if (k == "b") step({16, 32, 64, 128});
